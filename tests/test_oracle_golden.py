@@ -1,0 +1,80 @@
+"""Pin the CPU oracle against the reference's own outputs (tests/golden)."""
+
+import numpy as np
+import pytest
+
+import golden_io
+from oracle import search_oracle as so
+
+
+@pytest.fixture(scope="module", params=golden_io.NAMES)
+def fx(request):
+    return golden_io.load(request.param)
+
+
+def test_oracle_reproduces_reference(fx):
+    for run in golden_io.exact_runs(fx):
+        p = so.Params(**vars(run.params))
+        for qi, q in enumerate(fx.queries):
+            ids, d, st = so.search_one(fx.index, q, p)
+            want_ids, want_d = run.results[qi]
+            assert tuple(run.stats[qi]) == st, (fx.name, vars(run.params), qi)
+            np.testing.assert_array_equal(ids, want_ids)
+            # same numpy calls: equal to float32 rounding of SIMD-order LUTs
+            np.testing.assert_allclose(d, want_d, rtol=1e-6, atol=1e-6)
+
+
+def test_code_sums_is_pairwise8():
+    rng = np.random.default_rng(0)
+    for m in (8, 16):
+        lut = rng.standard_normal((m, 256)).astype(np.float32)
+        codes = rng.integers(0, 256, (5000, m)).astype(np.uint8)
+        np.testing.assert_array_equal(so.code_sums(lut, codes), so.code_sums_pairwise8(lut, codes))
+
+
+def test_ranges_to_rows_matches_loop():
+    rng = np.random.default_rng(1)
+    starts = rng.integers(0, 1000, 50)
+    lens = rng.integers(0, 7, 50)
+    want = np.concatenate([np.arange(s, s + n) for s, n in zip(starts, lens)])
+    np.testing.assert_array_equal(so.ranges_to_rows(starts, lens), want)
+
+
+def test_topk_is_prefix_of_full(fx):
+    run = golden_io.exact_runs(fx)[0]
+    if not run.params.rerank:
+        pytest.skip("scan-order run")
+    p = so.Params(**vars(run.params))
+    nq = min(6, fx.queries.shape[0])
+    ids, d, st = so.search_topk(fx.index, fx.queries[:nq], p, k=25)
+    for qi in range(nq):
+        want_ids, want_d = run.results[qi]
+        n = min(25, want_ids.shape[0])
+        np.testing.assert_array_equal(ids[qi, :n], want_ids[:n])
+        assert np.all(ids[qi, n:] == -1)
+
+
+def test_param_messages(fx):
+    q = fx.queries[0]
+    k = fx.index.centroids.shape[0]
+    for kw, msg in [(dict(nprobe=0), "nprobe"), (dict(nprobe=k + 1), "nprobe"),
+                    (dict(tau=0.0), "tau"), (dict(tau=1.5), "tau"),
+                    (dict(candidates=0), "candidates"), (dict(ef_search=0), "ef_search")]:
+        with pytest.raises(ValueError, match=msg):
+            so.search_one(fx.index, q, so.Params(**kw))
+    with pytest.raises(ValueError, match="query dim"):
+        so.search_one(fx.index, q[:-1], so.Params())
+
+
+@pytest.mark.parametrize("shards", [2, 3])
+def test_sharded_oracle_equals_unsharded(shards):
+    fx = golden_io.load("c1like_m8")
+    p = so.Params(nprobe=32, tau=0.5, candidates=3000)
+    want_i, want_d, want_s = so.search_topk(fx.index, fx.queries[:8], p, k=50)
+    parts = [so.shard_index(fx.index, g, shards) for g in range(shards)]
+    outs = [so.search_shard_topk(s, fx.queries[:8], p, k=50) for s in parts]
+    for o in outs:
+        np.testing.assert_array_equal(o[2], want_s)
+    got_i, got_d = so.merge_topk([o[0] for o in outs], [o[1] for o in outs], 50)
+    np.testing.assert_array_equal(got_i, want_i)
+    np.testing.assert_array_equal(got_d, want_d)
