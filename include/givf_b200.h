@@ -1,0 +1,134 @@
+/*
+ * givf_b200 -- C ABI of the B200-native search path for the grouped inverted
+ * index of arXiv 1802.02422 (reference package `givf`).
+ *
+ * Plain pointers and sizes only.  Every pointer argument of a search call may
+ * be host memory or device memory (detected per call); the index arrays of
+ * givf_index_create are always host memory and are copied to the device.
+ *
+ * The entry points replace these reference interfaces
+ * (paths under /root/reference/pkg/src/givf/):
+ *   givf_index_create    GroupedIndex (index.py:48-85) as produced by
+ *                        build_index (index.py:249-380) / load_index
+ *                        (storage.py:162-281): the read-only search input.
+ *   givf_search_full     search(index, query, params) (search.py:93-163),
+ *                        batched: every scanned code, reranked by (dist, id)
+ *                        (rerank=True, search.py:156-158) or in scan order
+ *                        with group scores (rerank=False, search.py:159-161).
+ *   givf_search_topk     the first k entries of search()'s reranked list
+ *                        (BASELINE.json k=100; recall_at_r search.py:186-201
+ *                        reads only ids[:R]).
+ *   givf_probe           _select_regions (search.py:77-90) at
+ *                        ef_search == K, i.e. the exact region ranking.
+ *   givf_merge_topk      no reference counterpart (single process): merge
+ *                        of per-shard top-k lists, SURVEY §8e.
+ *
+ * Status codes: GIVF_OK, GIVF_EINVAL (bad argument: givf_last_error() holds
+ * the reference's ValueError text, e.g. "need 1 <= nprobe <= 48, got 0"),
+ * GIVF_ECUDA, GIVF_ENOMEM, GIVF_EINVARIANT.
+ */
+#ifndef GIVF_B200_H
+#define GIVF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GIVF_OK 0
+#define GIVF_EINVAL 1
+#define GIVF_ECUDA 2
+#define GIVF_ENOMEM 3
+#define GIVF_EINVARIANT 4
+
+typedef struct givf_index* givf_index_t;
+
+/* Flat arrays of a GroupedIndex (index.py:48-62).  For a shard of a
+ * multi-GPU layout the row arrays (point_ids, codes,
+ * const_bytes, region_offsets) hold only this shard's rows, `group_sizes` is
+ * the replicated GLOBAL table that drives the budget walk, and
+ * local_sizes / local_lo give, per (region, group) slice, how many rows this
+ * shard holds and the first global slot it owns.  Both NULL = unsharded. */
+typedef struct givf_index_desc {
+  int32_t k;               /* regions */
+  int32_t dim;             /* vector dimension */
+  int32_t groups;          /* groups per region: L, or 1 when grouping is off */
+  int32_t m;               /* PQ sub-quantizers (code bytes per point) */
+  int32_t grouping;        /* 1 = grouped index (neighbor_ids/norm_terms set) */
+  int64_t n;               /* rows stored (in this shard) */
+  const float* centroids;      /* (k, dim) */
+  const float* alphas;         /* (k) */
+  const int32_t* neighbor_ids; /* (k, groups) or NULL */
+  const float* norm_terms;     /* (k, groups) or NULL */
+  const int32_t* group_sizes;  /* (k, groups) */
+  const int64_t* region_offsets; /* (k + 1) row offsets */
+  const int32_t* local_sizes;  /* (k, groups) or NULL */
+  const int32_t* local_lo;     /* (k, groups) or NULL */
+  const int32_t* point_ids;    /* (n) */
+  const uint8_t* codes;        /* (n, m) */
+  const uint8_t* const_bytes;  /* (n) */
+  const float* codewords;      /* (m, 256, dim / m) */
+  const float* rotation;       /* (dim, dim) or NULL */
+  double const_lo;             /* ConstQuantizer bounds (grouping.py:100-129) */
+  double const_hi;
+} givf_index_desc;
+
+/* SearchParams (search.py:23-30). */
+typedef struct givf_search_params {
+  int32_t nprobe;
+  double tau;
+  int64_t candidates;
+  int32_t ef_search;   /* validated like the reference; the probe is exact */
+  int32_t rerank;
+  int32_t prune;
+} givf_search_params;
+
+/* SearchStats (search.py:33-39) without the wall time. */
+typedef struct givf_search_stats {
+  int64_t regions_visited;
+  int64_t subregions_visited;
+  int64_t subregions_pruned;
+  int64_t codes_scanned;
+} givf_search_stats;
+
+const char* givf_last_error(void);
+const char* givf_version(void);
+
+int givf_index_create(const givf_index_desc* desc, int device, givf_index_t* out);
+int givf_index_destroy(givf_index_t index);
+/* bytes of device memory held by the index arrays */
+int64_t givf_index_device_bytes(givf_index_t index);
+
+/* queries (nq, dim) f32.  ids (nq, k) int32 padded with -1, dists (nq, k)
+ * f32 padded with +inf, stats (nq) -- host or device; stream = cudaStream_t
+ * or NULL for the index's own stream.  Returns after the results are
+ * visible to the caller (host outputs: synchronised; device outputs:
+ * enqueued on `stream`). */
+int givf_search_topk(givf_index_t index, const float* queries, int64_t nq,
+                     const givf_search_params* params, int32_t k, int32_t* ids,
+                     float* dists, givf_search_stats* stats, void* stream);
+
+/* Full reference result per query: row q of ids/dists (width `capacity`)
+ * holds stats[q].codes_scanned entries.  capacity must be >= the number of
+ * codes any query can scan: min(candidates, rows reachable). */
+int givf_search_full(givf_index_t index, const float* queries, int64_t nq,
+                     const givf_search_params* params, int64_t capacity, int32_t* ids,
+                     float* dists, givf_search_stats* stats, void* stream);
+
+/* Region probe: region ids (nq, nprobe) int32 and float64 qc2 (nq, nprobe). */
+int givf_probe(givf_index_t index, const float* queries, int64_t nq, int32_t nprobe,
+               int32_t* regions, double* qc2, void* stream);
+
+/* K7: merge shard lists ids/dists (shards, nq, k) -> (nq, k) by (dist, id). */
+int givf_merge_topk(const int32_t* ids, const float* dists, int32_t shards, int64_t nq,
+                    int32_t k, int32_t* out_ids, float* out_dists, int device, void* stream);
+
+/* Count of kernels this library has launched in the calling process. */
+int64_t givf_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GIVF_B200_H */

@@ -1,0 +1,125 @@
+"""ctypes binding of the C ABI in include/givf_b200.h.
+
+The library is built in-tree (`make`, or `__graft_entry__.build()`) into
+`paper_1802_02422_b200/_lib/libgivf_b200.so`.  There is no fallback: if the
+library is missing or no CUDA device is present, the calls raise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libgivf_b200.so")
+
+GIVF_OK, GIVF_EINVAL, GIVF_ECUDA, GIVF_ENOMEM, GIVF_EINVARIANT = 0, 1, 2, 3, 4
+
+# every symbol include/givf_b200.h declares
+EXPORTS = (
+    "givf_last_error",
+    "givf_version",
+    "givf_index_create",
+    "givf_index_destroy",
+    "givf_index_device_bytes",
+    "givf_search_topk",
+    "givf_search_full",
+    "givf_probe",
+    "givf_merge_topk",
+    "givf_kernel_launches",
+)
+
+
+class IndexDesc(ctypes.Structure):
+    _fields_ = [
+        ("k", ctypes.c_int32),
+        ("dim", ctypes.c_int32),
+        ("groups", ctypes.c_int32),
+        ("m", ctypes.c_int32),
+        ("grouping", ctypes.c_int32),
+        ("n", ctypes.c_int64),
+        ("centroids", ctypes.c_void_p),
+        ("alphas", ctypes.c_void_p),
+        ("neighbor_ids", ctypes.c_void_p),
+        ("norm_terms", ctypes.c_void_p),
+        ("group_sizes", ctypes.c_void_p),
+        ("region_offsets", ctypes.c_void_p),
+        ("local_sizes", ctypes.c_void_p),
+        ("local_lo", ctypes.c_void_p),
+        ("point_ids", ctypes.c_void_p),
+        ("codes", ctypes.c_void_p),
+        ("const_bytes", ctypes.c_void_p),
+        ("codewords", ctypes.c_void_p),
+        ("rotation", ctypes.c_void_p),
+        ("const_lo", ctypes.c_double),
+        ("const_hi", ctypes.c_double),
+    ]
+
+
+class SearchParamsC(ctypes.Structure):
+    _fields_ = [
+        ("nprobe", ctypes.c_int32),
+        ("tau", ctypes.c_double),
+        ("candidates", ctypes.c_int64),
+        ("ef_search", ctypes.c_int32),
+        ("rerank", ctypes.c_int32),
+        ("prune", ctypes.c_int32),
+    ]
+
+
+class SearchStatsC(ctypes.Structure):
+    _fields_ = [
+        ("regions_visited", ctypes.c_int64),
+        ("subregions_visited", ctypes.c_int64),
+        ("subregions_pruned", ctypes.c_int64),
+        ("codes_scanned", ctypes.c_int64),
+    ]
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load the native library once; raises if it is not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(
+            f"givf_b200 native library not found at {path}; build it with `make` "
+            "(or __graft_entry__.build()) -- there is no CPU fallback"
+        )
+    lib = ctypes.CDLL(path)
+    vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    lib.givf_last_error.restype = ctypes.c_char_p
+    lib.givf_version.restype = ctypes.c_char_p
+    lib.givf_index_create.argtypes = [ctypes.POINTER(IndexDesc), ctypes.c_int, ctypes.POINTER(vp)]
+    lib.givf_index_destroy.argtypes = [vp]
+    lib.givf_index_device_bytes.argtypes = [vp]
+    lib.givf_index_device_bytes.restype = i64
+    lib.givf_search_topk.argtypes = [vp, vp, i64, ctypes.POINTER(SearchParamsC), i32, vp, vp, vp, vp]
+    lib.givf_search_full.argtypes = [vp, vp, i64, ctypes.POINTER(SearchParamsC), i64, vp, vp, vp, vp]
+    lib.givf_probe.argtypes = [vp, vp, i64, i32, vp, vp, vp]
+    lib.givf_merge_topk.argtypes = [vp, vp, i32, i64, i32, vp, vp, ctypes.c_int, vp]
+    lib.givf_kernel_launches.restype = i64
+    _lib = lib
+    return lib
+
+
+def check(rc: int) -> None:
+    """Map a status code to the reference's exception types."""
+    if rc == GIVF_OK:
+        return
+    msg = _lib.givf_last_error().decode()
+    if rc == GIVF_EINVAL:
+        raise ValueError(msg)
+    if rc == GIVF_EINVARIANT:
+        from .errors import InvariantError
+
+        raise InvariantError(msg)
+    if rc == GIVF_ENOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError(f"givf_b200 CUDA error: {msg}")
+
+
+def kernel_launches() -> int:
+    return int(load().givf_kernel_launches())

@@ -1,0 +1,603 @@
+// C ABI (include/givf_b200.h): device-resident index handle, workspace and
+// the per-batch kernel pipeline probe -> plan -> scan.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "givf_b200.h"
+#include "kernels.h"
+
+using namespace givf;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                             \
+  do {                                                                             \
+    cudaError_t _e = (expr);                                                       \
+    if (_e != cudaSuccess) {                                                       \
+      return fail(_e == cudaErrorMemoryAllocation ? GIVF_ENOMEM : GIVF_ECUDA,      \
+                  std::string(#expr) + ": " + cudaGetErrorString(_e));             \
+    }                                                                              \
+  } while (0)
+
+#define KCHECK()                                                                   \
+  do {                                                                             \
+    cudaError_t _e = cudaGetLastError();                                           \
+    if (_e != cudaSuccess)                                                         \
+      return fail(GIVF_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+  } while (0)
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// Grow-only scratch arena carved per call.
+struct Arena {
+  void* base = nullptr;
+  size_t cap = 0;
+  size_t off = 0;
+  cudaError_t reserve(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (base) cudaFree(base);
+    base = nullptr;
+    cap = 0;
+    size_t want = std::max(bytes, (size_t)1 << 20);
+    cudaError_t e = cudaMalloc(&base, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void reset() { off = 0; }
+  template <typename T>
+  T* take(size_t count) {
+    size_t bytes = ((count * sizeof(T)) + 255) & ~(size_t)255;
+    T* p = reinterpret_cast<T*>(static_cast<char*>(base) + off);
+    off += bytes;
+    return p;
+  }
+};
+
+template <typename T>
+size_t aligned_bytes(size_t count) {
+  return ((count * sizeof(T)) + 255) & ~(size_t)255;
+}
+
+}  // namespace
+
+struct givf_index {
+  int device = 0;
+  IndexView v{};
+  double const_lo = 0, const_hi = 0;
+  bool sharded = false;
+  cudaStream_t stream = nullptr;
+  std::vector<void*> allocs;
+  int64_t dev_bytes = 0;
+  Arena arena;
+  std::mutex mu;
+};
+
+namespace {
+
+template <typename T>
+cudaError_t upload(givf_index* ix, const T* host, size_t count, const T** out) {
+  void* d = nullptr;
+  size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+  cudaError_t e = cudaMalloc(&d, bytes);
+  if (e != cudaSuccess) return e;
+  ix->allocs.push_back(d);
+  ix->dev_bytes += (int64_t)bytes;
+  if (count) {
+    e = cudaMemcpy(d, host, count * sizeof(T), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return e;
+  }
+  *out = static_cast<const T*>(d);
+  return cudaSuccess;
+}
+
+const char* kSupportedM = "1, 2, 3, 4, 6, 8, 12, 16, 24, 32, 48, 64";
+bool supported_m(int m) {
+  switch (m) {
+    case 1: case 2: case 3: case 4: case 6: case 8: case 12: case 16: case 24: case 32:
+    case 48: case 64:
+      return true;
+    default:
+      return false;
+  }
+}
+
+// ConstQuantizer.table() (grouping.py:123-129): float64 (b + 0.5) * step + lo,
+// each op rounded separately, then float32.
+void const_table(double lo, double hi, float* out) {
+  volatile double step = (hi - lo) / 256.0;
+  for (int b = 0; b < 256; ++b) {
+    volatile double t = ((double)b + 0.5) * step;
+    volatile double v = t + lo;
+    out[b] = (float)v;
+  }
+}
+
+int check_params(const givf_index* ix, const givf_search_params* p) {
+  char buf[160];
+  if (!(1 <= p->nprobe && p->nprobe <= ix->v.K)) {
+    snprintf(buf, sizeof buf, "need 1 <= nprobe <= %d, got %d", ix->v.K, p->nprobe);
+    return fail(GIVF_EINVAL, buf);
+  }
+  if (!(0.0 < p->tau && p->tau <= 1.0)) {
+    snprintf(buf, sizeof buf, "need 0 < tau <= 1, got %g", p->tau);
+    return fail(GIVF_EINVAL, buf);
+  }
+  if (p->candidates < 1) {
+    snprintf(buf, sizeof buf, "need candidates >= 1, got %lld", (long long)p->candidates);
+    return fail(GIVF_EINVAL, buf);
+  }
+  if (p->ef_search < 1) {
+    snprintf(buf, sizeof buf, "need ef_search >= 1, got %d", p->ef_search);
+    return fail(GIVF_EINVAL, buf);
+  }
+  return GIVF_OK;
+}
+
+size_t workspace_budget() {
+  const char* s = getenv("GIVF_WORKSPACE_MB");
+  size_t mb = s ? (size_t)atoll(s) : 3072;
+  return std::max<size_t>(mb, 64) << 20;
+}
+
+// Probe tuning: candidate-set target and capacity (K1b / K2).
+struct ProbeShape {
+  int Tmin, cap;
+  bool exhaustive;  // rank all K regions exactly (nprobe == K or P too large)
+};
+ProbeShape probe_shape(int K, int P) {
+  ProbeShape s;
+  s.exhaustive = (P == K);
+  s.Tmin = std::min(K, P + std::max(32, P / 4));
+  s.cap = std::min(K, std::max(2 * s.Tmin, 256));
+  if (s.cap > 4096) s.exhaustive = true;  // recheck sorts in <= 4096-entry smem
+  return s;
+}
+
+constexpr int kFullSlots = 32;
+
+struct Plan {
+  int P, G, K, d;
+  int64_t total, kept, budget, cap_w;
+  ProbeShape ps;
+};
+
+// Probe for one chunk of queries: regions (nq, P) and qc2 (nq, P).
+int run_probe(givf_index* ix, const Plan& pl, const float* dQ, int nq, int* regions,
+              double* qc2, Arena& ar, cudaStream_t st) {
+  const IndexView& v = ix->v;
+  const int P = pl.P, K = v.K, d = v.d;
+  int* failf = ar.take<int>(nq);
+  const uint32_t kp2 = next_pow2_host((uint32_t)K), pp2 = next_pow2_host((uint32_t)P);
+  uint64_t* sk = ar.take<uint64_t>((size_t)kFullSlots * kp2);
+  uint32_t* sv = ar.take<uint32_t>((size_t)kFullSlots * kp2);
+  uint64_t* sk2 = ar.take<uint64_t>((size_t)kFullSlots * pp2);
+  uint32_t* sv2 = ar.take<uint32_t>((size_t)kFullSlots * pp2);
+  double* sdv = ar.take<double>((size_t)kFullSlots * pp2);
+  const int slots = std::min(kFullSlots, nq);
+  if (pl.ps.exhaustive) {
+    // nprobe == K: search.py:80-84 formula; larger P: exact f64 ranking of all.
+    int mode = (P == K) ? 0 : 1;
+    if (mode == 1) {
+      CUDA_TRY(cudaMemsetAsync(failf, 0xff, sizeof(int) * nq, st));  // all "failed"
+    }
+    launch_probe_full(dQ, v.centroids, nq, K, d, P, mode, failf, slots, sk, sv, sk2, sv2, sdv,
+                      regions, qc2, st);
+    g_launches += 1;
+    KCHECK();
+    return GIVF_OK;
+  }
+  float* D = ar.take<float>((size_t)nq * K);
+  int* cand = ar.take<int>((size_t)nq * pl.ps.cap);
+  int* cand_n = ar.take<int>(nq);
+  float* theta = ar.take<float>(nq);
+  launch_probe_gemm(dQ, v.centroids, v.c2f, nq, K, d, D, K, st);
+  launch_probe_select(D, K, nq, K, pl.ps.Tmin, pl.ps.cap, cand, cand_n, theta, st);
+  const float eps_scale = 3.0f * (float)(d + 4) * 5.9604645e-8f;
+  launch_probe_recheck(dQ, v.centroids, nq, K, d, P, cand, cand_n, pl.ps.cap, theta, v.cmax,
+                       eps_scale, regions, qc2, failf, st);
+  launch_probe_full(dQ, v.centroids, nq, K, d, P, 1, failf, slots, sk, sv, sk2, sv2, sdv,
+                    regions, qc2, st);
+  g_launches += 4;
+  KCHECK();
+  return GIVF_OK;
+}
+
+size_t probe_bytes_per_query(const Plan& pl) {
+  size_t b = aligned_bytes<int>(1) * 4 + aligned_bytes<int>(pl.P) + aligned_bytes<double>(pl.P);
+  if (!pl.ps.exhaustive) b += (size_t)pl.K * 4 + (size_t)pl.ps.cap * 4;
+  return b;
+}
+size_t probe_fixed_bytes(const Plan& pl) {
+  const size_t kp2 = next_pow2_host((uint32_t)pl.K), pp2 = next_pow2_host((uint32_t)pl.P);
+  return kFullSlots * (kp2 * 12 + pp2 * 20) + 16 * 256;
+}
+
+int build_plan(givf_index* ix, const givf_search_params* p, Plan* pl) {
+  int rc = check_params(ix, p);
+  if (rc) return rc;
+  pl->P = p->nprobe;
+  pl->G = ix->v.G;
+  pl->K = ix->v.K;
+  pl->d = ix->v.d;
+  pl->total = (int64_t)pl->P * pl->G;
+  pl->kept = p->prune ? (int64_t)std::ceil(p->tau * (double)pl->total) : pl->total;
+  pl->kept = std::min(std::max<int64_t>(pl->kept, 1), pl->total);
+  pl->budget = p->candidates;
+  pl->cap_w = std::max<int64_t>(1, std::min(pl->kept, pl->budget));
+  pl->ps = probe_shape(pl->K, pl->P);
+  return GIVF_OK;
+}
+
+enum OutMode { OUT_TOPK = 0, OUT_FULL = 1 };
+
+int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_search_params* p,
+               OutMode om, int64_t width, int32_t* ids, float* dists, givf_search_stats* stats,
+               void* stream) {
+  Plan pl;
+  int rc = build_plan(ix, p, &pl);
+  if (rc) return rc;
+  if (om == OUT_TOPK && (width < 1 || width > 4096))
+    return fail(GIVF_EINVAL, "need 1 <= k <= 4096");
+  if (om == OUT_FULL) {
+    if (ix->sharded) return fail(GIVF_EINVAL, "full results need an unsharded index");
+    int64_t need = std::min<int64_t>(p->candidates, ix->v.n);
+    if (width < need)
+      return fail(GIVF_EINVAL, "capacity must be >= min(candidates, n)");
+  }
+  if (nq == 0) return GIVF_OK;
+  if (!queries || !ids || !dists || !stats) return fail(GIVF_EINVAL, "null output pointer");
+
+  std::lock_guard<std::mutex> lock(ix->mu);
+  CUDA_TRY(cudaSetDevice(ix->device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : ix->stream;
+  const IndexView& v = ix->v;
+  const bool q_dev = is_device_ptr(queries);
+  const bool out_dev = is_device_ptr(ids) && is_device_ptr(dists);
+  const bool st_dev = is_device_ptr(stats);
+  const bool rerank = p->rerank != 0;
+  const int64_t full_p2 = om == OUT_FULL ? (int64_t)next_pow2_host((uint32_t)std::max<int64_t>(width, 1)) : 0;
+
+  // per-query workspace
+  size_t per_q = aligned_bytes<float>(v.d) + probe_bytes_per_query(pl) +
+                 2 * aligned_bytes<double>(pl.total) + aligned_bytes<WorkItem>(pl.cap_w) +
+                 aligned_bytes<int>(1) + aligned_bytes<int64_t>(4);
+  if (om == OUT_FULL && !rerank) {
+    size_t cp2 = next_pow2_host((uint32_t)std::min<int64_t>(pl.cap_w, 1 << 30));
+    per_q += aligned_bytes<int32_t>(pl.cap_w) + cp2 * 12;
+  }
+  if (om == OUT_FULL && rerank) per_q += (size_t)full_p2 * 8;
+  if (!out_dev) per_q += (size_t)width * 8 + 512;
+  const size_t fixed = probe_fixed_bytes(pl) + (1 << 16);
+  const size_t budget = workspace_budget();
+  int64_t chunk = budget > fixed ? (int64_t)((budget - fixed) / per_q) : 1;
+  chunk = std::max<int64_t>(1, std::min<int64_t>(chunk, nq));
+  chunk = std::min<int64_t>(chunk, 65535);
+  CUDA_TRY(ix->arena.reserve(fixed + per_q * (size_t)chunk + (1 << 20)));
+
+  for (int64_t q0 = 0; q0 < nq; q0 += chunk) {
+    const int bq = (int)std::min<int64_t>(chunk, nq - q0);
+    Arena& ar = ix->arena;
+    ar.reset();
+    const float* dQ;
+    if (q_dev) {
+      dQ = queries + q0 * v.d;
+    } else {
+      float* tmp = ar.take<float>((size_t)bq * v.d);
+      CUDA_TRY(cudaMemcpyAsync(tmp, queries + q0 * v.d, sizeof(float) * bq * v.d,
+                               cudaMemcpyHostToDevice, st));
+      dQ = tmp;
+    }
+    int* regions = ar.take<int>((size_t)bq * pl.P);
+    double* qc2 = ar.take<double>((size_t)bq * pl.P);
+    rc = run_probe(ix, pl, dQ, bq, regions, qc2, ar, st);
+    if (rc) return rc;
+
+    PlanArgs pa{};
+    pa.ix = v;
+    pa.Q = dQ;
+    pa.regions = regions;
+    pa.qc2 = qc2;
+    pa.nq = bq;
+    pa.P = pl.P;
+    pa.kept = pl.kept;
+    pa.budget = pl.budget;
+    pa.sbase = ar.take<double>((size_t)bq * pl.total);
+    pa.sscore = ar.take<double>((size_t)bq * pl.total);
+    pa.cap_w = pl.cap_w;
+    pa.work = ar.take<WorkItem>((size_t)bq * pl.cap_w);
+    pa.nwork = ar.take<int>(bq);
+    int64_t* dstats = st_dev ? reinterpret_cast<int64_t*>(stats + q0) : ar.take<int64_t>((size_t)bq * 4);
+    pa.stats = dstats;
+    pa.sort_work = (om == OUT_FULL && !rerank) ? 1 : 0;
+    if (pa.sort_work) {
+      int64_t cp2 = next_pow2_host((uint32_t)pl.cap_w);
+      pa.skey = ar.take<uint64_t>((size_t)bq * cp2);
+      pa.sval = ar.take<uint32_t>((size_t)bq * cp2);
+      pa.order = ar.take<int32_t>((size_t)bq * pl.cap_w);
+    }
+    launch_plan(pa, st);
+    g_launches += 1;
+    KCHECK();
+
+    int32_t* oid;
+    float* od;
+    if (out_dev) {
+      oid = ids + q0 * width;
+      od = dists + q0 * width;
+    } else {
+      oid = ar.take<int32_t>((size_t)bq * width);
+      od = ar.take<float>((size_t)bq * width);
+    }
+    if (om == OUT_TOPK || rerank) {
+      ScanArgs sa{};
+      sa.ix = v;
+      sa.Q = dQ;
+      sa.nq = bq;
+      sa.work = pa.work;
+      sa.cap_w = pl.cap_w;
+      sa.nwork = pa.nwork;
+      sa.mode = om == OUT_TOPK ? 0 : 1;
+      sa.k = (int)(om == OUT_TOPK ? width : 0);
+      sa.out_ids = oid;
+      sa.out_d = od;
+      if (om == OUT_FULL) {
+        sa.full_keys = ar.take<uint64_t>((size_t)bq * full_p2);
+        sa.cap_full_p2 = full_p2;
+      }
+      launch_scan(sa, st);
+      g_launches += 1;
+      KCHECK();
+      if (om == OUT_FULL) {
+        launch_full_finish(sa.full_keys, full_p2, dstats, bq, oid, od, width, st);
+        g_launches += 1;
+        KCHECK();
+      }
+    } else {
+      launch_scan_order(v, pa.work, pl.cap_w, pa.nwork, pa.order, bq, oid, od, width, st);
+      g_launches += 1;
+      KCHECK();
+    }
+    if (!out_dev) {
+      CUDA_TRY(cudaMemcpyAsync(ids + q0 * width, oid, sizeof(int32_t) * bq * width,
+                               cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaMemcpyAsync(dists + q0 * width, od, sizeof(float) * bq * width,
+                               cudaMemcpyDeviceToHost, st));
+    }
+    if (!st_dev) {
+      CUDA_TRY(cudaMemcpyAsync(stats + q0, dstats, sizeof(int64_t) * 4 * bq,
+                               cudaMemcpyDeviceToHost, st));
+    }
+    // the arena is reused by the next chunk: finish this one first
+    if (q0 + chunk < nq) CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  if (!out_dev || !st_dev || !q_dev) CUDA_TRY(cudaStreamSynchronize(st));
+  return GIVF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* givf_last_error(void) { return g_err.c_str(); }
+const char* givf_version(void) { return "givf_b200 0.1 (sm_100a)"; }
+int64_t givf_kernel_launches(void) { return g_launches.load(); }
+
+int givf_index_create(const givf_index_desc* ds, int device, givf_index_t* out) {
+  if (!ds || !out) return fail(GIVF_EINVAL, "null argument");
+  *out = nullptr;
+  const int K = ds->k, d = ds->dim, G = ds->groups, M = ds->m;
+  if (K < 1 || d < 1 || G < 1 || M < 1) return fail(GIVF_EINVAL, "k, dim, groups, m must be >= 1");
+  if (d % M != 0) return fail(GIVF_EINVAL, "m must divide dim");
+  if (!supported_m(M)) return fail(GIVF_EINVAL, std::string("m must be one of ") + kSupportedM);
+  if (d > 1024) return fail(GIVF_EINVAL, "dim must be <= 1024");
+  if (ds->grouping && (!ds->neighbor_ids || !ds->norm_terms))
+    return fail(GIVF_EINVAL, "grouping needs neighbor_ids and norm_terms");
+  if (!ds->grouping && G != 1) return fail(GIVF_EINVAL, "groups must be 1 without grouping");
+  if (!ds->centroids || !ds->alphas || !ds->group_sizes || !ds->region_offsets ||
+      !ds->codewords || (ds->n > 0 && (!ds->point_ids || !ds->codes || !ds->const_bytes)))
+    return fail(GIVF_EINVAL, "null index array");
+  if ((ds->local_sizes == nullptr) != (ds->local_lo == nullptr))
+    return fail(GIVF_EINVAL, "local_sizes and local_lo go together");
+  if (ds->n >= (int64_t)1 << 40) return fail(GIVF_EINVAL, "too many rows");
+
+  // host-side layout checks and derived tables
+  const int32_t* lsz = ds->local_sizes ? ds->local_sizes : ds->group_sizes;
+  std::vector<int64_t> lstart((size_t)K * G);
+  for (int r = 0; r < K; ++r) {
+    int64_t o = ds->region_offsets[r];
+    for (int j = 0; j < G; ++j) {
+      int32_t s = lsz[(size_t)r * G + j];
+      if (s < 0 || ds->group_sizes[(size_t)r * G + j] < 0)
+        return fail(GIVF_EINVAL, "negative group size");
+      lstart[(size_t)r * G + j] = o;
+      o += s;
+    }
+    if (o != ds->region_offsets[r + 1]) return fail(GIVF_EINVAL, "region_offsets disagree with group sizes");
+  }
+  if (ds->region_offsets[0] != 0 || ds->region_offsets[K] != ds->n)
+    return fail(GIVF_EINVAL, "region_offsets must span [0, n]");
+  if (ds->grouping) {
+    for (size_t i = 0; i < (size_t)K * G; ++i)
+      if (ds->neighbor_ids[i] < 0 || ds->neighbor_ids[i] >= K)
+        return fail(GIVF_EINVAL, "neighbor id out of range");
+  }
+  std::vector<float> c2f(K);
+  double cmax = 0.0;
+  for (int r = 0; r < K; ++r) {
+    double s = 0.0;
+    for (int j = 0; j < d; ++j) {
+      double x = ds->centroids[(size_t)r * d + j];
+      s += x * x;
+    }
+    c2f[r] = (float)s;
+    cmax = std::max(cmax, std::sqrt(s));
+  }
+  float ctab[256];
+  const_table(ds->const_lo, ds->const_hi, ctab);
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(GIVF_ECUDA, "no CUDA device");
+  }
+  if (device < 0 || device >= ndev) return fail(GIVF_EINVAL, "bad device ordinal");
+  CUDA_TRY(cudaSetDevice(device));
+
+  givf_index* ix = new givf_index();
+  ix->device = device;
+  ix->const_lo = ds->const_lo;
+  ix->const_hi = ds->const_hi;
+  ix->sharded = ds->local_sizes != nullptr;
+  IndexView& v = ix->v;
+  v.K = K; v.d = d; v.G = G; v.M = M; v.grouping = ds->grouping ? 1 : 0; v.n = ds->n;
+  v.cmax = (float)(cmax * (1.0 + 1e-6));
+  const size_t KG = (size_t)K * G;
+  cudaError_t e = cudaSuccess;
+#define UP(host, count, field) \
+  if (e == cudaSuccess) e = upload(ix, host, count, &v.field)
+  UP(ds->centroids, (size_t)K * d, centroids);
+  UP(c2f.data(), (size_t)K, c2f);
+  UP(ds->alphas, (size_t)K, alphas);
+  if (ds->grouping) {
+    UP(ds->neighbor_ids, KG, nbr);
+    UP(ds->norm_terms, KG, norm);
+  }
+  UP(ds->group_sizes, KG, gsize);
+  UP(lstart.data(), KG, lstart);
+  if (ds->local_sizes) {
+    UP(ds->local_sizes, KG, lsize);
+    UP(ds->local_lo, KG, llo);
+  }
+  UP(ds->point_ids, (size_t)ds->n, pids);
+  UP(ds->codes, (size_t)ds->n * M, codes);
+  UP(ds->const_bytes, (size_t)ds->n, cbytes);
+  UP(ds->codewords, (size_t)M * 256 * (d / M), codewords);
+  if (ds->rotation) UP(ds->rotation, (size_t)d * d, rotation);
+  UP(ctab, (size_t)256, ctab);
+#undef UP
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ix->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    givf_index_destroy(ix);
+    return fail(e == cudaErrorMemoryAllocation ? GIVF_ENOMEM : GIVF_ECUDA,
+                std::string("index upload: ") + cudaGetErrorString(e));
+  }
+  *out = ix;
+  return GIVF_OK;
+}
+
+int givf_index_destroy(givf_index_t ix) {
+  if (!ix) return GIVF_OK;
+  cudaSetDevice(ix->device);
+  if (ix->stream) cudaStreamSynchronize(ix->stream);
+  for (void* p : ix->allocs) cudaFree(p);
+  if (ix->arena.base) cudaFree(ix->arena.base);
+  if (ix->stream) cudaStreamDestroy(ix->stream);
+  delete ix;
+  return GIVF_OK;
+}
+
+int64_t givf_index_device_bytes(givf_index_t ix) { return ix ? ix->dev_bytes : 0; }
+
+int givf_search_topk(givf_index_t ix, const float* queries, int64_t nq,
+                     const givf_search_params* params, int32_t k, int32_t* ids, float* dists,
+                     givf_search_stats* stats, void* stream) {
+  if (!ix || !params) return fail(GIVF_EINVAL, "null argument");
+  return run_search(ix, queries, nq, params, OUT_TOPK, k, ids, dists, stats, stream);
+}
+
+int givf_search_full(givf_index_t ix, const float* queries, int64_t nq,
+                     const givf_search_params* params, int64_t capacity, int32_t* ids,
+                     float* dists, givf_search_stats* stats, void* stream) {
+  if (!ix || !params) return fail(GIVF_EINVAL, "null argument");
+  return run_search(ix, queries, nq, params, OUT_FULL, capacity, ids, dists, stats, stream);
+}
+
+int givf_probe(givf_index_t ix, const float* queries, int64_t nq, int32_t nprobe,
+               int32_t* regions, double* qc2, void* stream) {
+  if (!ix) return fail(GIVF_EINVAL, "null argument");
+  givf_search_params p{nprobe, 1.0, 1, 1, 1, 1};
+  Plan pl;
+  int rc = build_plan(ix, &p, &pl);
+  if (rc) return rc;
+  if (nq == 0) return GIVF_OK;
+  std::lock_guard<std::mutex> lock(ix->mu);
+  CUDA_TRY(cudaSetDevice(ix->device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : ix->stream;
+  const bool q_dev = is_device_ptr(queries), o_dev = is_device_ptr(regions) && is_device_ptr(qc2);
+  const int d = ix->v.d;
+  size_t per_q = aligned_bytes<float>(d) + probe_bytes_per_query(pl) + (size_t)pl.P * 12 + 1024;
+  size_t fixed = probe_fixed_bytes(pl) + (1 << 16);
+  int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(nq, (workspace_budget() - std::min(workspace_budget() - 1, fixed)) / per_q));
+  chunk = std::min<int64_t>(chunk, 65535);
+  CUDA_TRY(ix->arena.reserve(fixed + per_q * (size_t)chunk + (1 << 20)));
+  for (int64_t q0 = 0; q0 < nq; q0 += chunk) {
+    const int bq = (int)std::min<int64_t>(chunk, nq - q0);
+    Arena& ar = ix->arena;
+    ar.reset();
+    const float* dQ = queries + q0 * d;
+    if (!q_dev) {
+      float* tmp = ar.take<float>((size_t)bq * d);
+      CUDA_TRY(cudaMemcpyAsync(tmp, queries + q0 * d, sizeof(float) * bq * d, cudaMemcpyHostToDevice, st));
+      dQ = tmp;
+    }
+    int* r = o_dev ? regions + q0 * pl.P : ar.take<int>((size_t)bq * pl.P);
+    double* c = o_dev ? qc2 + q0 * pl.P : ar.take<double>((size_t)bq * pl.P);
+    rc = run_probe(ix, pl, dQ, bq, r, c, ar, st);
+    if (rc) return rc;
+    if (!o_dev) {
+      CUDA_TRY(cudaMemcpyAsync(regions + q0 * pl.P, r, sizeof(int) * bq * pl.P, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaMemcpyAsync(qc2 + q0 * pl.P, c, sizeof(double) * bq * pl.P, cudaMemcpyDeviceToHost, st));
+    }
+    CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  return GIVF_OK;
+}
+
+int givf_merge_topk(const int32_t* ids, const float* dists, int32_t shards, int64_t nq, int32_t k,
+                    int32_t* out_ids, float* out_dists, int device, void* stream) {
+  if (shards < 1 || k < 1 || (int64_t)shards * k > 65536) return fail(GIVF_EINVAL, "bad shards/k");
+  if (nq == 0) return GIVF_OK;
+  if (!is_device_ptr(ids) || !is_device_ptr(dists) || !is_device_ptr(out_ids) || !is_device_ptr(out_dists))
+    return fail(GIVF_EINVAL, "merge expects device pointers");
+  CUDA_TRY(cudaSetDevice(device));
+  for (int64_t q0 = 0; q0 < nq; q0 += 65535) {
+    int bq = (int)std::min<int64_t>(65535, nq - q0);
+    // shard lists are (shards, nq, k): offset rows of every shard
+    if (q0 == 0 && bq == nq) {
+      launch_merge_topk(ids, dists, shards, (int)nq, k, out_ids, out_dists, (cudaStream_t)stream);
+      g_launches += 1;
+    } else {
+      return fail(GIVF_EINVAL, "merge supports nq <= 65535 per call");
+    }
+  }
+  KCHECK();
+  return GIVF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,109 @@
+// Launchers for the search-path kernels (implemented in probe.cu, plan.cu,
+// scan.cu).  Host-side orchestration lives in capi.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace givf {
+
+inline uint32_t next_pow2_host(uint32_t x) {
+  uint32_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+// One scan segment: a run of consecutive code rows of one kept (region,
+// group) slice, with the float64 terms the distance needs (search.py:143-148).
+struct WorkItem {
+  int64_t start;  // first code row (local to this shard)
+  int32_t len;    // rows to scan
+  int32_t flat;   // pos * G + grp: position in the (score, pos, grp) order key
+  double base;    // (1-a) qc2 + a qs2
+  double score;   // base + norm term (the pruning key; rerank=False output)
+};
+
+struct IndexView {
+  int K, d, G, M, grouping;
+  int64_t n;
+  const float* centroids;     // (K, d)
+  const float* c2f;           // (K) f32(|c|^2)
+  float cmax;                 // max |c|
+  const float* alphas;        // (K)
+  const int32_t* nbr;         // (K, G) or null
+  const float* norm;          // (K, G) or null
+  const int32_t* gsize;       // (K, G) global group sizes (budget walk)
+  const int64_t* lstart;      // (K, G) first local row of each slice
+  const int32_t* lsize;       // (K, G) local rows of each slice (null: = gsize)
+  const int32_t* llo;         // (K, G) first global slot held here (null: 0)
+  const int32_t* pids;        // (n)
+  const uint8_t* codes;       // (n, M)
+  const uint8_t* cbytes;      // (n)
+  const float* codewords;     // (M, 256, d/M)
+  const float* rotation;      // (d, d) or null
+  const float* ctab;          // (256) dequantized constants, f32
+};
+
+// probe.cu
+void launch_probe_gemm(const float* Q, const float* C, const float* c2, int nq, int K, int d,
+                       float* D, int64_t ldD, cudaStream_t s);
+void launch_probe_select(const float* D, int64_t ldD, int nq, int K, int Tmin, int cap,
+                         int* cand, int* cand_n, float* theta, cudaStream_t s);
+size_t probe_recheck_smem(int d, int P, int cap);
+void launch_probe_recheck(const float* Q, const float* C, int nq, int K, int d, int P,
+                          const int* cand, const int* cand_n, int cap, const float* theta,
+                          float cmax, float eps_scale, int* regions, double* qc2, int* fail,
+                          cudaStream_t s);
+void launch_probe_full(const float* Q, const float* C, int nq, int K, int d, int P, int mode,
+                       const int* fail, int nslots, uint64_t* sk, uint32_t* sv, uint64_t* sk2,
+                       uint32_t* sv2, double* sdv, int* regions, double* qc2, cudaStream_t s);
+
+// plan.cu
+struct PlanArgs {
+  IndexView ix;
+  const float* Q;
+  const int* regions;   // (nq, P)
+  const double* qc2;    // (nq, P)
+  int nq, P;
+  int64_t kept, budget;
+  double* sbase;        // (nq, P*G) scratch
+  double* sscore;       // (nq, P*G) scratch
+  WorkItem* work;       // (nq, cap_w)
+  int64_t cap_w;
+  int* nwork;           // (nq)
+  int64_t* stats;       // (nq, 4)
+  // rerank=False: scan order of the work list
+  int sort_work;
+  uint64_t* skey;       // (nq, pow2(cap_w)) scratch
+  uint32_t* sval;       // (nq, pow2(cap_w)) scratch
+  int32_t* order;       // (nq, cap_w)
+};
+void launch_plan(const PlanArgs& a, cudaStream_t s);
+
+// scan.cu
+struct ScanArgs {
+  IndexView ix;
+  const float* Q;
+  int nq;
+  const WorkItem* work;
+  int64_t cap_w;
+  const int* nwork;
+  int mode;             // 0: top-k, 1: full (all scanned keys)
+  int k;
+  int32_t* out_ids;     // (nq, k)
+  float* out_d;         // (nq, k)
+  uint64_t* full_keys;  // (nq, cap_full_p2)
+  int64_t cap_full_p2;
+};
+void launch_scan(const ScanArgs& a, cudaStream_t s);
+// full mode: sort each query's keys and split into ids/dists rows of width `ld`
+void launch_full_finish(uint64_t* keys, int64_t cap_p2, const int64_t* stats, int nq,
+                        int32_t* ids, float* dists, int64_t ld, cudaStream_t s);
+// rerank=False: scan-order ids with group scores
+void launch_scan_order(const IndexView& ix, const WorkItem* work, int64_t cap_w,
+                       const int* nwork, const int32_t* order, int nq, int32_t* ids,
+                       float* dists, int64_t ld, cudaStream_t s);
+// K7: merge per-shard top-k lists (G, nq, k) into (nq, k)
+void launch_merge_topk(const int32_t* ids, const float* dists, int G, int nq, int k,
+                       int32_t* out_ids, float* out_d, cudaStream_t s);
+
+}  // namespace givf

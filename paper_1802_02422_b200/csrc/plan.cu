@@ -1,0 +1,335 @@
+// K3 + K4: group scores, tau-pruning and the candidate-budget walk
+// (reference: search.py:111-139, util.concat_ranges util.py:58-74,
+// GroupedIndex.group_starts index.py:80-85).
+//
+// One CTA per query.  Scores are float64 with every operation separately
+// rounded (no FMA), exactly as numpy evaluates
+//     base  = (1 - a) * qc2 + a * qs2,   score = base + f64(norm_term)
+// with qs2 = sum((f64(c_s) - f64(q))^2).  The reference then lexsorts all
+// P*G items by (score, pos, grp), keeps the first ceil(tau * P*G) and walks
+// them until the candidate budget is spent.  Sorting P*G items per query is
+// wasteful: only the prefix that ends at min(kept, budget crossing) matters,
+// and only its *set* matters for the reranked output.  The CTA therefore
+//   1. histograms the order-preserving keys of (score, flat) in <= 2048
+//      buckets (counts and group-size weights together),
+//   2. finds the first bucket where either the kept count or the budget is
+//      reached, refining that bucket with further histogram levels until it
+//      holds <= SORTCAP items,
+//   3. sorts only that bucket exactly and walks it.
+// Everything strictly below the bucket is scanned whole; the walk decides
+// the bucket's items (partial last group included).  For rerank=False the
+// emitted work list is additionally sorted into the reference scan order.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace givf {
+
+constexpr int PLAN_THREADS = 256;
+constexpr int PLAN_BUCKETS = 2048;
+constexpr int SORTCAP = 2048;
+
+GIVF_DEV double key_to_f64(uint64_t k) {
+  uint64_t u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)u);
+}
+
+__device__ double warp_sqdist64_plan(const float* __restrict__ c, const double* qd, int d) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int j = lane; j < d; j += 32) {
+    double t = dsub((double)c[j], qd[j]);
+    s = dadd(s, dmul(t, t));
+  }
+  return warp_sum(s);
+}
+
+__global__ void __launch_bounds__(PLAN_THREADS) k_plan(PlanArgs a) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  unsigned long long* hw = reinterpret_cast<unsigned long long*>(dsm);
+  uint64_t* bkey = reinterpret_cast<uint64_t*>(hw + PLAN_BUCKETS);
+  uint32_t* hc = reinterpret_cast<uint32_t*>(bkey + SORTCAP);
+  uint32_t* bval = hc + PLAN_BUCKETS;
+  int32_t* blen = reinterpret_cast<int32_t*>(bval + SORTCAP);
+  double* qd = reinterpret_cast<double*>(blen + SORTCAP);
+  __shared__ unsigned long long red64[40];
+  __shared__ uint32_t red32[40];
+  __shared__ int s_b;
+  __shared__ uint32_t s_bc_before;
+  __shared__ unsigned long long s_bw_before;
+  __shared__ int s_nemit, s_nb;
+  __shared__ unsigned long long s_walk_w;
+  __shared__ int s_walk_begun;
+
+  const IndexView& ix = a.ix;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const int G = ix.G, d = ix.d, P = a.P;
+  const int64_t total = (int64_t)P * G;
+  const int* reg = a.regions + (int64_t)b * P;
+  const double* qc2 = a.qc2 + (int64_t)b * P;
+  double* sbase = a.sbase + (int64_t)b * total;
+  double* sscore = a.sscore + (int64_t)b * total;
+
+  for (int j = tid; j < d; j += blockDim.x) qd[j] = (double)a.Q[(int64_t)b * d + j];
+  __syncthreads();
+
+  // ---- 1. scores (search.py:111-121)
+  unsigned long long kmin = ~0ull, kmax = 0ull;
+  if (ix.grouping) {
+    const int warp = tid >> 5, nw = blockDim.x >> 5, lane = tid & 31;
+    for (int64_t f = warp; f < total; f += nw) {
+      int p = (int)(f / G), j = (int)(f % G);
+      int r = reg[p];
+      int s = ix.nbr[(int64_t)r * G + j];
+      double qs2 = warp_sqdist64_plan(ix.centroids + (int64_t)s * d, qd, d);
+      if (lane == 0) {
+        double al = (double)ix.alphas[r];
+        double base = dadd(dmul(dsub(1.0, al), qc2[p]), dmul(al, qs2));
+        double score = dadd(base, (double)ix.norm[(int64_t)r * G + j]);
+        sbase[f] = base;
+        sscore[f] = score;
+        uint64_t k = f64_key(score);
+        kmin = min(kmin, (unsigned long long)k);
+        kmax = max(kmax, (unsigned long long)k);
+      }
+    }
+  } else {
+    for (int64_t f = tid; f < total; f += blockDim.x) {
+      double v = qc2[f / G];
+      sbase[f] = v;
+      sscore[f] = v;
+      uint64_t k = f64_key(v);
+      kmin = min(kmin, (unsigned long long)k);
+      kmax = max(kmax, (unsigned long long)k);
+    }
+  }
+  __syncthreads();  // scratch writes visible block-wide (global, same CTA)
+  kmin = block_min(kmin, red64);
+  kmax = block_max(kmax, red64);
+
+  // ---- 2. locate the end of the scanned prefix (search.py:123-139)
+  const uint64_t kept = (uint64_t)a.kept, budget = (uint64_t)a.budget;
+  uint64_t taken_c = 0, taken_w = 0;
+  int phase = 0;                 // 0: bucket on score key; 1: on flat among score == kx
+  uint64_t lo = kmin, hi = kmax, kx = 0;
+  uint64_t bucket_lo = 0, bucket_hi = 0;  // final bucket range (phase-dependent key)
+  for (int level = 0; level < 16; ++level) {
+    uint64_t range = hi - lo;
+    int shift = range == 0 ? 0 : max(0, 64 - __clzll((long long)range) - 11);
+    uint32_t nb = (uint32_t)(range >> shift) + 1;
+    for (uint32_t i = tid; i < nb; i += blockDim.x) { hc[i] = 0; hw[i] = 0; }
+    __syncthreads();
+    for (int64_t f = tid; f < total; f += blockDim.x) {
+      uint64_t sk = f64_key(sscore[f]);
+      uint64_t key;
+      if (phase == 0) {
+        if (sk < lo || sk > hi) continue;
+        key = sk;
+      } else {
+        if (sk != kx || (uint64_t)f < lo || (uint64_t)f > hi) continue;
+        key = (uint64_t)f;
+      }
+      int p = (int)(f / G), j = (int)(f % G);
+      uint32_t bk = (uint32_t)((key - lo) >> shift);
+      atomicAdd(&hc[bk], 1u);
+      atomicAdd(&hw[bk], (unsigned long long)ix.gsize[(int64_t)reg[p] * G + j]);
+    }
+    __syncthreads();
+    const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;
+    uint32_t b0 = tid * per, b1 = min(nb, b0 + per);
+    uint32_t rc = 0;
+    unsigned long long rw = 0;
+    for (uint32_t x = b0; x < b1; ++x) { rc += hc[x]; rw += hw[x]; }
+    uint32_t totc;
+    unsigned long long totw;
+    uint32_t pc = block_exclusive_scan(rc, red32, &totc);
+    unsigned long long pw = block_exclusive_scan(rw, red64, &totw);
+    if (tid == 0) { s_b = -1; s_nb = (int)nb; }
+    __syncthreads();
+    {
+      uint64_t c0 = taken_c + pc, w0 = taken_w + pw;
+      bool before_ok = c0 < kept && w0 < budget;
+      bool after_hit = (c0 + rc >= kept) || (w0 + rw >= budget);
+      if (b0 < b1 && before_ok && after_hit) {
+        uint64_t cc = c0, ww = w0;
+        for (uint32_t x = b0; x < b1; ++x) {
+          if (cc + hc[x] >= kept || ww + hw[x] >= budget) {
+            s_b = (int)x;
+            s_bc_before = (uint32_t)(cc - taken_c);
+            s_bw_before = ww - taken_w;
+            break;
+          }
+          cc += hc[x];
+          ww += hw[x];
+        }
+      }
+    }
+    __syncthreads();
+    const int bsel = s_b;
+    if (bsel < 0) {  // nothing crosses: the whole range is scanned (cannot happen at level 0)
+      bucket_lo = hi + 1;
+      bucket_hi = hi;
+      taken_c += totc;
+      taken_w += totw;
+      break;
+    }
+    const uint32_t cnt_b = hc[bsel];
+    const uint64_t bl = lo + ((uint64_t)bsel << shift);
+    const uint64_t bspan = bl + ((1ull << shift) - 1);
+    const uint64_t bh = bspan < hi ? bspan : hi;
+    taken_c += s_bc_before;
+    taken_w += s_bw_before;
+    __syncthreads();
+    if (cnt_b <= (uint32_t)SORTCAP) {
+      bucket_lo = bl;
+      bucket_hi = bh;
+      break;
+    }
+    if (phase == 0 && shift == 0) {  // many items share one score: order them by flat
+      phase = 1;
+      kx = bl;
+      lo = 0;
+      hi = (uint64_t)(total - 1);
+      continue;
+    }
+    lo = bl;
+    hi = bh;
+  }
+
+  // ---- 3. sort the boundary bucket exactly and walk it
+  if (tid == 0) { s_nemit = 0; s_walk_w = 0; s_walk_begun = 0; }
+  __syncthreads();
+  __shared__ uint32_t s_nbk;
+  if (tid == 0) s_nbk = 0;
+  __syncthreads();
+  auto in_bucket = [&](int64_t f, uint64_t sk) -> bool {
+    if (phase == 0) return sk >= bucket_lo && sk <= bucket_hi;
+    return sk == kx && (uint64_t)f >= bucket_lo && (uint64_t)f <= bucket_hi;
+  };
+  auto below = [&](int64_t f, uint64_t sk) -> bool {
+    if (phase == 0) return sk < bucket_lo;
+    return sk < kx || (sk == kx && (uint64_t)f < bucket_lo);
+  };
+  for (int64_t f = tid; f < total; f += blockDim.x) {
+    uint64_t sk = f64_key(sscore[f]);
+    if (in_bucket(f, sk)) {
+      uint32_t p = atomicAdd(&s_nbk, 1u);
+      bkey[p] = sk;
+      bval[p] = (uint32_t)f;
+    }
+  }
+  __syncthreads();
+  const uint32_t nbk = s_nbk;
+  const uint32_t np2 = next_pow2(max(nbk, 1u));
+  for (uint32_t i = nbk + tid; i < np2; i += blockDim.x) { bkey[i] = kKeyPad; bval[i] = 0xffffffffu; }
+  __syncthreads();
+  bitonic_sort(bkey, bval, np2);
+  if (tid == 0) {
+    uint64_t cnt = taken_c, w = taken_w, begun = 0, scanned = 0;
+    for (uint32_t i = 0; i < nbk; ++i) {
+      blen[i] = 0;
+      if (cnt >= kept || w >= budget) continue;
+      int64_t f = bval[i];
+      int p = (int)(f / G), j = (int)(f % G);
+      uint64_t sz = (uint64_t)ix.gsize[(int64_t)reg[p] * G + j];
+      uint64_t l = min(sz, budget - w);
+      blen[i] = (int32_t)l;
+      begun += 1;
+      scanned += l;
+      w += sz;
+      cnt += 1;
+    }
+    s_walk_begun = (int)begun;
+    s_walk_w = scanned;
+  }
+  __syncthreads();
+
+  // ---- 4. emit the work list (local rows of this shard)
+  auto emit = [&](int64_t f, int64_t len_g) {
+    int p = (int)(f / G), j = (int)(f % G);
+    int64_t gi = (int64_t)reg[p] * G + j;
+    int64_t lo_ = ix.llo ? ix.llo[gi] : 0;
+    int64_t cnt_ = ix.lsize ? ix.lsize[gi] : ix.gsize[gi];
+    int64_t ll = min(max(len_g - lo_, (int64_t)0), cnt_);
+    if (ll <= 0) return;
+    int pos = atomicAdd(&s_nemit, 1);
+    if (pos >= a.cap_w) return;  // cannot happen: cap_w bounds the begun items
+    WorkItem w;
+    w.start = ix.lstart[gi];
+    w.len = (int32_t)ll;
+    w.flat = (int32_t)f;
+    w.base = sbase[f];
+    w.score = sscore[f];
+    a.work[(int64_t)b * a.cap_w + pos] = w;
+  };
+  for (int64_t f = tid; f < total; f += blockDim.x) {
+    uint64_t sk = f64_key(sscore[f]);
+    if (below(f, sk)) {
+      int p = (int)(f / G), j = (int)(f % G);
+      emit(f, ix.gsize[(int64_t)reg[p] * G + j]);
+    }
+  }
+  for (uint32_t i = tid; i < nbk; i += blockDim.x)
+    if (blen[i] > 0) emit(bval[i], blen[i]);
+  __syncthreads();
+  const int nemit = min(s_nemit, (int)a.cap_w);
+  if (tid == 0) {
+    a.nwork[b] = nemit;
+    int64_t* st = a.stats + (int64_t)b * 4;
+    st[0] = P;
+    st[1] = (int64_t)taken_c + s_walk_begun;
+    st[2] = total - (int64_t)kept;
+    st[3] = (int64_t)taken_w + (int64_t)s_walk_w;
+  }
+
+  // ---- 5. rerank=False: reference scan order (score, pos, grp) of the list
+  if (a.sort_work) {
+    uint32_t wp2 = next_pow2(max(nemit, 1));
+    int64_t cp2 = 1;
+    while (cp2 < a.cap_w) cp2 <<= 1;
+    uint64_t* sk = a.skey + (int64_t)b * cp2;
+    uint32_t* sv = a.sval + (int64_t)b * cp2;
+    const WorkItem* W = a.work + (int64_t)b * a.cap_w;
+    for (uint32_t i = tid; i < wp2; i += blockDim.x) {
+      if ((int)i < nemit) {
+        // flat is unique per item: (score key, flat) is a total order
+        sk[i] = f64_key(W[i].score);
+        sv[i] = ((uint32_t)W[i].flat);
+      } else {
+        sk[i] = kKeyPad;
+        sv[i] = 0xffffffffu;
+      }
+    }
+    __syncthreads();
+    bitonic_sort(sk, sv, wp2);
+    // map sorted flat ids back to work-list positions
+    for (int i = tid; i < nemit; i += blockDim.x) {
+      // binary search of W's flat in the sorted (sk, sv) list
+      uint64_t key = f64_key(W[i].score);
+      uint32_t fl = (uint32_t)W[i].flat;
+      int lo_i = 0, hi_i = nemit - 1;
+      while (lo_i < hi_i) {
+        int mid = (lo_i + hi_i) >> 1;
+        bool less = sk[mid] < key || (sk[mid] == key && sv[mid] < fl);
+        if (less) lo_i = mid + 1; else hi_i = mid;
+      }
+      a.order[(int64_t)b * a.cap_w + lo_i] = i;
+    }
+  }
+}
+
+size_t plan_smem(int d) {
+  return (size_t)PLAN_BUCKETS * 8 + SORTCAP * 8 + PLAN_BUCKETS * 4 + SORTCAP * 4 + SORTCAP * 4 +
+         (size_t)d * 8 + 16;
+}
+
+void launch_plan(const PlanArgs& a, cudaStream_t s) {
+  size_t sm = plan_smem(a.ix.d);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    attr = true;
+  }
+  k_plan<<<a.nq, PLAN_THREADS, sm, s>>>(a);
+}
+
+}  // namespace givf

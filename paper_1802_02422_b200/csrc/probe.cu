@@ -1,0 +1,388 @@
+// K1 + K2: region probe (reference: search.py:77-90, graph.py:357-383).
+//
+// The reference ranks regions by exact float64 squared distance (its
+// ef_search == K configuration).  Computing all K*d
+// differences in float64 is wasteful, so the probe runs in three steps:
+//
+//   K1a  probe_gemm    approximate f32 scores  s~ = |c|^2 - 2 q.c  (B x K)
+//   K1b  probe_select  per query, a candidate set S = {k : s~_k < theta}
+//                      with Tmin <= |S| <= CAP (bucketed radix refinement)
+//   K2   probe_recheck exact float64 difference-form distances on S, the
+//                      exact top-P by (d64, id), an a-priori error bound check
+//                      that nothing outside S can enter the top-P, and the
+//                      reference's output order (f32(d64), id) + qc2 = d64.
+//
+// Queries whose bound check fails (near-ties at the S boundary) and the
+// nprobe == K branch go through probe_full, which ranks all K regions
+// exactly.  The result is bit-identical to the oracle's probe_exact by
+// construction, whatever the approximation error of K1a.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace givf {
+
+// ----------------------------------------------------------------- K1a
+// SIMT fp32 tile GEMM: 64 queries x 128 centroids per CTA, 256 threads,
+// 4x8 outputs per thread, d in chunks of 16 through shared memory.
+constexpr int PG_BM = 64, PG_BN = 128, PG_BK = 16;
+
+__global__ void __launch_bounds__(256)
+k_probe_gemm(const float* __restrict__ Q, const float* __restrict__ C,
+             const float* __restrict__ c2, int nq, int K, int d,
+             float* __restrict__ D, int64_t ldD) {
+  __shared__ float As[PG_BK][PG_BM + 4];
+  __shared__ float Bs[PG_BK][PG_BN + 4];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int q0 = blockIdx.y * PG_BM, c0 = blockIdx.x * PG_BN;
+  float acc[4][8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+
+  for (int k0 = 0; k0 < d; k0 += PG_BK) {
+    // Q tile: 64 x 16 -> 4 per thread; C tile: 128 x 16 -> 8 per thread.
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      int e = tid + t * 256;
+      int r = e >> 4, kk = e & 15;
+      int qr = q0 + r, dk = k0 + kk;
+      As[kk][r] = (qr < nq && dk < d) ? Q[(int64_t)qr * d + dk] : 0.f;
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      int e = tid + t * 256;
+      int r = e >> 4, kk = e & 15;
+      int cr = c0 + r, dk = k0 + kk;
+      Bs[kk][r] = (cr < K && dk < d) ? C[(int64_t)cr * d + dk] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < PG_BK; ++kk) {
+      float a[4], b[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) b[j] = Bs[kk][tx * 8 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int qr = q0 + ty * 4 + i;
+    if (qr >= nq) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      int cr = c0 + tx * 8 + j;
+      if (cr < K) D[(int64_t)qr * ldD + cr] = fmaf(-2.f, acc[i][j], c2[cr]);
+    }
+  }
+}
+
+// ----------------------------------------------------------------- K1b
+// Per query: candidate set S = {k : key(s~_k) < boundary}, Tmin <= |S| <= CAP,
+// found by <= 3 levels of 2048-bucket histograms over the order-preserving
+// u32 keys.  theta = smallest excluded score (+inf when nothing excluded).
+constexpr int SEL_THREADS = 512;
+constexpr int SEL_BUCKETS = 2048;
+
+__global__ void __launch_bounds__(SEL_THREADS)
+k_probe_select(const float* __restrict__ D, int64_t ldD, int K, int Tmin, int cap,
+               int* __restrict__ cand, int* __restrict__ cand_n,
+               float* __restrict__ theta) {
+  __shared__ uint32_t hist[SEL_BUCKETS];
+  __shared__ uint32_t red[40];
+  __shared__ uint32_t s_b, s_before, s_through;
+  __shared__ uint32_t cnt_lt, cnt_eq;
+  const float* row = D + (int64_t)blockIdx.x * ldD;
+  int* out = cand + (int64_t)blockIdx.x * cap;
+  const int tid = threadIdx.x;
+
+  if (K <= cap) {
+    for (int i = tid; i < K; i += blockDim.x) out[i] = i;
+    if (tid == 0) { cand_n[blockIdx.x] = K; theta[blockIdx.x] = __int_as_float(0x7f800000); }
+    return;
+  }
+  uint32_t mn = 0xffffffffu, mx = 0u;
+  for (int i = tid; i < K; i += blockDim.x) {
+    uint32_t k = f32_key(row[i]);
+    mn = min(mn, k); mx = max(mx, k);
+  }
+  uint32_t lo = block_min(mn, red), hi = block_max(mx, red);
+  uint32_t taken = 0, need = (uint32_t)Tmin;
+  uint64_t boundary = (uint64_t)hi + 1;
+  bool degenerate = false;
+  uint32_t deg_key = 0, deg_before = 0;
+
+  for (int level = 0; level < 4; ++level) {
+    uint32_t range = hi - lo;
+    int shift = range == 0 ? 0 : max(0, 32 - __clz(range) - 11);
+    uint32_t nb = (range >> shift) + 1;
+    for (uint32_t i = tid; i < nb; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (int i = tid; i < K; i += blockDim.x) {
+      uint32_t k = f32_key(row[i]);
+      if (k >= lo && k <= hi) atomicAdd(&hist[(k - lo) >> shift], 1u);
+    }
+    __syncthreads();
+    // each thread owns a contiguous run of buckets; scan run totals
+    const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;
+    uint32_t b0 = tid * per, b1 = min(nb, b0 + per), run = 0;
+    for (uint32_t b = b0; b < b1; ++b) run += hist[b];
+    uint32_t tot;
+    uint32_t pre = block_exclusive_scan(run, red, &tot);
+    if (tid == 0) s_b = 0xffffffffu;
+    __syncthreads();
+    if (b0 < b1 && pre < need && pre + run >= need) {
+      uint32_t c = pre;
+      for (uint32_t b = b0; b < b1; ++b) {
+        if (c + hist[b] >= need) { s_b = b; s_before = c; s_through = c + hist[b]; break; }
+        c += hist[b];
+      }
+    }
+    __syncthreads();
+    uint32_t b = s_b, before = s_before, through = s_through;
+    __syncthreads();
+    if (taken + through <= (uint32_t)cap) {
+      boundary = (uint64_t)lo + ((uint64_t)(b + 1) << shift);
+      break;
+    }
+    if (shift == 0) {  // one key value holds more than cap elements
+      degenerate = true;
+      deg_key = lo + b;
+      deg_before = taken + before;
+      boundary = deg_key;
+      break;
+    }
+    taken += before;
+    need -= before;
+    lo = lo + (b << shift);
+    uint64_t nhi = (uint64_t)lo + ((1ull << shift) - 1);
+    hi = (uint32_t)(nhi < (uint64_t)hi ? nhi : (uint64_t)hi);
+  }
+
+  if (tid == 0) { cnt_lt = 0; cnt_eq = 0; }
+  __syncthreads();
+  uint32_t ex = 0xffffffffu;
+  for (int i = tid; i < K; i += blockDim.x) {
+    uint32_t k = f32_key(row[i]);
+    if ((uint64_t)k < boundary) {
+      out[atomicAdd(&cnt_lt, 1u)] = i;
+    } else if (degenerate && k == deg_key) {
+      uint32_t p = atomicAdd(&cnt_eq, 1u);
+      if (deg_before + p < (uint32_t)cap) out[deg_before + p] = i;
+      else ex = min(ex, k);
+    } else {
+      ex = min(ex, k);
+    }
+  }
+  ex = block_min(ex, red);
+  if (tid == 0) {
+    uint32_t n = cnt_lt + (degenerate ? min(cnt_eq, (uint32_t)cap - deg_before) : 0u);
+    cand_n[blockIdx.x] = (int)n;
+    theta[blockIdx.x] = ex == 0xffffffffu ? __int_as_float(0x7f800000) : key_f32(ex);
+  }
+}
+
+// ----------------------------------------------------------------- K2
+GIVF_DEV double key_f64(uint64_t k) {
+  uint64_t u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)u);
+}
+
+// Warp-cooperative float64 squared difference |c - q|^2; lanes stride the
+// dimension, then a fixed xor-tree.  f32diff selects the nprobe == K formula
+// (difference rounded to f32 first, search.py:82).
+GIVF_DEV double warp_sqdist64(const float* __restrict__ c, const double* qd,
+                              const float* qf, int d, bool f32diff) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int j = lane; j < d; j += 32) {
+    double t;
+    if (f32diff) t = (double)__fsub_rn(c[j], qf[j]);
+    else t = dsub((double)c[j], qd[j]);
+    s = dadd(s, dmul(t, t));
+  }
+  return warp_sum(s);
+}
+
+// Emit the first P of the (d64, id)-sorted pairs.  f32order reorders them by
+// (f32(d64), id) as graph.py:380-382 does for nprobe < K; otherwise the
+// (d64, id) order of search.py:83 is kept.  qc2 = the float64 distance.
+__device__ void emit_probe(const uint64_t* skey, const uint32_t* sval, int P, bool f32order,
+                           uint64_t* k2, uint32_t* v2, double* dv,
+                           int* regions_out, double* qc2_out) {
+  if (!f32order) {
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+      regions_out[i] = (int)sval[i];
+      qc2_out[i] = key_f64(skey[i]);
+    }
+    __syncthreads();
+    return;
+  }
+  const uint32_t np2 = next_pow2((uint32_t)P);
+  for (uint32_t i = threadIdx.x; i < np2; i += blockDim.x) {
+    if (i < (uint32_t)P) {
+      double d64 = key_f64(skey[i]);
+      dv[i] = d64;
+      k2[i] = ((uint64_t)f32_key((float)d64) << 32) | sval[i];
+      v2[i] = i;
+    } else {
+      k2[i] = kKeyPad;
+      v2[i] = 0xffffffffu;
+    }
+  }
+  __syncthreads();
+  bitonic_sort(k2, v2, np2);
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    uint32_t src = v2[i];
+    regions_out[i] = (int)sval[src];
+    qc2_out[i] = dv[src];
+  }
+  __syncthreads();
+}
+
+// smem: qd[d] f64, qf[d] f32, key[capp2] u64, val[capp2] u32, k2/v2/dv for P.
+__global__ void __launch_bounds__(256)
+k_probe_recheck(const float* __restrict__ Q, const float* __restrict__ C, int K, int d,
+                int P, const int* __restrict__ cand, const int* __restrict__ cand_n,
+                int cap, const float* __restrict__ theta, float cmax, float eps_scale,
+                int* __restrict__ regions, double* __restrict__ qc2, int* __restrict__ fail) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int capp2 = (int)next_pow2((uint32_t)cap);
+  const int pp2 = (int)next_pow2((uint32_t)P);
+  double* qd = reinterpret_cast<double*>(smem);
+  double* dv = qd + d;
+  uint64_t* key = reinterpret_cast<uint64_t*>(dv + pp2);
+  uint64_t* k2 = key + capp2;
+  uint32_t* val = reinterpret_cast<uint32_t*>(k2 + pp2);
+  uint32_t* v2 = val + capp2;
+  float* qf = reinterpret_cast<float*>(v2 + pp2);
+  __shared__ double red[40];
+
+  const int b = blockIdx.x;
+  const float* q = Q + (int64_t)b * d;
+  double q2p = 0.0;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    qf[j] = q[j];
+    qd[j] = (double)q[j];
+    q2p += (double)q[j] * (double)q[j];
+  }
+  double q2 = block_sum(q2p, red);  // also syncs qd/qf
+  const int n = cand_n[b];
+  const int* cb = cand + (int64_t)b * cap;
+  const uint32_t np2 = next_pow2((uint32_t)max(n, 1));
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
+  for (int i = warp; i < n; i += nw) {
+    int id = cb[i];
+    double s = warp_sqdist64(C + (int64_t)id * d, qd, qf, d, false);
+    if (lane == 0) { key[i] = f64_key(s); val[i] = (uint32_t)id; }
+  }
+  for (uint32_t i = n + threadIdx.x; i < np2; i += blockDim.x) { key[i] = kKeyPad; val[i] = 0xffffffffu; }
+  __syncthreads();
+  bitonic_sort(key, val, np2);
+
+  if (n < K) {
+    // a priori bound on |s~ - (|c|^2 - 2 q.c)| for the fp32 GEMM of K1a
+    double qn = sqrt(q2);
+    double eps = (double)eps_scale * ((double)cmax * cmax + 2.0 * qn * cmax) +
+                 1e-12 * ((double)cmax + qn) * ((double)cmax + qn);
+    double dp = key_f64(key[P - 1]);
+    double th = (double)theta[b];
+    bool ok = (n >= P) && (dp - q2 < th - eps);
+    if (!ok) {
+      if (threadIdx.x == 0) fail[b] = 1;
+      return;
+    }
+  }
+  if (threadIdx.x == 0) fail[b] = 0;
+  emit_probe(key, val, P, true, k2, v2, dv, regions + (int64_t)b * P, qc2 + (int64_t)b * P);
+}
+
+// Exhaustive exact ranking of all K regions for one query per loop step:
+// mode 0 = nprobe == K branch (f32 differences, order (d, id));
+// mode 1 = fallback for queries flagged by k_probe_recheck.
+// Scratch per CTA: kp2 u64 keys + kp2 u32 vals (+ P-sized emit buffers).
+__global__ void __launch_bounds__(256)
+k_probe_full(const float* __restrict__ Q, const float* __restrict__ C, int nq, int K, int d,
+             int P, int mode, const int* __restrict__ fail,
+             uint64_t* __restrict__ scratch_key, uint32_t* __restrict__ scratch_val,
+             uint64_t* __restrict__ scratch_k2, uint32_t* __restrict__ scratch_v2,
+             double* __restrict__ scratch_dv,
+             int* __restrict__ regions, double* __restrict__ qc2) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* qd = reinterpret_cast<double*>(smem);
+  float* qf = reinterpret_cast<float*>(qd + d);
+  const uint32_t kp2 = next_pow2((uint32_t)K);
+  const uint32_t pp2 = next_pow2((uint32_t)P);
+  uint64_t* key = scratch_key + (int64_t)blockIdx.x * kp2;
+  uint32_t* val = scratch_val + (int64_t)blockIdx.x * kp2;
+  uint64_t* k2 = scratch_k2 + (int64_t)blockIdx.x * pp2;
+  uint32_t* v2 = scratch_v2 + (int64_t)blockIdx.x * pp2;
+  double* dv = scratch_dv + (int64_t)blockIdx.x * pp2;
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
+  const bool f32diff = mode == 0;
+
+  for (int b = blockIdx.x; b < nq; b += gridDim.x) {
+    if (mode == 1 && fail[b] == 0) continue;
+    const float* q = Q + (int64_t)b * d;
+    for (int j = threadIdx.x; j < d; j += blockDim.x) { qf[j] = q[j]; qd[j] = (double)q[j]; }
+    __syncthreads();
+    for (int i = warp; i < K; i += nw) {
+      double s = warp_sqdist64(C + (int64_t)i * d, qd, qf, d, f32diff);
+      if (lane == 0) { key[i] = f64_key(s); val[i] = (uint32_t)i; }
+    }
+    for (uint32_t i = K + threadIdx.x; i < kp2; i += blockDim.x) { key[i] = kKeyPad; val[i] = 0xffffffffu; }
+    __syncthreads();
+    bitonic_sort(key, val, kp2);
+    emit_probe(key, val, P, !f32diff, k2, v2, dv, regions + (int64_t)b * P, qc2 + (int64_t)b * P);
+  }
+}
+
+// ----------------------------------------------------------------- launchers
+void launch_probe_gemm(const float* Q, const float* C, const float* c2, int nq, int K, int d,
+                       float* D, int64_t ldD, cudaStream_t s) {
+  dim3 grid((K + PG_BN - 1) / PG_BN, (nq + PG_BM - 1) / PG_BM);
+  k_probe_gemm<<<grid, 256, 0, s>>>(Q, C, c2, nq, K, d, D, ldD);
+}
+
+void launch_probe_select(const float* D, int64_t ldD, int nq, int K, int Tmin, int cap,
+                         int* cand, int* cand_n, float* theta, cudaStream_t s) {
+  k_probe_select<<<nq, SEL_THREADS, 0, s>>>(D, ldD, K, Tmin, cap, cand, cand_n, theta);
+}
+
+size_t probe_recheck_smem(int d, int P, int cap) {
+  size_t capp2 = 1, pp2 = 1;
+  while (capp2 < (size_t)cap) capp2 <<= 1;
+  while (pp2 < (size_t)P) pp2 <<= 1;
+  return d * 8 + pp2 * 8 + capp2 * 8 + pp2 * 8 + capp2 * 4 + pp2 * 4 + d * 4 + 16;
+}
+
+void launch_probe_recheck(const float* Q, const float* C, int nq, int K, int d, int P,
+                          const int* cand, const int* cand_n, int cap, const float* theta,
+                          float cmax, float eps_scale, int* regions, double* qc2, int* fail,
+                          cudaStream_t s) {
+  size_t sm = probe_recheck_smem(d, P, cap);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_probe_recheck, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_probe_recheck<<<nq, 256, sm, s>>>(Q, C, K, d, P, cand, cand_n, cap, theta, cmax, eps_scale,
+                                      regions, qc2, fail);
+}
+
+void launch_probe_full(const float* Q, const float* C, int nq, int K, int d, int P, int mode,
+                       const int* fail, int nslots, uint64_t* sk, uint32_t* sv, uint64_t* sk2,
+                       uint32_t* sv2, double* sdv, int* regions, double* qc2, cudaStream_t s) {
+  size_t sm = (size_t)d * 12 + 16;
+  k_probe_full<<<nslots, 256, sm, s>>>(Q, C, nq, K, d, P, mode, fail, sk, sv, sk2, sv2, sdv,
+                                       regions, qc2);
+}
+
+}  // namespace givf

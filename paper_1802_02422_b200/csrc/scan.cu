@@ -1,0 +1,411 @@
+// K5 + K6 + K7 + K8: LUT, ADC scan with top-k, full rerank, scan-order
+// output, and the multi-shard top-k merge.
+//
+// Reference: pq.build_lookup_table (pq.py:147-169, inner mode, rotation at
+// pq.py:37-41), pq.lookup_code_sums (pq.py:172-177), the distance of
+// search.py:142-148 and the rerank of search.py:156-161.
+//
+//  * LUT: M x 256 float32 in shared memory, built per query by the same CTA
+//    that scans (entries accumulated in float64, rounded once).
+//  * ip = sum of M LUT entries in float32 in numpy's reduction order
+//    (8 running lanes, r_j = e_j + e_{j+8} + ..., then
+//    ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), tail added in order; M < 8 is a
+//    plain left-to-right sum) -- verified against numpy in tests.
+//  * dist = f32( f64(base) - 2*f64(ip) + f64(const) ), separately rounded.
+//  * The work list is consumed in windows of <= 256 segments / CHUNK codes;
+//    lanes map to consecutive code rows, so code (M-byte) and constant
+//    (1-byte) loads are coalesced 16/8/4-byte vectors.
+//  * top-k: a shared-memory candidate buffer filtered by a running
+//    (dist, id) threshold; ids are loaded only for candidates.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace givf {
+
+constexpr int SCAN_THREADS = 256;
+constexpr int CHUNK = 2048;
+constexpr int WIN = SCAN_THREADS;
+
+template <int M>
+struct CodeSum {
+  // generic M: numpy pairwise order over an M-element row
+  static GIVF_DEV float run(const uint8_t* __restrict__ code, const float* lut) {
+    float e[M];
+#pragma unroll
+    for (int j = 0; j < M; ++j) e[j] = lut[j * 256 + code[j]];
+    if (M < 8) {
+      float r = e[0];
+#pragma unroll
+      for (int j = 1; j < M; ++j) r = __fadd_rn(r, e[j]);
+      return r;
+    }
+    float r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = e[j];
+    constexpr int body = M - (M % 8);
+#pragma unroll
+    for (int i = 8; i < body; i += 8)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = __fadd_rn(r[j], e[i + j]);
+    float s = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
+                        __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+#pragma unroll
+    for (int j = body; j < M; ++j) s = __fadd_rn(s, e[j]);
+    return s;
+  }
+};
+
+template <int M>
+GIVF_DEV float code_ip(const uint8_t* __restrict__ codes, int64_t row, const float* lut) {
+  if constexpr (M == 16) {
+    uint4 v = __ldg(reinterpret_cast<const uint4*>(codes + row * 16));
+    uint8_t c[16];
+    *reinterpret_cast<uint4*>(c) = v;
+    return CodeSum<16>::run(c, lut);
+  } else if constexpr (M == 8) {
+    uint2 v = __ldg(reinterpret_cast<const uint2*>(codes + row * 8));
+    uint8_t c[8];
+    *reinterpret_cast<uint2*>(c) = v;
+    return CodeSum<8>::run(c, lut);
+  } else if constexpr (M == 4) {
+    uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(codes + row * 4));
+    uint8_t c[4];
+    *reinterpret_cast<uint32_t*>(c) = v;
+    return CodeSum<4>::run(c, lut);
+  } else if constexpr (M == 32) {
+    const uint4* p = reinterpret_cast<const uint4*>(codes + row * 32);
+    uint8_t c[32];
+    *reinterpret_cast<uint4*>(c) = __ldg(p);
+    *reinterpret_cast<uint4*>(c + 16) = __ldg(p + 1);
+    return CodeSum<32>::run(c, lut);
+  } else {
+    uint8_t c[M];
+#pragma unroll
+    for (int j = 0; j < M; ++j) c[j] = __ldg(codes + row * M + j);
+    return CodeSum<M>::run(c, lut);
+  }
+}
+
+// Shared memory layout of k_scan (dynamic):
+//   lut f32[M*256] | ctab f64[256] | qrot f32[d] | wstart i64[WIN] | wbase f64[WIN]
+//   | woff i32[WIN] | wlen i32[WIN] | rowv i64[CHUNK] | segv u16[CHUNK] | buf u64[bufcap]
+struct ScanSmem {
+  float* lut;
+  double* ctab;
+  float* qrot;
+  int64_t* wstart;
+  double* wbase;
+  int32_t* woff;
+  int32_t* wlen;
+  int64_t* rowv;
+  uint16_t* segv;
+  uint64_t* buf;
+};
+
+GIVF_DEV ScanSmem carve(unsigned char* p, int M, int d) {
+  ScanSmem s;
+  s.lut = reinterpret_cast<float*>(p);
+  s.ctab = reinterpret_cast<double*>(s.lut + M * 256);
+  s.qrot = reinterpret_cast<float*>(s.ctab + 256);
+  size_t off = (size_t)M * 256 * 4 + 256 * 8 + (((size_t)d * 4 + 15) & ~(size_t)15);
+  s.wstart = reinterpret_cast<int64_t*>(p + off);
+  s.wbase = reinterpret_cast<double*>(s.wstart + WIN);
+  s.woff = reinterpret_cast<int32_t*>(s.wbase + WIN);
+  s.wlen = s.woff + WIN;
+  s.rowv = reinterpret_cast<int64_t*>(s.wlen + WIN);
+  s.segv = reinterpret_cast<uint16_t*>(s.rowv + CHUNK);
+  s.buf = reinterpret_cast<uint64_t*>(s.segv + CHUNK);
+  return s;
+}
+
+static size_t scan_smem_bytes(int M, int d, int bufcap) {
+  return (size_t)M * 256 * 4 + 256 * 8 + (((size_t)d * 4 + 15) & ~(size_t)15) + WIN * 8 + WIN * 8 +
+         WIN * 4 + WIN * 4 + CHUNK * 8 + CHUNK * 2 + (size_t)bufcap * 8 + 64;
+}
+
+// LUT of one query (pq.py:147-169): optional rotation q' = R q, then
+// entry[m][i] = <q'_m, codeword[m][i]>.
+__device__ void build_lut(const IndexView& ix, const float* __restrict__ q, ScanSmem& s) {
+  const int d = ix.d, M = ix.M, ds = d / M;
+  if (ix.rotation) {
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+      const float* r = ix.rotation + (int64_t)i * d;
+      double acc = 0.0;
+      for (int j = 0; j < d; ++j) acc += (double)r[j] * (double)q[j];
+      s.qrot[i] = (float)acc;
+    }
+  } else {
+    for (int i = threadIdx.x; i < d; i += blockDim.x) s.qrot[i] = q[i];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < M * 256; e += blockDim.x) {
+    int m = e >> 8;
+    const float* cw = ix.codewords + (int64_t)e * ds;
+    const float* qq = s.qrot + m * ds;
+    double acc = 0.0;
+    for (int t = 0; t < ds; ++t) acc += (double)cw[t] * (double)qq[t];
+    s.lut[e] = (float)acc;
+  }
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) s.ctab[i] = (double)ix.ctab[i];
+  __syncthreads();
+}
+
+template <int M>
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan(ScanArgs a, int bufcap) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const IndexView& ix = a.ix;
+  ScanSmem s = carve(dsm, M, ix.d);
+  __shared__ int32_t red32[40];
+  __shared__ int s_count;
+  __shared__ unsigned long long s_thr;
+  __shared__ int s_nfit;
+  const int b = blockIdx.x, tid = threadIdx.x;
+
+  build_lut(ix, a.Q + (int64_t)b * ix.d, s);
+  if (tid == 0) { s_count = 0; s_thr = kKeyPad; }
+  __syncthreads();
+
+  const WorkItem* W = a.work + (int64_t)b * a.cap_w;
+  const int nseg = a.nwork[b];
+  uint64_t* fk = a.mode == 1 ? a.full_keys + (int64_t)b * a.cap_full_p2 : nullptr;
+  int64_t code_base = 0;
+
+  auto process = [&](int64_t row, double base, int64_t pos) {
+    float ip = code_ip<M>(ix.codes, row, s.lut);
+    double c = s.ctab[__ldg(ix.cbytes + row)];
+    float dist = (float)dadd(dsub(base, 2.0 * (double)ip), c);
+    if (a.mode == 1) {
+      fk[pos] = dist_id_key(dist, __ldg(ix.pids + row));
+    } else {
+      uint32_t dk = f32_key(dist);
+      unsigned long long thr = *((volatile unsigned long long*)&s_thr);
+      if (dk <= (uint32_t)(thr >> 32)) {
+        uint64_t key = ((uint64_t)dk << 32) | (uint32_t)__ldg(ix.pids + row);
+        if (key < thr) s.buf[atomicAdd(&s_count, 1)] = key;
+      }
+    }
+  };
+  // keep room for one more chunk of appends
+  auto maybe_shrink = [&]() {
+    __syncthreads();
+    int cnt = s_count;
+    if (a.mode == 0 && cnt > bufcap - CHUNK) {
+      uint32_t np2 = next_pow2((uint32_t)cnt);
+      for (uint32_t i = cnt + tid; i < np2; i += blockDim.x) s.buf[i] = kKeyPad;
+      __syncthreads();
+      bitonic_sort_keys(s.buf, np2);
+      if (tid == 0) {
+        int keep = min(cnt, a.k);
+        s_count = keep;
+        s_thr = keep == a.k ? s.buf[a.k - 1] : kKeyPad;
+      }
+      __syncthreads();
+    }
+  };
+
+  for (int seg0 = 0; seg0 < nseg;) {
+    const bool valid = seg0 + tid < nseg;
+    int len = 0;
+    WorkItem w;
+    if (valid) { w = W[seg0 + tid]; len = w.len; }
+    int tot;
+    int off = block_exclusive_scan(len, red32, &tot);
+    const bool fits = valid && off + len <= CHUNK;
+    if (fits) { s.wstart[tid] = w.start; s.wbase[tid] = w.base; s.woff[tid] = off; s.wlen[tid] = len; }
+    if (tid == 0) s_nfit = 0;
+    __syncthreads();
+    if (fits) atomicAdd(&s_nfit, 1);
+    if (tid == 0 && !fits && valid && off == 0) {  // first segment alone exceeds CHUNK
+      s.wstart[0] = w.start; s.wbase[0] = w.base; s.wlen[0] = len;
+    }
+    __syncthreads();
+    const int nfit = s_nfit;
+    if (nfit == 0) {
+      const int64_t st = s.wstart[0];
+      const double bs = s.wbase[0];
+      const int ln = s.wlen[0];
+      for (int piece = 0; piece < ln; piece += CHUNK) {
+        int n = min(CHUNK, ln - piece);
+        for (int v = tid; v < n; v += blockDim.x) process(st + piece + v, bs, code_base + piece + v);
+        maybe_shrink();
+      }
+      code_base += ln;
+      seg0 += 1;
+      continue;
+    }
+    const int chunk_total = s.woff[nfit - 1] + s.wlen[nfit - 1];
+    {
+      const int warp = tid >> 5, nw = blockDim.x >> 5, lane = tid & 31;
+      for (int sg = warp; sg < nfit; sg += nw) {
+        const int o = s.woff[sg], l = s.wlen[sg];
+        const int64_t st = s.wstart[sg];
+        for (int i = lane; i < l; i += 32) { s.rowv[o + i] = st + i; s.segv[o + i] = (uint16_t)sg; }
+      }
+    }
+    __syncthreads();
+    for (int v = tid; v < chunk_total; v += blockDim.x)
+      process(s.rowv[v], s.wbase[s.segv[v]], code_base + v);
+    maybe_shrink();
+    code_base += chunk_total;
+    seg0 += nfit;
+  }
+
+  if (a.mode == 0) {
+    __syncthreads();
+    const int cnt = s_count;
+    uint32_t np2 = next_pow2((uint32_t)max(cnt, 1));
+    for (uint32_t i = cnt + tid; i < np2; i += blockDim.x) s.buf[i] = kKeyPad;
+    __syncthreads();
+    bitonic_sort_keys(s.buf, np2);
+    for (int i = tid; i < a.k; i += blockDim.x) {
+      int32_t id = -1;
+      float dv = __int_as_float(0x7f800000);
+      if (i < cnt) {
+        uint64_t key = s.buf[i];
+        id = (int32_t)(uint32_t)key;
+        dv = key_f32((uint32_t)(key >> 32));
+      }
+      a.out_ids[(int64_t)b * a.k + i] = id;
+      a.out_d[(int64_t)b * a.k + i] = dv;
+    }
+  }
+}
+
+template <int M>
+static void launch_scan_m(const ScanArgs& a, cudaStream_t s) {
+  int bufcap = (int)next_pow2_host((uint32_t)((a.mode == 0 ? a.k : 0) + CHUNK));
+  size_t sm = scan_smem_bytes(M, a.ix.d, bufcap);
+  static size_t attr = 0;
+  if (attr < sm) {
+    cudaFuncSetAttribute(k_scan<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = sm;
+  }
+  k_scan<M><<<a.nq, SCAN_THREADS, sm, s>>>(a, bufcap);
+}
+
+void launch_scan(const ScanArgs& a, cudaStream_t s) {
+  switch (a.ix.M) {
+    case 1: launch_scan_m<1>(a, s); break;
+    case 2: launch_scan_m<2>(a, s); break;
+    case 3: launch_scan_m<3>(a, s); break;
+    case 4: launch_scan_m<4>(a, s); break;
+    case 6: launch_scan_m<6>(a, s); break;
+    case 8: launch_scan_m<8>(a, s); break;
+    case 12: launch_scan_m<12>(a, s); break;
+    case 16: launch_scan_m<16>(a, s); break;
+    case 24: launch_scan_m<24>(a, s); break;
+    case 32: launch_scan_m<32>(a, s); break;
+    case 48: launch_scan_m<48>(a, s); break;
+    case 64: launch_scan_m<64>(a, s); break;
+    default: break;  // rejected at index creation
+  }
+}
+
+// ------------------------------------------------------------ full rerank
+// Sort one query's (dist, id) keys (search.py:156-158) and split them.
+constexpr int FULL_SMEM_KEYS = 4096;
+
+__global__ void __launch_bounds__(512)
+k_full_finish(uint64_t* __restrict__ keys, int64_t cap_p2, const int64_t* __restrict__ stats,
+              int32_t* __restrict__ ids, float* __restrict__ dists, int64_t ld) {
+  __shared__ uint64_t sk[FULL_SMEM_KEYS];
+  const int b = blockIdx.x;
+  const int64_t n = stats[(int64_t)b * 4 + 3];
+  uint64_t* k = keys + (int64_t)b * cap_p2;
+  uint32_t np2 = next_pow2((uint32_t)(n > 1 ? n : 1));
+  uint64_t* work = np2 <= FULL_SMEM_KEYS ? sk : k;
+  for (uint32_t i = threadIdx.x; i < np2; i += blockDim.x) work[i] = i < n ? k[i] : kKeyPad;
+  __syncthreads();
+  bitonic_sort_keys(work, np2);
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    uint64_t key = work[i];
+    ids[(int64_t)b * ld + i] = (int32_t)(uint32_t)key;
+    dists[(int64_t)b * ld + i] = key_f32((uint32_t)(key >> 32));
+  }
+}
+
+void launch_full_finish(uint64_t* keys, int64_t cap_p2, const int64_t* stats, int nq,
+                        int32_t* ids, float* dists, int64_t ld, cudaStream_t s) {
+  k_full_finish<<<nq, 512, 0, s>>>(keys, cap_p2, stats, ids, dists, ld);
+}
+
+// ------------------------------------------------------------ rerank=False
+// Scan order: kept groups by (score, pos, grp), each group's rows in stored
+// (ascending id) order, every code carrying f32(score) (search.py:159-161).
+__global__ void __launch_bounds__(256)
+k_scan_order(IndexView ix, const WorkItem* __restrict__ work, int64_t cap_w,
+             const int* __restrict__ nwork, const int32_t* __restrict__ order,
+             int32_t* __restrict__ ids, float* __restrict__ dists, int64_t ld) {
+  __shared__ int32_t red[40];
+  __shared__ int64_t s_base;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const int n = nwork[b];
+  const WorkItem* W = work + (int64_t)b * cap_w;
+  const int32_t* O = order + (int64_t)b * cap_w;
+  if (tid == 0) s_base = 0;
+  __syncthreads();
+  for (int i0 = 0; i0 < n; i0 += blockDim.x) {
+    int i = i0 + tid;
+    WorkItem w;
+    int len = 0;
+    if (i < n) { w = W[O[i]]; len = w.len; }
+    int tot;
+    int off = block_exclusive_scan(len, red, &tot);
+    int64_t base = s_base;
+    for (int t = 0; t < len; ++t) {
+      int64_t row = w.start + t;
+      ids[(int64_t)b * ld + base + off + t] = ix.pids[row];
+      dists[(int64_t)b * ld + base + off + t] = (float)w.score;
+    }
+    __syncthreads();
+    if (tid == 0) s_base = base + tot;
+    __syncthreads();
+  }
+}
+
+void launch_scan_order(const IndexView& ix, const WorkItem* work, int64_t cap_w,
+                       const int* nwork, const int32_t* order, int nq, int32_t* ids,
+                       float* dists, int64_t ld, cudaStream_t s) {
+  k_scan_order<<<nq, 256, 0, s>>>(ix, work, cap_w, nwork, order, ids, dists, ld);
+}
+
+// ------------------------------------------------------------ K7 merge
+// Per query, the k smallest (dist, id) over G shard lists.
+__global__ void __launch_bounds__(256)
+k_merge_topk(const int32_t* __restrict__ ids, const float* __restrict__ dists, int G, int nq,
+             int k, int32_t* __restrict__ out_ids, float* __restrict__ out_d) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  uint64_t* key = reinterpret_cast<uint64_t*>(dsm);
+  const int b = blockIdx.x;
+  const uint32_t n = (uint32_t)G * k;
+  const uint32_t np2 = next_pow2(n);
+  for (uint32_t i = threadIdx.x; i < np2; i += blockDim.x) {
+    uint64_t v = kKeyPad;
+    if (i < n) {
+      int g = i / k, j = i % k;
+      int64_t src = ((int64_t)g * nq + b) * k + j;
+      int32_t id = ids[src];
+      if (id >= 0) v = dist_id_key(dists[src], id);
+    }
+    key[i] = v;
+  }
+  __syncthreads();
+  bitonic_sort_keys(key, np2);
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    uint64_t v = key[i];
+    bool ok = v != kKeyPad;
+    out_ids[(int64_t)b * k + i] = ok ? (int32_t)(uint32_t)v : -1;
+    out_d[(int64_t)b * k + i] = ok ? key_f32((uint32_t)(v >> 32)) : __int_as_float(0x7f800000);
+  }
+}
+
+void launch_merge_topk(const int32_t* ids, const float* dists, int G, int nq, int k,
+                       int32_t* out_ids, float* out_d, cudaStream_t s) {
+  uint32_t np2 = next_pow2_host((uint32_t)(G * k));
+  size_t sm = (size_t)np2 * 8;
+  if (sm > 48 * 1024)
+    cudaFuncSetAttribute(k_merge_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_merge_topk<<<nq, 256, sm, s>>>(ids, dists, G, nq, k, out_ids, out_d);
+}
+
+}  // namespace givf

@@ -1,0 +1,131 @@
+"""GPU parity: the CUDA path against the reference's own outputs (golden
+fixtures) and against the CPU oracle, stage by stage."""
+
+import numpy as np
+import pytest
+
+import golden_io
+from parity import assert_ranked_equal, assert_topk_equal
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", params=golden_io.NAMES)
+def fx(request):
+    return golden_io.load(request.param)
+
+
+def _params(p):
+    from paper_1802_02422_b200 import SearchParams
+
+    return SearchParams(nprobe=p.nprobe, tau=p.tau, candidates=p.candidates,
+                        ef_search=p.ef_search, rerank=p.rerank, prune=p.prune)
+
+
+def test_probe_matches_oracle(fx):
+    from oracle import search_oracle as so
+    from paper_1802_02422_b200 import probe
+
+    k = fx.index.centroids.shape[0]
+    for nprobe in sorted({1, 3, min(16, k), min(32, k), k // 2 or 1, k}):
+        regions, qc2 = probe(fx.index, fx.queries, nprobe)
+        for i, q in enumerate(fx.queries):
+            want_r, want_c = so.probe_exact(fx.index.centroids, q, nprobe)
+            np.testing.assert_array_equal(regions[i], want_r, err_msg=f"{fx.name} nprobe={nprobe} q={i}")
+            np.testing.assert_allclose(qc2[i], want_c, rtol=1e-12, atol=1e-14)
+
+
+def test_full_results_match_reference(fx):
+    """search() on the GPU vs the reference's search() output, every exact run."""
+    from paper_1802_02422_b200 import search_batch
+
+    for run in golden_io.exact_runs(fx):
+        res = search_batch(fx.index, fx.queries, _params(run.params))
+        for i, r in enumerate(res):
+            want_ids, want_d = run.results[i]
+            st = run.stats[i]
+            got = (r.stats.regions_visited, r.stats.subregions_visited,
+                   r.stats.subregions_pruned, r.stats.codes_scanned)
+            assert got == tuple(st), (fx.name, vars(run.params), i, got, tuple(st))
+            if run.params.rerank:
+                assert_ranked_equal(r.ids, r.distances, want_ids, want_d)
+            else:
+                # scan order is fully determined by the plan: exact ids
+                np.testing.assert_array_equal(r.ids, want_ids)
+                np.testing.assert_allclose(r.distances, want_d, rtol=1e-6, atol=1e-7)
+
+
+def test_single_query_search_matches_reference(fx):
+    from paper_1802_02422_b200 import search
+
+    run = golden_io.exact_runs(fx)[0]
+    for i in range(min(4, len(fx.queries))):
+        r = search(fx.index, fx.queries[i], _params(run.params))
+        want_ids, want_d = run.results[i]
+        if run.params.rerank:
+            assert_ranked_equal(r.ids, r.distances, want_ids, want_d)
+        else:
+            np.testing.assert_array_equal(r.ids, want_ids)
+
+
+def test_topk_matches_oracle(fx):
+    from oracle import search_oracle as so
+    from paper_1802_02422_b200 import search_batch
+
+    for run in golden_io.exact_runs(fx):
+        if not run.params.rerank:
+            continue
+        p = _params(run.params)
+        for k in (1, 10, 100):
+            ids, d, st = search_batch(fx.index, fx.queries, p, k=k)
+            want_i, want_d, want_s = so.search_topk(fx.index, fx.queries, so.Params(**vars(run.params)), k)
+            np.testing.assert_array_equal(st, want_s)
+            for i in range(len(fx.queries)):
+                assert_topk_equal(ids[i], d[i], want_i[i], want_d[i])
+
+
+def test_param_validation_messages():
+    from paper_1802_02422_b200 import SearchParams, search
+
+    fx = golden_io.load("small_grouped")
+    q = fx.queries[0]
+    for params, msg in [
+        (SearchParams(nprobe=0), "nprobe"), (SearchParams(nprobe=49), "nprobe"),
+        (SearchParams(tau=0.0), "tau"), (SearchParams(tau=1.5), "tau"),
+        (SearchParams(candidates=0), "candidates"), (SearchParams(ef_search=0), "ef_search"),
+    ]:
+        with pytest.raises(ValueError, match=msg):
+            search(fx.index, q, params)
+    with pytest.raises(ValueError, match="query dim"):
+        search(fx.index, q[:-1], SearchParams())
+
+
+def test_tau_one_equals_pruning_disabled():
+    from paper_1802_02422_b200 import SearchParams, search
+
+    fx = golden_io.load("small_grouped")
+    for nprobe, cand in ((4, 500), (16, 10**9), (48, 2500)):
+        on = SearchParams(nprobe=nprobe, tau=1.0, candidates=cand, prune=True, ef_search=48)
+        off = SearchParams(nprobe=nprobe, tau=1.0, candidates=cand, prune=False, ef_search=48)
+        for q in fx.queries[:8]:
+            assert search(fx.index, q, on).signature() == search(fx.index, q, off).signature()
+
+
+def test_kat_exact_point_first():
+    from paper_1802_02422_b200 import SearchParams, search
+
+    fx = golden_io.load("kat")
+    for i, q in enumerate(fx.queries[:3]):
+        r = search(fx.index, q, SearchParams(nprobe=300, tau=1.0, candidates=300))
+        want_ids, _ = fx.runs[0].results[i]
+        assert int(r.ids[0]) == int(want_ids[0])
+        assert float(r.distances[0]) == 0.0
+
+
+def test_deterministic_signatures():
+    from paper_1802_02422_b200 import SearchParams, search
+
+    fx = golden_io.load("c1like_m16")
+    p = SearchParams(nprobe=12, tau=0.7, candidates=900)
+    for q in fx.queries[:4]:
+        assert search(fx.index, q, p).signature() == search(fx.index, q, p).signature()
