@@ -26,7 +26,12 @@ EXPORTS = (
     "givf_probe",
     "givf_merge_topk",
     "givf_kernel_launches",
+    "givf_profile_enable",
+    "givf_profile_read",
 )
+
+STAGES = ("probe_gemm", "probe_select", "probe_recheck", "probe_full", "plan", "scan",
+          "finish", "merge")
 
 
 class IndexDesc(ctypes.Structure):
@@ -101,6 +106,8 @@ def load(path: str = LIB_PATH):
     lib.givf_probe.argtypes = [vp, vp, i64, i32, vp, vp, vp]
     lib.givf_merge_topk.argtypes = [vp, vp, i32, i64, i32, vp, vp, ctypes.c_int, vp]
     lib.givf_kernel_launches.restype = i64
+    lib.givf_profile_enable.argtypes = [ctypes.c_int]
+    lib.givf_profile_read.argtypes = [vp, vp, i32]
     _lib = lib
     return lib
 
@@ -123,3 +130,17 @@ def check(rc: int) -> None:
 
 def kernel_launches() -> int:
     return int(load().givf_kernel_launches())
+
+
+def profile_enable(on: bool = True) -> None:
+    load().givf_profile_enable(1 if on else 0)
+
+
+def profile_read() -> dict:
+    """{stage: (ms, launches)} since the last read (synchronises)."""
+    import numpy as np
+
+    ms = np.zeros(len(STAGES), np.float64)
+    cnt = np.zeros(len(STAGES), np.int64)
+    check(load().givf_profile_read(ms.ctypes.data, cnt.ctypes.data, len(STAGES)))
+    return {name: (float(ms[i]), int(cnt[i])) for i, name in enumerate(STAGES)}

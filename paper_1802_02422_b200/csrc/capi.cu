@@ -22,6 +22,47 @@ namespace {
 thread_local std::string g_err;
 std::atomic<int64_t> g_launches{0};
 
+// Per-stage device timing: CUDA events around every launch, on its stream.
+enum Stage { ST_GEMM, ST_SELECT, ST_RECHECK, ST_FULL, ST_PLAN, ST_SCAN, ST_FINISH, ST_MERGE, ST_N };
+struct Profiler {
+  std::mutex mu;
+  std::atomic<bool> on{false};
+  struct Rec {
+    int stage;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> pool;
+  double ms[ST_N] = {};
+  int64_t cnt[ST_N] = {};
+  cudaEvent_t ev() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+Profiler g_prof;
+
+template <class F>
+void staged(int stage, cudaStream_t st, F&& launch) {
+  g_launches += 1;
+  if (!g_prof.on.load()) {
+    launch();
+    return;
+  }
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  cudaEvent_t a = g_prof.ev(), b = g_prof.ev();
+  cudaEventRecord(a, st);
+  launch();
+  cudaEventRecord(b, st);
+  g_prof.pending.push_back({stage, a, b});
+}
+
 int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
@@ -109,7 +150,7 @@ cudaError_t upload(givf_index* ix, const T* host, size_t count, const T** out) {
   ix->allocs.push_back(d);
   ix->dev_bytes += (int64_t)bytes;
   if (count) {
-    e = cudaMemcpy(d, host, count * sizeof(T), cudaMemcpyHostToDevice);
+    e = cudaMemcpy(d, host, count * sizeof(T), cudaMemcpyDefault);  // host or device source
     if (e != cudaSuccess) return e;
   }
   *out = static_cast<const T*>(d);
@@ -206,9 +247,10 @@ int run_probe(givf_index* ix, const Plan& pl, const float* dQ, int nq, int* regi
     if (mode == 1) {
       CUDA_TRY(cudaMemsetAsync(failf, 0xff, sizeof(int) * nq, st));  // all "failed"
     }
-    launch_probe_full(dQ, v.centroids, nq, K, d, P, mode, failf, slots, sk, sv, sk2, sv2, sdv,
-                      regions, qc2, st);
-    g_launches += 1;
+    staged(ST_FULL, st, [&] {
+      launch_probe_full(dQ, v.centroids, nq, K, d, P, mode, failf, slots, sk, sv, sk2, sv2, sdv,
+                        regions, qc2, st);
+    });
     KCHECK();
     return GIVF_OK;
   }
@@ -216,14 +258,19 @@ int run_probe(givf_index* ix, const Plan& pl, const float* dQ, int nq, int* regi
   int* cand = ar.take<int>((size_t)nq * pl.ps.cap);
   int* cand_n = ar.take<int>(nq);
   float* theta = ar.take<float>(nq);
-  launch_probe_gemm(dQ, v.centroids, v.c2f, nq, K, d, D, K, st);
-  launch_probe_select(D, K, nq, K, pl.ps.Tmin, pl.ps.cap, cand, cand_n, theta, st);
+  staged(ST_GEMM, st, [&] { launch_probe_gemm(dQ, v.centroids, v.c2f, nq, K, d, D, K, st); });
+  staged(ST_SELECT, st, [&] {
+    launch_probe_select(D, K, nq, K, pl.ps.Tmin, pl.ps.cap, cand, cand_n, theta, st);
+  });
   const float eps_scale = 3.0f * (float)(d + 4) * 5.9604645e-8f;
-  launch_probe_recheck(dQ, v.centroids, nq, K, d, P, cand, cand_n, pl.ps.cap, theta, v.cmax,
-                       eps_scale, regions, qc2, failf, st);
-  launch_probe_full(dQ, v.centroids, nq, K, d, P, 1, failf, slots, sk, sv, sk2, sv2, sdv,
-                    regions, qc2, st);
-  g_launches += 4;
+  staged(ST_RECHECK, st, [&] {
+    launch_probe_recheck(dQ, v.centroids, nq, K, d, P, cand, cand_n, pl.ps.cap, theta, v.cmax,
+                         eps_scale, regions, qc2, failf, st);
+  });
+  staged(ST_FULL, st, [&] {
+    launch_probe_full(dQ, v.centroids, nq, K, d, P, 1, failf, slots, sk, sv, sk2, sv2, sdv,
+                      regions, qc2, st);
+  });
   KCHECK();
   return GIVF_OK;
 }
@@ -341,8 +388,7 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
       pa.sval = ar.take<uint32_t>((size_t)bq * cp2);
       pa.order = ar.take<int32_t>((size_t)bq * pl.cap_w);
     }
-    launch_plan(pa, st);
-    g_launches += 1;
+    staged(ST_PLAN, st, [&] { launch_plan(pa, st); });
     KCHECK();
 
     int32_t* oid;
@@ -370,17 +416,18 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
         sa.full_keys = ar.take<uint64_t>((size_t)bq * full_p2);
         sa.cap_full_p2 = full_p2;
       }
-      launch_scan(sa, st);
-      g_launches += 1;
+      staged(ST_SCAN, st, [&] { launch_scan(sa, st); });
       KCHECK();
       if (om == OUT_FULL) {
-        launch_full_finish(sa.full_keys, full_p2, dstats, bq, oid, od, width, st);
-        g_launches += 1;
+        staged(ST_FINISH, st, [&] {
+          launch_full_finish(sa.full_keys, full_p2, dstats, bq, oid, od, width, st);
+        });
         KCHECK();
       }
     } else {
-      launch_scan_order(v, pa.work, pl.cap_w, pa.nwork, pa.order, bq, oid, od, width, st);
-      g_launches += 1;
+      staged(ST_FINISH, st, [&] {
+        launch_scan_order(v, pa.work, pl.cap_w, pa.nwork, pa.order, bq, oid, od, width, st);
+      });
       KCHECK();
     }
     if (!out_dev) {
@@ -407,6 +454,31 @@ extern "C" {
 const char* givf_last_error(void) { return g_err.c_str(); }
 const char* givf_version(void) { return "givf_b200 0.1 (sm_100a)"; }
 int64_t givf_kernel_launches(void) { return g_launches.load(); }
+
+int givf_profile_enable(int on) {
+  g_prof.on.store(on != 0);
+  return GIVF_OK;
+}
+
+int givf_profile_read(double* stage_ms, int64_t* stage_launches, int32_t nstages) {
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  for (auto& r : g_prof.pending) {
+    CUDA_TRY(cudaEventSynchronize(r.b));
+    float t = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&t, r.a, r.b));
+    g_prof.ms[r.stage] += t;
+    g_prof.cnt[r.stage] += 1;
+    g_prof.pool.push_back(r.a);
+    g_prof.pool.push_back(r.b);
+  }
+  g_prof.pending.clear();
+  for (int i = 0; i < nstages && i < ST_N; ++i) {
+    if (stage_ms) stage_ms[i] = g_prof.ms[i];
+    if (stage_launches) stage_launches[i] = g_prof.cnt[i];
+  }
+  for (int i = 0; i < ST_N; ++i) { g_prof.ms[i] = 0; g_prof.cnt[i] = 0; }
+  return GIVF_OK;
+}
 
 int givf_index_create(const givf_index_desc* ds, int device, givf_index_t* out) {
   if (!ds || !out) return fail(GIVF_EINVAL, "null argument");
@@ -590,8 +662,9 @@ int givf_merge_topk(const int32_t* ids, const float* dists, int32_t shards, int6
     int bq = (int)std::min<int64_t>(65535, nq - q0);
     // shard lists are (shards, nq, k): offset rows of every shard
     if (q0 == 0 && bq == nq) {
-      launch_merge_topk(ids, dists, shards, (int)nq, k, out_ids, out_dists, (cudaStream_t)stream);
-      g_launches += 1;
+      staged(ST_MERGE, (cudaStream_t)stream, [&] {
+        launch_merge_topk(ids, dists, shards, (int)nq, k, out_ids, out_dists, (cudaStream_t)stream);
+      });
     } else {
       return fail(GIVF_EINVAL, "merge supports nq <= 65535 per call");
     }

@@ -81,7 +81,8 @@ def _vp(a) -> ctypes.c_void_p:
     return ctypes.c_void_p(a.ctypes.data)
 
 
-def search_batch(index, queries, params: SearchParams, k: int | None = None, device: int = 0):
+def search_batch(index, queries, params: SearchParams, k: int | None = None, device: int = 0,
+                 out=None):
     """Batched search.
 
     k=None: one `SearchResult` per query with the reference's full semantics
@@ -90,17 +91,24 @@ def search_batch(index, queries, params: SearchParams, k: int | None = None, dev
     stats (B, 4) int64) -- row b is the first k entries of search()'s
     reranked list.  `queries` may be a numpy array or a CUDA torch tensor;
     with a tensor the outputs are CUDA tensors on the current stream.
+    `out=(ids, dists, stats)` reuses caller-owned (e.g. pinned) arrays.
     """
     dev = device_index(index, device)
     lib = _native.load()
     cp = _cparams(params)
     if _is_torch_cuda(queries):
-        return _search_batch_torch(dev, queries, cp, params, k)
+        return _search_batch_torch(dev, queries, cp, params, k, out)
     q = np.ascontiguousarray(np.asarray(queries, dtype=np.float32))
     if q.ndim == 1:
         q = q[None, :]
     _check_query_dim(dev, q)
     b = q.shape[0]
+    if k is not None and out is not None:
+        ids, dists, stats = out
+        assert ids.shape == (b, k) and dists.shape == (b, k) and stats.shape == (b, 4)
+        _native.check(lib.givf_search_topk(dev.handle, _vp(q), b, ctypes.byref(cp), int(k),
+                                           _vp(ids), _vp(dists), _vp(stats), None))
+        return ids, dists, stats
     stats = np.zeros((b, 4), np.int64)
     if k is not None:
         ids = np.empty((b, int(k)), np.int32)
@@ -129,7 +137,7 @@ def _is_torch_cuda(x) -> bool:
     return mod.startswith("torch") and getattr(x, "is_cuda", False)
 
 
-def _search_batch_torch(dev, queries, cp, params, k):
+def _search_batch_torch(dev, queries, cp, params, k, out=None):
     import torch
 
     if k is None:
@@ -140,9 +148,12 @@ def _search_batch_torch(dev, queries, cp, params, k):
     if q.shape[-1] != dev.dim:
         raise ValueError(f"query dim {q.shape[-1]} != index dim {dev.dim}")
     b = q.shape[0]
-    ids = torch.empty((b, int(k)), dtype=torch.int32, device=q.device)
-    dists = torch.empty((b, int(k)), dtype=torch.float32, device=q.device)
-    stats = torch.empty((b, 4), dtype=torch.int64, device=q.device)
+    if out is not None:
+        ids, dists, stats = out
+    else:
+        ids = torch.empty((b, int(k)), dtype=torch.int32, device=q.device)
+        dists = torch.empty((b, int(k)), dtype=torch.float32, device=q.device)
+        stats = torch.empty((b, 4), dtype=torch.int64, device=q.device)
     stream = torch.cuda.current_stream(q.device).cuda_stream
     _native.check(_native.load().givf_search_topk(
         dev.handle, ctypes.c_void_p(q.data_ptr()), b, ctypes.byref(cp), int(k),

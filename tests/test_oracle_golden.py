@@ -78,3 +78,25 @@ def test_sharded_oracle_equals_unsharded(shards):
     got_i, got_d = so.merge_topk([o[0] for o in outs], [o[1] for o in outs], 50)
     np.testing.assert_array_equal(got_i, want_i)
     np.testing.assert_array_equal(got_d, want_d)
+
+
+def test_fast_probe_equals_exact_probe():
+    rng = np.random.default_rng(5)
+    for fxn in ("c1like_m8", "small_grouped", "rot_m8"):
+        fx = golden_io.load(fxn)
+        c = fx.index.centroids
+        k = c.shape[0]
+        for nprobe in (1, 7, 32, k // 2, k):
+            nprobe = max(1, min(k, nprobe))
+            for q in fx.queries[:6]:
+                a = so.probe_exact(c, q, nprobe)
+                b = so.probe_exact_fast(c, q, nprobe)
+                np.testing.assert_array_equal(a[0], b[0])
+                np.testing.assert_array_equal(a[1], b[1])
+    # many near-duplicate centroids exercise the fallback
+    c = rng.standard_normal((3000, 24)).astype(np.float32)
+    c[1000:2000] = c[:1000] + 1e-7
+    for _ in range(10):
+        q = rng.standard_normal(24).astype(np.float32)
+        a, b = so.probe_exact(c, q, 40), so.probe_exact_fast(c, q, 40)
+        np.testing.assert_array_equal(a[0], b[0])
