@@ -102,7 +102,7 @@ int64_t givf_index_device_bytes(givf_index_t index);
 
 /* queries (nq, dim) f32.  ids (nq, k) int32 padded with -1, dists (nq, k)
  * f32 padded with +inf, stats (nq) -- host or device; stream = cudaStream_t
- * or NULL for the index's own stream.  Returns after the results are
+ * to launch on (NULL = the default stream).  Returns after the results are
  * visible to the caller (host outputs: synchronised; device outputs:
  * enqueued on `stream`). */
 int givf_search_topk(givf_index_t index, const float* queries, int64_t nq,

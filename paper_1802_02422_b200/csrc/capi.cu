@@ -322,7 +322,7 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
 
   std::lock_guard<std::mutex> lock(ix->mu);
   CUDA_TRY(cudaSetDevice(ix->device));
-  cudaStream_t st = stream ? (cudaStream_t)stream : ix->stream;
+  cudaStream_t st = (cudaStream_t)stream;  // NULL = the default stream
   const IndexView& v = ix->v;
   const bool q_dev = is_device_ptr(queries);
   const bool out_dev = is_device_ptr(ids) && is_device_ptr(dists);
@@ -620,7 +620,7 @@ int givf_probe(givf_index_t ix, const float* queries, int64_t nq, int32_t nprobe
   if (nq == 0) return GIVF_OK;
   std::lock_guard<std::mutex> lock(ix->mu);
   CUDA_TRY(cudaSetDevice(ix->device));
-  cudaStream_t st = stream ? (cudaStream_t)stream : ix->stream;
+  cudaStream_t st = (cudaStream_t)stream;  // NULL = the default stream
   const bool q_dev = is_device_ptr(queries), o_dev = is_device_ptr(regions) && is_device_ptr(qc2);
   const int d = ix->v.d;
   size_t per_q = aligned_bytes<float>(d) + probe_bytes_per_query(pl) + (size_t)pl.P * 12 + 1024;

@@ -33,14 +33,30 @@ GIVF_DEV double key_to_f64(uint64_t k) {
   return __longlong_as_double((long long)u);
 }
 
-__device__ double warp_sqdist64_plan(const float* __restrict__ c, const double* qd, int d) {
-  const int lane = threadIdx.x & 31;
+// float64 |c - q|^2 by an 8-lane group (4 centroid rows in flight per warp):
+// lanes stride the row in float4 steps, then a 3-level xor tree.
+__device__ double group8_sqdist64(const float* __restrict__ c, const double* qd, int d) {
+  const int gl = threadIdx.x & 7;
   double s = 0.0;
-  for (int j = lane; j < d; j += 32) {
-    double t = dsub((double)c[j], qd[j]);
-    s = dadd(s, dmul(t, t));
+  if ((d & 3) == 0) {
+    const float4* c4 = reinterpret_cast<const float4*>(c);
+    for (int j = gl; j < (d >> 2); j += 8) {
+      float4 v = __ldg(c4 + j);
+      const double* qq = qd + 4 * j;
+      double t0 = dsub((double)v.x, qq[0]), t1 = dsub((double)v.y, qq[1]);
+      double t2 = dsub((double)v.z, qq[2]), t3 = dsub((double)v.w, qq[3]);
+      s = dadd(s, dadd(dadd(dmul(t0, t0), dmul(t1, t1)), dadd(dmul(t2, t2), dmul(t3, t3))));
+    }
+  } else {
+    for (int j = gl; j < d; j += 8) {
+      double t = dsub((double)__ldg(c + j), qd[j]);
+      s = dadd(s, dmul(t, t));
+    }
   }
-  return warp_sum(s);
+  s += __shfl_xor_sync(0xffffffffu, s, 4);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  return s;
 }
 
 __global__ void __launch_bounds__(PLAN_THREADS) k_plan(PlanArgs a) {
@@ -75,13 +91,18 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan(PlanArgs a) {
   // ---- 1. scores (search.py:111-121)
   unsigned long long kmin = ~0ull, kmax = 0ull;
   if (ix.grouping) {
-    const int warp = tid >> 5, nw = blockDim.x >> 5, lane = tid & 31;
-    for (int64_t f = warp; f < total; f += nw) {
-      int p = (int)(f / G), j = (int)(f % G);
+    const int grp = tid >> 3, ngrp = blockDim.x >> 3, gl = tid & 7;
+    // all 32 lanes of a warp iterate together (shuffles need the full mask)
+    const int64_t iters = (total + ngrp - 1) / ngrp;
+    for (int64_t it = 0; it < iters; ++it) {
+      const int64_t f = it * ngrp + grp;
+      const bool live = f < total;
+      const int64_t fc = live ? f : 0;
+      int p = (int)(fc / G), j = (int)(fc % G);
       int r = reg[p];
       int s = ix.nbr[(int64_t)r * G + j];
-      double qs2 = warp_sqdist64_plan(ix.centroids + (int64_t)s * d, qd, d);
-      if (lane == 0) {
+      double qs2 = group8_sqdist64(ix.centroids + (int64_t)s * d, qd, d);
+      if (live && gl == 0) {
         double al = (double)ix.alphas[r];
         double base = dadd(dmul(dsub(1.0, al), qc2[p]), dmul(al, qs2));
         double score = dadd(base, (double)ix.norm[(int64_t)r * G + j]);
@@ -223,23 +244,33 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan(PlanArgs a) {
   for (uint32_t i = nbk + tid; i < np2; i += blockDim.x) { bkey[i] = kKeyPad; bval[i] = 0xffffffffu; }
   __syncthreads();
   bitonic_sort(bkey, bval, np2);
-  if (tid == 0) {
-    uint64_t cnt = taken_c, w = taken_w, begun = 0, scanned = 0;
-    for (uint32_t i = 0; i < nbk; ++i) {
-      blen[i] = 0;
-      if (cnt >= kept || w >= budget) continue;
-      int64_t f = bval[i];
-      int p = (int)(f / G), j = (int)(f % G);
-      uint64_t sz = (uint64_t)ix.gsize[(int64_t)reg[p] * G + j];
-      uint64_t l = min(sz, budget - w);
-      blen[i] = (int32_t)l;
-      begun += 1;
-      scanned += l;
-      w += sz;
-      cnt += 1;
+  // walk the sorted bucket in parallel: item i has count prefix taken_c + i
+  // and weight prefix taken_w + (exclusive scan of sizes)
+  {
+    unsigned long long carry = taken_w, my_scanned = 0;
+    uint32_t my_begun = 0;
+    for (uint32_t t0 = 0; t0 < nbk; t0 += blockDim.x) {
+      const uint32_t i = t0 + tid;
+      unsigned long long sz = 0;
+      if (i < nbk) {
+        int64_t f = bval[i];
+        sz = (unsigned long long)ix.gsize[(int64_t)reg[f / G] * G + (f % G)];
+      }
+      unsigned long long tile;
+      unsigned long long excl = block_exclusive_scan(sz, red64, &tile);
+      if (i < nbk) {
+        const unsigned long long w = carry + excl;
+        const bool ok = (taken_c + i < kept) && (w < budget);
+        const unsigned long long l = ok ? min(sz, budget - w) : 0ull;
+        blen[i] = (int32_t)l;
+        my_begun += ok ? 1u : 0u;
+        my_scanned += l;
+      }
+      carry += tile;
     }
-    s_walk_begun = (int)begun;
-    s_walk_w = scanned;
+    uint32_t tb = block_sum(my_begun, red32);
+    unsigned long long ts = block_sum(my_scanned, red64);
+    if (tid == 0) { s_walk_begun = (int)tb; s_walk_w = ts; }
   }
   __syncthreads();
 
