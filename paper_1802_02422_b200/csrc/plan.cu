@@ -25,8 +25,9 @@
 namespace givf {
 
 constexpr int PLAN_THREADS = 256;
-constexpr int PLAN_BUCKETS = 2048;
-constexpr int SORTCAP = 2048;
+constexpr int PLAN_BUCKETS = 1024;
+constexpr int SORTCAP = 1024;
+constexpr int PLAN_SREG = 2048;  // probed regions staged in shared memory
 
 GIVF_DEV double key_to_f64(uint64_t k) {
   uint64_t u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
@@ -59,6 +60,41 @@ __device__ double group8_sqdist64(const float* __restrict__ c, const double* qd,
   return s;
 }
 
+// U rows at once (d % 4 == 0, d <= 128): all loads issued before any math so
+// each lane keeps 4*U float4 requests in flight.
+template <int U>
+__device__ void group8_sqdist64_multi(const float* const* rows, const double* qd, int d4,
+                                      double* out) {
+  const int gl = threadIdx.x & 7;
+  float4 v[U][4];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int j = gl + 8 * t;
+      v[u][t] = j < d4 ? __ldg(reinterpret_cast<const float4*>(rows[u]) + j)
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    double s = 0.0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int j = gl + 8 * t;
+      if (j < d4) {
+        const double* qq = qd + 4 * j;
+        double t0 = dsub((double)v[u][t].x, qq[0]), t1 = dsub((double)v[u][t].y, qq[1]);
+        double t2 = dsub((double)v[u][t].z, qq[2]), t3 = dsub((double)v[u][t].w, qq[3]);
+        s = dadd(s, dadd(dadd(dmul(t0, t0), dmul(t1, t1)), dadd(dmul(t2, t2), dmul(t3, t3))));
+      }
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    out[u] = s;
+  }
+}
+
 __global__ void __launch_bounds__(PLAN_THREADS) k_plan(PlanArgs a) {
   extern __shared__ __align__(16) unsigned char dsm[];
   unsigned long long* hw = reinterpret_cast<unsigned long long*>(dsm);
@@ -66,7 +102,8 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan(PlanArgs a) {
   uint32_t* hc = reinterpret_cast<uint32_t*>(bkey + SORTCAP);
   uint32_t* bval = hc + PLAN_BUCKETS;
   int32_t* blen = reinterpret_cast<int32_t*>(bval + SORTCAP);
-  double* qd = reinterpret_cast<double*>(blen + SORTCAP);
+  int32_t* sreg = blen + SORTCAP;
+  double* qd = reinterpret_cast<double*>(sreg + PLAN_SREG);
   __shared__ unsigned long long red64[40];
   __shared__ uint32_t red32[40];
   __shared__ int s_b;
@@ -80,17 +117,55 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan(PlanArgs a) {
   const int b = blockIdx.x, tid = threadIdx.x;
   const int G = ix.G, d = ix.d, P = a.P;
   const int64_t total = (int64_t)P * G;
-  const int* reg = a.regions + (int64_t)b * P;
+  const int* reg = a.regions + (int64_t)b * P;  // staged in smem when P <= PLAN_SREG
   const double* qc2 = a.qc2 + (int64_t)b * P;
   double* sbase = a.sbase + (int64_t)b * total;
   double* sscore = a.sscore + (int64_t)b * total;
 
   for (int j = tid; j < d; j += blockDim.x) qd[j] = (double)a.Q[(int64_t)b * d + j];
+  for (int p = tid; p < P && P <= PLAN_SREG; p += blockDim.x) sreg[p] = a.regions[(int64_t)b * P + p];
   __syncthreads();
+  if (P <= PLAN_SREG) reg = sreg;
 
   // ---- 1. scores (search.py:111-121)
   unsigned long long kmin = ~0ull, kmax = 0ull;
-  if (ix.grouping) {
+  if (ix.grouping && (d & 3) == 0 && d <= 128) {
+    constexpr int U = 4;
+    const int grp = tid >> 3, ngrp = blockDim.x >> 3, gl = tid & 7;
+    const int64_t iters = (total + (int64_t)ngrp * U - 1) / ((int64_t)ngrp * U);
+    for (int64_t it = 0; it < iters; ++it) {
+      const float* rows[U];
+      int64_t fs[U];
+      int rr[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        fs[u] = (it * U + u) * ngrp + grp;
+        const int64_t fc = fs[u] < total ? fs[u] : 0;
+        const int p = (int)(fc / G), j = (int)(fc % G);
+        rr[u] = reg[p];
+        rows[u] = ix.centroids + (int64_t)ix.nbr[(int64_t)rr[u] * G + j] * d;
+      }
+      double qs2[U];
+      group8_sqdist64_multi<U>(rows, qd, d >> 2, qs2);
+      if (gl == 0) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t f = fs[u];
+          if (f >= total) continue;
+          const int p = (int)(f / G), j = (int)(f % G);
+          const int r = rr[u];
+          double al = (double)ix.alphas[r];
+          double base = dadd(dmul(dsub(1.0, al), qc2[p]), dmul(al, qs2[u]));
+          double score = dadd(base, (double)ix.norm[(int64_t)r * G + j]);
+          sbase[f] = base;
+          sscore[f] = score;
+          uint64_t k = f64_key(score);
+          kmin = min(kmin, (unsigned long long)k);
+          kmax = max(kmax, (unsigned long long)k);
+        }
+      }
+    }
+  } else if (ix.grouping) {
     const int grp = tid >> 3, ngrp = blockDim.x >> 3, gl = tid & 7;
     // all 32 lanes of a warp iterate together (shuffles need the full mask)
     const int64_t iters = (total + ngrp - 1) / ngrp;
@@ -135,7 +210,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan(PlanArgs a) {
   uint64_t bucket_lo = 0, bucket_hi = 0;  // final bucket range (phase-dependent key)
   for (int level = 0; level < 16; ++level) {
     uint64_t range = hi - lo;
-    int shift = range == 0 ? 0 : max(0, 64 - __clzll((long long)range) - 11);
+    int shift = range == 0 ? 0 : max(0, 64 - __clzll((long long)range) - 10);  // <= 1024 buckets
     uint32_t nb = (uint32_t)(range >> shift) + 1;
     for (uint32_t i = tid; i < nb; i += blockDim.x) { hc[i] = 0; hw[i] = 0; }
     __syncthreads();
@@ -350,7 +425,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan(PlanArgs a) {
 
 size_t plan_smem(int d) {
   return (size_t)PLAN_BUCKETS * 8 + SORTCAP * 8 + PLAN_BUCKETS * 4 + SORTCAP * 4 + SORTCAP * 4 +
-         (size_t)d * 8 + 16;
+         PLAN_SREG * 4 + (size_t)d * 8 + 16;
 }
 
 void launch_plan(const PlanArgs& a, cudaStream_t s) {

@@ -23,7 +23,7 @@
 namespace givf {
 
 constexpr int SCAN_THREADS = 256;
-constexpr int CHUNK = 2048;
+constexpr int CHUNK = 1024;
 constexpr int WIN = SCAN_THREADS;
 
 template <int M>
@@ -157,12 +157,11 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(ScanArgs a, int bufcap) {
   ScanSmem s = carve(dsm, M, ix.d);
   __shared__ int32_t red32[40];
   __shared__ int s_count;
-  __shared__ unsigned long long s_thr;
   __shared__ int s_nfit;
   const int b = blockIdx.x, tid = threadIdx.x;
 
   build_lut(ix, a.Q + (int64_t)b * ix.d, s);
-  if (tid == 0) { s_count = 0; s_thr = kKeyPad; }
+  if (tid == 0) s_count = 0;
   __syncthreads();
 
   const WorkItem* W = a.work + (int64_t)b * a.cap_w;
@@ -170,6 +169,10 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(ScanArgs a, int bufcap) {
   uint64_t* fk = a.mode == 1 ? a.full_keys + (int64_t)b * a.cap_full_p2 : nullptr;
   int64_t code_base = 0;
 
+  // Candidates are appended while their distance key is <= thr (the k-th
+  // smallest key seen so far, ties kept); ids are loaded only for them.
+  uint32_t thr = 0xffffffffu;
+  uint64_t thr64 = kKeyPad;
   auto process = [&](int64_t row, double base, int64_t pos) {
     float ip = code_ip<M>(ix.codes, row, s.lut);
     double c = s.ctab[__ldg(ix.cbytes + row)];
@@ -178,27 +181,77 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(ScanArgs a, int bufcap) {
       fk[pos] = dist_id_key(dist, __ldg(ix.pids + row));
     } else {
       uint32_t dk = f32_key(dist);
-      unsigned long long thr = *((volatile unsigned long long*)&s_thr);
-      if (dk <= (uint32_t)(thr >> 32)) {
+      if (dk <= thr) {
         uint64_t key = ((uint64_t)dk << 32) | (uint32_t)__ldg(ix.pids + row);
-        if (key < thr) s.buf[atomicAdd(&s_count, 1)] = key;
+        if (key < thr64) s.buf[atomicAdd(&s_count, 1)] = key;
       }
     }
   };
-  // keep room for one more chunk of appends
+  // Keep room for one more chunk of appends: radix-select the k-th smallest
+  // distance key of the buffer (4 x 8-bit digits) and compact to keys <= it.
   auto maybe_shrink = [&]() {
     __syncthreads();
-    int cnt = s_count;
-    if (a.mode == 0 && cnt > bufcap - CHUNK) {
-      uint32_t np2 = next_pow2((uint32_t)cnt);
-      for (uint32_t i = cnt + tid; i < np2; i += blockDim.x) s.buf[i] = kKeyPad;
+    const int cnt = s_count;
+    if (a.mode != 0 || cnt <= bufcap - CHUNK) return;
+    uint32_t* hist = reinterpret_cast<uint32_t*>(s.rowv);  // free between chunks
+    uint32_t prefix = 0, mask = 0, need = (uint32_t)a.k;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
+      __syncthreads();
+      for (int i = tid; i < cnt; i += blockDim.x) {
+        uint32_t dk = (uint32_t)(s.buf[i] >> 32);
+        if ((dk & mask) == prefix) atomicAdd(&hist[(dk >> shift) & 255u], 1u);
+      }
+      __syncthreads();
+      if (tid < 32) {  // warp 0: find the digit holding the need-th key
+        uint32_t h[8], run = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) { h[j] = hist[tid * 8 + j]; run += h[j]; }
+        uint32_t incl = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (tid >= o) incl += y;
+        }
+        uint32_t excl = incl - run;
+        if (excl < need && incl >= need) {
+          uint32_t c = excl;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (c + h[j] >= need) { s_nfit = (int)(tid * 8 + j); red32[32] = (int32_t)c; break; }
+            c += h[j];
+          }
+        }
+      }
+      __syncthreads();
+      prefix |= (uint32_t)s_nfit << shift;
+      mask |= 255u << shift;
+      need -= (uint32_t)red32[32];
+      __syncthreads();
+    }
+    // in-place stable compaction (output index <= input index, tile by tile)
+    int base = 0;
+    for (int t0 = 0; t0 < cnt; t0 += blockDim.x) {
+      const int i = t0 + tid;
+      uint64_t v = i < cnt ? s.buf[i] : kKeyPad;
+      int keep = (i < cnt && (uint32_t)(v >> 32) <= prefix) ? 1 : 0;
+      int tot;
+      int pos = block_exclusive_scan(keep, red32, &tot);
+      if (keep) s.buf[base + pos] = v;
+      base += tot;
+      __syncthreads();
+    }
+    if (tid == 0) s_count = base;
+    thr = prefix;
+    __syncthreads();
+    if (base > bufcap - CHUNK) {  // > CHUNK exact distance ties: order them by id
+      const uint32_t np2 = next_pow2((uint32_t)base);
+      for (uint32_t i = base + tid; i < np2; i += blockDim.x) s.buf[i] = kKeyPad;
       __syncthreads();
       bitonic_sort_keys(s.buf, np2);
-      if (tid == 0) {
-        int keep = min(cnt, a.k);
-        s_count = keep;
-        s_thr = keep == a.k ? s.buf[a.k - 1] : kKeyPad;
-      }
+      thr64 = s.buf[a.k - 1];
+      thr = (uint32_t)(thr64 >> 32);
+      if (tid == 0) s_count = a.k;
       __syncthreads();
     }
   };
