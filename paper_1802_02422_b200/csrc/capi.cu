@@ -49,8 +49,8 @@ struct Profiler {
 Profiler g_prof;
 
 template <class F>
-void staged(int stage, cudaStream_t st, F&& launch) {
-  g_launches += 1;
+void staged(int stage, cudaStream_t st, F&& launch, int kernels = 1) {
+  g_launches += kernels;
   if (!g_prof.on.load()) {
     launch();
     return;
@@ -228,11 +228,16 @@ struct Plan {
   ProbeShape ps;
 };
 
-// Probe for one chunk of queries: regions (nq, P) and qc2 (nq, P).
+constexpr float kEpsScaleUlp = 5.9604645e-8f;  // 2^-24
+float probe_eps_scale(int d) { return 3.0f * (float)(d + 4) * kEpsScaleUlp; }
+
+// Probe for one chunk of queries: regions (nq, P) and qc2 (nq, P).  *D_out
+// receives the fp32 score matrix (nq, K) when the GEMM path ran, else null.
 int run_probe(givf_index* ix, const Plan& pl, const float* dQ, int nq, int* regions,
-              double* qc2, Arena& ar, cudaStream_t st) {
+              double* qc2, Arena& ar, cudaStream_t st, const float** D_out = nullptr) {
   const IndexView& v = ix->v;
   const int P = pl.P, K = v.K, d = v.d;
+  if (D_out) *D_out = nullptr;
   int* failf = ar.take<int>(nq);
   const uint32_t kp2 = next_pow2_host((uint32_t)K), pp2 = next_pow2_host((uint32_t)P);
   uint64_t* sk = ar.take<uint64_t>((size_t)kFullSlots * kp2);
@@ -255,6 +260,7 @@ int run_probe(givf_index* ix, const Plan& pl, const float* dQ, int nq, int* regi
     return GIVF_OK;
   }
   float* D = ar.take<float>((size_t)nq * K);
+  if (D_out) *D_out = D;
   int* cand = ar.take<int>((size_t)nq * pl.ps.cap);
   int* cand_n = ar.take<int>(nq);
   float* theta = ar.take<float>(nq);
@@ -262,7 +268,7 @@ int run_probe(givf_index* ix, const Plan& pl, const float* dQ, int nq, int* regi
   staged(ST_SELECT, st, [&] {
     launch_probe_select(D, K, nq, K, pl.ps.Tmin, pl.ps.cap, cand, cand_n, theta, st);
   });
-  const float eps_scale = 3.0f * (float)(d + 4) * 5.9604645e-8f;
+  const float eps_scale = probe_eps_scale(d);
   staged(ST_RECHECK, st, [&] {
     launch_probe_recheck(dQ, v.centroids, nq, K, d, P, cand, cand_n, pl.ps.cap, theta, v.cmax,
                          eps_scale, regions, qc2, failf, st);
@@ -332,7 +338,8 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
 
   // per-query workspace
   size_t per_q = aligned_bytes<float>(v.d) + probe_bytes_per_query(pl) +
-                 2 * aligned_bytes<double>(pl.total) + aligned_bytes<WorkItem>(pl.cap_w) +
+                 2 * aligned_bytes<double>(pl.total) + aligned_bytes<int32_t>(pl.total) +
+                 aligned_bytes<WorkItem>(pl.cap_w) + aligned_bytes<int>(1) +
                  aligned_bytes<int>(1) + aligned_bytes<int64_t>(4);
   if (om == OUT_FULL && !rerank) {
     size_t cp2 = next_pow2_host((uint32_t)std::min<int64_t>(pl.cap_w, 1 << 30));
@@ -362,7 +369,8 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
     }
     int* regions = ar.take<int>((size_t)bq * pl.P);
     double* qc2 = ar.take<double>((size_t)bq * pl.P);
-    rc = run_probe(ix, pl, dQ, bq, regions, qc2, ar, st);
+    const float* Dmat = nullptr;
+    rc = run_probe(ix, pl, dQ, bq, regions, qc2, ar, st, &Dmat);
     if (rc) return rc;
 
     PlanArgs pa{};
@@ -376,6 +384,7 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
     pa.budget = pl.budget;
     pa.sbase = ar.take<double>((size_t)bq * pl.total);
     pa.sscore = ar.take<double>((size_t)bq * pl.total);
+    pa.ssize = ar.take<int32_t>((size_t)bq * pl.total);
     pa.cap_w = pl.cap_w;
     pa.work = ar.take<WorkItem>((size_t)bq * pl.cap_w);
     pa.nwork = ar.take<int>(bq);
@@ -388,7 +397,14 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
       pa.sval = ar.take<uint32_t>((size_t)bq * cp2);
       pa.order = ar.take<int32_t>((size_t)bq * pl.cap_w);
     }
-    staged(ST_PLAN, st, [&] { launch_plan(pa, st); });
+    pa.D = Dmat;
+    pa.ldD = v.K;
+    pa.cmax = v.cmax;
+    pa.eps_scale = probe_eps_scale(v.d);
+    pa.only = Dmat ? ar.take<int>(bq) : nullptr;
+    int nk = 0;
+    staged(ST_PLAN, st, [&] { nk = launch_plan(pa, st); }, 0);
+    g_launches += nk;
     KCHECK();
 
     int32_t* oid;

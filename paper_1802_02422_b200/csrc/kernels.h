@@ -67,6 +67,7 @@ struct PlanArgs {
   int64_t kept, budget;
   double* sbase;        // (nq, P*G) scratch
   double* sscore;       // (nq, P*G) scratch
+  int32_t* ssize;       // (nq, P*G) scratch: global group size of each item
   WorkItem* work;       // (nq, cap_w)
   int64_t cap_w;
   int* nwork;           // (nq)
@@ -76,8 +77,15 @@ struct PlanArgs {
   uint64_t* skey;       // (nq, pow2(cap_w)) scratch
   uint32_t* sval;       // (nq, pow2(cap_w)) scratch
   int32_t* order;       // (nq, cap_w)
+  // approximate-first path: the probe's fp32 scores s~ = |c|^2 - 2 q.c
+  const float* D;       // (nq, ldD) or null (exact path only)
+  int64_t ldD;
+  float cmax, eps_scale;
+  int* only;            // (nq) fallback flags: exact kernels run where only[b] != 0
 };
-void launch_plan(const PlanArgs& a, cudaStream_t s);
+// Launches the approximate-first planner (when a.D is set) followed by the
+// exact planner for the queries it could not certify; returns kernels launched.
+int launch_plan(const PlanArgs& a, cudaStream_t s);
 
 // scan.cu
 struct ScanArgs {

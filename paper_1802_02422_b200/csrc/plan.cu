@@ -95,43 +95,46 @@ __device__ void group8_sqdist64_multi(const float* const* rows, const double* qd
   }
 }
 
-__global__ void __launch_bounds__(PLAN_THREADS) k_plan(PlanArgs a) {
-  extern __shared__ __align__(16) unsigned char dsm[];
-  unsigned long long* hw = reinterpret_cast<unsigned long long*>(dsm);
-  uint64_t* bkey = reinterpret_cast<uint64_t*>(hw + PLAN_BUCKETS);
-  uint32_t* hc = reinterpret_cast<uint32_t*>(bkey + SORTCAP);
-  uint32_t* bval = hc + PLAN_BUCKETS;
-  int32_t* blen = reinterpret_cast<int32_t*>(bval + SORTCAP);
-  int32_t* sreg = blen + SORTCAP;
-  double* qd = reinterpret_cast<double*>(sreg + PLAN_SREG);
-  __shared__ unsigned long long red64[40];
-  __shared__ uint32_t red32[40];
-  __shared__ int s_b;
-  __shared__ uint32_t s_bc_before;
-  __shared__ unsigned long long s_bw_before;
-  __shared__ int s_nemit, s_nb;
-  __shared__ unsigned long long s_walk_w;
-  __shared__ int s_walk_begun;
-
+// ---- K3: float64 group scores (search.py:111-121), one CTA per query.
+__global__ void __launch_bounds__(PLAN_THREADS) k_plan_score(PlanArgs a) {
+  __shared__ double qd[1024];
+  __shared__ int32_t sreg[PLAN_SREG];
   const IndexView& ix = a.ix;
   const int b = blockIdx.x, tid = threadIdx.x;
+  if (a.only && a.only[b] == 0) return;  // fallback mode: flagged queries only
   const int G = ix.G, d = ix.d, P = a.P;
   const int64_t total = (int64_t)P * G;
-  const int* reg = a.regions + (int64_t)b * P;  // staged in smem when P <= PLAN_SREG
+  const int* reg = a.regions + (int64_t)b * P;
   const double* qc2 = a.qc2 + (int64_t)b * P;
   double* sbase = a.sbase + (int64_t)b * total;
   double* sscore = a.sscore + (int64_t)b * total;
+  int32_t* ssize = a.ssize + (int64_t)b * total;
 
   for (int j = tid; j < d; j += blockDim.x) qd[j] = (double)a.Q[(int64_t)b * d + j];
-  for (int p = tid; p < P && P <= PLAN_SREG; p += blockDim.x) sreg[p] = a.regions[(int64_t)b * P + p];
+  if (P <= PLAN_SREG)
+    for (int p = tid; p < P; p += blockDim.x) sreg[p] = reg[p];
   __syncthreads();
   if (P <= PLAN_SREG) reg = sreg;
 
-  // ---- 1. scores (search.py:111-121)
-  unsigned long long kmin = ~0ull, kmax = 0ull;
-  if (ix.grouping && (d & 3) == 0 && d <= 128) {
+  auto finish = [&](int64_t f, int r, int j, double qs2, int p) {
+    double al = (double)ix.alphas[r];
+    double base = dadd(dmul(dsub(1.0, al), qc2[p]), dmul(al, qs2));
+    sbase[f] = base;
+    sscore[f] = dadd(base, (double)ix.norm[(int64_t)r * G + j]);
+    ssize[f] = ix.gsize[(int64_t)r * G + j];
+  };
+  if (!ix.grouping) {
+    for (int64_t f = tid; f < total; f += blockDim.x) {
+      double v = qc2[f / G];
+      sbase[f] = v;
+      sscore[f] = v;
+      ssize[f] = ix.gsize[(int64_t)reg[f / G] * G + (f % G)];
+    }
+    return;
+  }
+  const int grp = tid >> 3, ngrp = blockDim.x >> 3, gl = tid & 7;
+  if ((d & 3) == 0 && d <= 128) {
     constexpr int U = 4;
-    const int grp = tid >> 3, ngrp = blockDim.x >> 3, gl = tid & 7;
     const int64_t iters = (total + (int64_t)ngrp * U - 1) / ((int64_t)ngrp * U);
     for (int64_t it = 0; it < iters; ++it) {
       const float* rows[U];
@@ -141,64 +144,65 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan(PlanArgs a) {
       for (int u = 0; u < U; ++u) {
         fs[u] = (it * U + u) * ngrp + grp;
         const int64_t fc = fs[u] < total ? fs[u] : 0;
-        const int p = (int)(fc / G), j = (int)(fc % G);
-        rr[u] = reg[p];
-        rows[u] = ix.centroids + (int64_t)ix.nbr[(int64_t)rr[u] * G + j] * d;
+        rr[u] = reg[fc / G];
+        rows[u] = ix.centroids + (int64_t)ix.nbr[(int64_t)rr[u] * G + (fc % G)] * d;
       }
       double qs2[U];
       group8_sqdist64_multi<U>(rows, qd, d >> 2, qs2);
       if (gl == 0) {
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int64_t f = fs[u];
-          if (f >= total) continue;
-          const int p = (int)(f / G), j = (int)(f % G);
-          const int r = rr[u];
-          double al = (double)ix.alphas[r];
-          double base = dadd(dmul(dsub(1.0, al), qc2[p]), dmul(al, qs2[u]));
-          double score = dadd(base, (double)ix.norm[(int64_t)r * G + j]);
-          sbase[f] = base;
-          sscore[f] = score;
-          uint64_t k = f64_key(score);
-          kmin = min(kmin, (unsigned long long)k);
-          kmax = max(kmax, (unsigned long long)k);
-        }
+        for (int u = 0; u < U; ++u)
+          if (fs[u] < total) finish(fs[u], rr[u], (int)(fs[u] % G), qs2[u], (int)(fs[u] / G));
       }
     }
-  } else if (ix.grouping) {
-    const int grp = tid >> 3, ngrp = blockDim.x >> 3, gl = tid & 7;
+  } else {
     // all 32 lanes of a warp iterate together (shuffles need the full mask)
     const int64_t iters = (total + ngrp - 1) / ngrp;
     for (int64_t it = 0; it < iters; ++it) {
       const int64_t f = it * ngrp + grp;
-      const bool live = f < total;
-      const int64_t fc = live ? f : 0;
-      int p = (int)(fc / G), j = (int)(fc % G);
-      int r = reg[p];
-      int s = ix.nbr[(int64_t)r * G + j];
-      double qs2 = group8_sqdist64(ix.centroids + (int64_t)s * d, qd, d);
-      if (live && gl == 0) {
-        double al = (double)ix.alphas[r];
-        double base = dadd(dmul(dsub(1.0, al), qc2[p]), dmul(al, qs2));
-        double score = dadd(base, (double)ix.norm[(int64_t)r * G + j]);
-        sbase[f] = base;
-        sscore[f] = score;
-        uint64_t k = f64_key(score);
-        kmin = min(kmin, (unsigned long long)k);
-        kmax = max(kmax, (unsigned long long)k);
-      }
-    }
-  } else {
-    for (int64_t f = tid; f < total; f += blockDim.x) {
-      double v = qc2[f / G];
-      sbase[f] = v;
-      sscore[f] = v;
-      uint64_t k = f64_key(v);
-      kmin = min(kmin, (unsigned long long)k);
-      kmax = max(kmax, (unsigned long long)k);
+      const int64_t fc = f < total ? f : 0;
+      const int p = (int)(fc / G), j = (int)(fc % G);
+      const int r = reg[p];
+      double qs2 = group8_sqdist64(ix.centroids + (int64_t)ix.nbr[(int64_t)r * G + j] * d, qd, d);
+      if (f < total && gl == 0) finish(f, r, j, qs2, p);
     }
   }
-  __syncthreads();  // scratch writes visible block-wide (global, same CTA)
+}
+
+// ---- K4: tau-pruning + budget walk + work-list emission, one CTA per query.
+__global__ void __launch_bounds__(PLAN_THREADS) k_plan_select(PlanArgs a) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  unsigned long long* hw = reinterpret_cast<unsigned long long*>(dsm);
+  uint64_t* bkey = reinterpret_cast<uint64_t*>(hw + PLAN_BUCKETS);
+  uint32_t* hc = reinterpret_cast<uint32_t*>(bkey + SORTCAP);
+  uint32_t* bval = hc + PLAN_BUCKETS;
+  int32_t* blen = reinterpret_cast<int32_t*>(bval + SORTCAP);
+  __shared__ unsigned long long red64[40];
+  __shared__ uint32_t red32[40];
+  __shared__ int s_b;
+  __shared__ uint32_t s_bc_before;
+  __shared__ unsigned long long s_bw_before;
+  __shared__ int s_nemit;
+  __shared__ unsigned long long s_walk_w;
+  __shared__ int s_walk_begun;
+  __shared__ uint32_t s_nbk;
+
+  const IndexView& ix = a.ix;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  if (a.only && a.only[b] == 0) return;  // fallback mode: flagged queries only
+  const int G = ix.G, P = a.P;
+  const int64_t total = (int64_t)P * G;
+  const int* reg = a.regions + (int64_t)b * P;
+  const double* sbase = a.sbase + (int64_t)b * total;
+  const double* sscore = a.sscore + (int64_t)b * total;
+  const int32_t* ssize = a.ssize + (int64_t)b * total;
+
+  unsigned long long kmin = ~0ull, kmax = 0ull;
+  for (int64_t f = tid; f < total; f += blockDim.x) {
+    unsigned long long k = f64_key(sscore[f]);
+    kmin = min(kmin, k);
+    kmax = max(kmax, k);
+  }
   kmin = block_min(kmin, red64);
   kmax = block_max(kmax, red64);
 
@@ -224,10 +228,9 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan(PlanArgs a) {
         if (sk != kx || (uint64_t)f < lo || (uint64_t)f > hi) continue;
         key = (uint64_t)f;
       }
-      int p = (int)(f / G), j = (int)(f % G);
       uint32_t bk = (uint32_t)((key - lo) >> shift);
       atomicAdd(&hc[bk], 1u);
-      atomicAdd(&hw[bk], (unsigned long long)ix.gsize[(int64_t)reg[p] * G + j]);
+      atomicAdd(&hw[bk], (unsigned long long)ssize[f]);
     }
     __syncthreads();
     const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;
@@ -239,7 +242,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan(PlanArgs a) {
     unsigned long long totw;
     uint32_t pc = block_exclusive_scan(rc, red32, &totc);
     unsigned long long pw = block_exclusive_scan(rw, red64, &totw);
-    if (tid == 0) { s_b = -1; s_nb = (int)nb; }
+    if (tid == 0) s_b = -1;
     __syncthreads();
     {
       uint64_t c0 = taken_c + pc, w0 = taken_w + pw;
@@ -294,7 +297,6 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan(PlanArgs a) {
   // ---- 3. sort the boundary bucket exactly and walk it
   if (tid == 0) { s_nemit = 0; s_walk_w = 0; s_walk_begun = 0; }
   __syncthreads();
-  __shared__ uint32_t s_nbk;
   if (tid == 0) s_nbk = 0;
   __syncthreads();
   auto in_bucket = [&](int64_t f, uint64_t sk) -> bool {
@@ -329,7 +331,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan(PlanArgs a) {
       unsigned long long sz = 0;
       if (i < nbk) {
         int64_t f = bval[i];
-        sz = (unsigned long long)ix.gsize[(int64_t)reg[f / G] * G + (f % G)];
+        sz = (unsigned long long)ssize[f];
       }
       unsigned long long tile;
       unsigned long long excl = block_exclusive_scan(sz, red64, &tile);
@@ -370,8 +372,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan(PlanArgs a) {
   for (int64_t f = tid; f < total; f += blockDim.x) {
     uint64_t sk = f64_key(sscore[f]);
     if (below(f, sk)) {
-      int p = (int)(f / G), j = (int)(f % G);
-      emit(f, ix.gsize[(int64_t)reg[p] * G + j]);
+      emit(f, ssize[f]);
     }
   }
   for (uint32_t i = tid; i < nbk; i += blockDim.x)
@@ -423,19 +424,391 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan(PlanArgs a) {
   }
 }
 
-size_t plan_smem(int d) {
-  return (size_t)PLAN_BUCKETS * 8 + SORTCAP * 8 + PLAN_BUCKETS * 4 + SORTCAP * 4 + SORTCAP * 4 +
-         PLAN_SREG * 4 + (size_t)d * 8 + 16;
+// ---- K3+K4 fast path: approximate scores, exact where it matters.
+//
+// qs2 needs a float64 centroid row per (region, group) item; the probe GEMM
+// already holds s~_c = |c|^2 - 2 q.c for every centroid with an a-priori
+// error bound eps (probe.cu).  With qs2~ = s~ + |q|^2 every approximate score
+// is within E of the exact one (alpha <= 1).  The CTA
+//   1. selects on approximate keys exactly like k_plan_select and takes v*,
+//      the approximate score of the last begun group;
+//   2. splits items into A (score~ < v*-3E: exact < v*-2E), the window W
+//      (|score~ - v*| <= 3E) and C (score~ > v*+3E: exact > v*+2E);
+//   3. scores W exactly, sorts it and walks it from the prefix of A;
+//   4. certifies the walk: the exact last begun group x_c lies in W with
+//      v*-2E <= score(x_c) <= v*+2E, and the walk has ended inside W (or at
+//      its end).  Then every A item precedes x_c, every C item follows it,
+//      and the begun set, lengths and stats equal the exact walk's.
+//      Otherwise the query is flagged for the exact planner.
+//   5. emits A and the begun W items with float64 base/score recomputed
+//      exactly (one centroid row per emitted group only).
+constexpr int WCAP = 256;
+
+__global__ void __launch_bounds__(PLAN_THREADS) k_plan_approx(PlanArgs a) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  unsigned long long* hw = reinterpret_cast<unsigned long long*>(dsm);
+  uint64_t* bkey = reinterpret_cast<uint64_t*>(hw + PLAN_BUCKETS);
+  uint64_t* wkey = bkey + SORTCAP;
+  uint32_t* hc = reinterpret_cast<uint32_t*>(wkey + WCAP);
+  uint32_t* bval = hc + PLAN_BUCKETS;
+  int32_t* blen = reinterpret_cast<int32_t*>(bval + SORTCAP);
+  uint32_t* wval = reinterpret_cast<uint32_t*>(blen + SORTCAP);
+  int32_t* wlen = reinterpret_cast<int32_t*>(wval + WCAP);
+  double* qd = reinterpret_cast<double*>(wlen + WCAP);
+  __shared__ unsigned long long red64[40];
+  __shared__ uint32_t red32[40];
+  __shared__ double redd[40];
+  __shared__ int s_b, s_nemit, s_lastb;
+  __shared__ uint32_t s_bc_before, s_nbk, s_nw;
+  __shared__ unsigned long long s_bw_before;
+
+  const IndexView& ix = a.ix;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const int G = ix.G, d = ix.d, P = a.P;
+  const int64_t total = (int64_t)P * G;
+  const int* reg = a.regions + (int64_t)b * P;
+  const double* qc2 = a.qc2 + (int64_t)b * P;
+  double* sscore = a.sscore + (int64_t)b * total;
+  int32_t* ssize = a.ssize + (int64_t)b * total;
+  const float* Drow = a.D + (int64_t)b * a.ldD;
+  const uint64_t kept = (uint64_t)a.kept, budget = (uint64_t)a.budget;
+
+  double q2p = 0.0;
+  for (int j = tid; j < d; j += blockDim.x) {
+    double x = (double)a.Q[(int64_t)b * d + j];
+    qd[j] = x;
+    q2p += x * x;
+  }
+  const double q2 = block_sum(q2p, redd);
+  const double qn = sqrt(q2);
+  const double E = ix.grouping
+      ? 1.0001 * ((double)a.eps_scale * ((double)a.cmax * a.cmax + 2.0 * qn * a.cmax)) +
+            1e-12 * ((double)a.cmax + qn) * ((double)a.cmax + qn)
+      : 0.0;
+
+  // ---- 1. approximate scores
+  unsigned long long kmin = ~0ull, kmax = 0ull;
+  for (int64_t f = tid; f < total; f += blockDim.x) {
+    const int p = (int)(f / G), j = (int)(f % G);
+    const int r = reg[p];
+    double score;
+    if (ix.grouping) {
+      const int64_t gi = (int64_t)r * G + j;
+      const double qs2 = dadd((double)__ldg(Drow + ix.nbr[gi]), q2);
+      const double al = (double)ix.alphas[r];
+      score = dadd(dadd(dmul(dsub(1.0, al), qc2[p]), dmul(al, qs2)), (double)ix.norm[gi]);
+    } else {
+      score = qc2[p];
+    }
+    sscore[f] = score;
+    ssize[f] = ix.gsize[(int64_t)r * G + j];
+    unsigned long long k = f64_key(score);
+    kmin = min(kmin, k);
+    kmax = max(kmax, k);
+  }
+  __syncthreads();
+  kmin = block_min(kmin, red64);
+  kmax = block_max(kmax, red64);
+
+  // ---- 2. approximate crossing (same bucket refinement as k_plan_select)
+  uint64_t taken_c = 0, taken_w = 0;
+  uint64_t lo = kmin, hi = kmax, bucket_lo = 0, bucket_hi = 0;
+  bool no_cut = false, flag = false;
+  for (int level = 0; level < 16; ++level) {
+    uint64_t range = hi - lo;
+    int shift = range == 0 ? 0 : max(0, 64 - __clzll((long long)range) - 10);
+    uint32_t nb = (uint32_t)(range >> shift) + 1;
+    for (uint32_t i = tid; i < nb; i += blockDim.x) { hc[i] = 0; hw[i] = 0; }
+    __syncthreads();
+    for (int64_t f = tid; f < total; f += blockDim.x) {
+      uint64_t sk = f64_key(sscore[f]);
+      if (sk < lo || sk > hi) continue;
+      uint32_t bk = (uint32_t)((sk - lo) >> shift);
+      atomicAdd(&hc[bk], 1u);
+      atomicAdd(&hw[bk], (unsigned long long)ssize[f]);
+    }
+    __syncthreads();
+    const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;
+    uint32_t b0 = tid * per, b1 = min(nb, b0 + per);
+    uint32_t rc = 0;
+    unsigned long long rw = 0;
+    for (uint32_t x = b0; x < b1; ++x) { rc += hc[x]; rw += hw[x]; }
+    uint32_t totc;
+    unsigned long long totw;
+    uint32_t pc = block_exclusive_scan(rc, red32, &totc);
+    unsigned long long pw = block_exclusive_scan(rw, red64, &totw);
+    if (tid == 0) s_b = -1;
+    __syncthreads();
+    {
+      uint64_t c0 = taken_c + pc, w0 = taken_w + pw;
+      if (b0 < b1 && c0 < kept && w0 < budget && (c0 + rc >= kept || w0 + rw >= budget)) {
+        uint64_t cc = c0, ww = w0;
+        for (uint32_t x = b0; x < b1; ++x) {
+          if (cc + hc[x] >= kept || ww + hw[x] >= budget) {
+            s_b = (int)x;
+            s_bc_before = (uint32_t)(cc - taken_c);
+            s_bw_before = ww - taken_w;
+            break;
+          }
+          cc += hc[x];
+          ww += hw[x];
+        }
+      }
+    }
+    __syncthreads();
+    const int bsel = s_b;
+    if (bsel < 0) {  // never crosses: every group is scanned whole
+      no_cut = true;
+      break;
+    }
+    const uint32_t cnt_b = hc[bsel];
+    const uint64_t bl = lo + ((uint64_t)bsel << shift);
+    const uint64_t bspan = bl + ((1ull << shift) - 1);
+    const uint64_t bh = bspan < hi ? bspan : hi;
+    taken_c += s_bc_before;
+    taken_w += s_bw_before;
+    __syncthreads();
+    if (cnt_b <= (uint32_t)SORTCAP) {
+      bucket_lo = bl;
+      bucket_hi = bh;
+      break;
+    }
+    if (shift == 0) {  // > SORTCAP equal approximate scores: leave it to the exact planner
+      flag = true;
+      break;
+    }
+    lo = bl;
+    hi = bh;
+  }
+
+  double vstar = __longlong_as_double(0x7ff0000000000000ll);  // +inf: no cut
+  if (!no_cut && !flag) {
+    if (tid == 0) s_nbk = 0;
+    __syncthreads();
+    for (int64_t f = tid; f < total; f += blockDim.x) {
+      uint64_t sk = f64_key(sscore[f]);
+      if (sk >= bucket_lo && sk <= bucket_hi) {
+        uint32_t p = atomicAdd(&s_nbk, 1u);
+        bkey[p] = sk;
+        bval[p] = (uint32_t)f;
+      }
+    }
+    __syncthreads();
+    const uint32_t nbk = s_nbk;
+    const uint32_t np2 = next_pow2(max(nbk, 1u));
+    for (uint32_t i = nbk + tid; i < np2; i += blockDim.x) { bkey[i] = kKeyPad; bval[i] = 0xffffffffu; }
+    __syncthreads();
+    bitonic_sort(bkey, bval, np2);
+    // approximate walk: index of the last begun item
+    if (tid == 0) s_lastb = -1;
+    __syncthreads();
+    unsigned long long carry = taken_w;
+    for (uint32_t t0 = 0; t0 < nbk; t0 += blockDim.x) {
+      const uint32_t i = t0 + tid;
+      unsigned long long sz = i < nbk ? (unsigned long long)ssize[bval[i]] : 0ull;
+      unsigned long long tile;
+      unsigned long long excl = block_exclusive_scan(sz, red64, &tile);
+      if (i < nbk && taken_c + i < kept && carry + excl < budget) atomicMax(&s_lastb, (int)i);
+      carry += tile;
+    }
+    __syncthreads();
+    vstar = key_to_f64(bkey[max(s_lastb, 0)]);
+  }
+
+  // ---- 3. window around v*: exact scores, sorted, walked from A's prefix
+  const double wlo = vstar - 3.0 * E, whi = vstar + 3.0 * E;
+  uint64_t nA = 0, wA = 0;
+  if (tid == 0) { s_nw = 0; s_nemit = 0; }
+  __syncthreads();
+  {
+    uint64_t c = 0, w = 0;
+    for (int64_t f = tid; f < total; f += blockDim.x) {
+      const double sc = sscore[f];
+      if (sc < wlo) {
+        c += 1;
+        w += (uint64_t)ssize[f];
+      } else if (sc <= whi && !no_cut) {
+        uint32_t p = atomicAdd(&s_nw, 1u);
+        if (p < WCAP) wval[p] = (uint32_t)f;
+      }
+    }
+    nA = block_sum((unsigned long long)c, red64);
+    wA = block_sum((unsigned long long)w, red64);
+  }
+  const uint32_t nw = s_nw;
+  if (nw > WCAP) flag = true;
+  uint32_t lastw = 0;
+  bool ended = no_cut;
+  if (!flag && !no_cut) {
+    // exact float64 scores of the window (8-lane groups)
+    const int grp = tid >> 3, ngrp = blockDim.x >> 3, gl = tid & 7;
+    for (uint32_t i0 = 0; i0 < nw; i0 += ngrp) {
+      const uint32_t i = i0 + grp;
+      const int64_t f = i < nw ? wval[i] : 0;
+      const int p = (int)(f / G), j = (int)(f % G);
+      const int r = reg[p];
+      double score = qc2[p];
+      if (ix.grouping) {
+        const int64_t gi = (int64_t)r * G + j;
+        double qs2 = group8_sqdist64(ix.centroids + (int64_t)ix.nbr[gi] * d, qd, d);
+        const double al = (double)ix.alphas[r];
+        score = dadd(dadd(dmul(dsub(1.0, al), qc2[p]), dmul(al, qs2)), (double)ix.norm[gi]);
+      }
+      if (i < nw && gl == 0) wkey[i] = f64_key(score);
+    }
+    const uint32_t np2 = next_pow2(max(nw, 1u));
+    for (uint32_t i = nw + tid; i < np2; i += blockDim.x) { wkey[i] = kKeyPad; wval[i] = 0xffffffffu; }
+    __syncthreads();
+    bitonic_sort(wkey, wval, np2);
+    // exact walk over W starting from A's count/weight
+    if (tid == 0) s_lastb = -1;
+    __syncthreads();
+    unsigned long long carry = wA;
+    for (uint32_t t0 = 0; t0 < nw; t0 += blockDim.x) {
+      const uint32_t i = t0 + tid;
+      unsigned long long sz = i < nw ? (unsigned long long)ssize[wval[i]] : 0ull;
+      unsigned long long tile;
+      unsigned long long excl = block_exclusive_scan(sz, red64, &tile);
+      if (i < nw) {
+        const unsigned long long w = carry + excl;
+        const bool ok = (nA + i < kept) && (w < budget);
+        wlen[i] = ok ? (int32_t)min(sz, budget - w) : 0;
+        if (ok) atomicMax(&s_lastb, (int)i);
+      }
+      carry += tile;
+    }
+    __syncthreads();
+    const int xc = s_lastb;
+    if (xc < 0) {
+      flag = true;  // the exact crossing precedes the window
+    } else {
+      lastw = (uint32_t)xc;
+      const double sx = key_to_f64(wkey[xc]);
+      if (!(sx >= vstar - 2.0 * E && sx <= vstar + 2.0 * E)) flag = true;
+      // the walk must end at or inside W: the item after x_c is not begun
+      if ((uint32_t)xc + 1 == nw) ended = (nA + nw >= kept) || (carry >= budget);
+      else ended = true;
+      if (!ended) flag = true;
+    }
+  }
+  if (flag) {
+    if (tid == 0) a.only[b] = 1;
+    return;
+  }
+  if (tid == 0) a.only[b] = 0;
+
+  // ---- 4. emit A + begun W with exact base/score (local rows of this shard)
+  WorkItem* W = a.work + (int64_t)b * a.cap_w;
+  auto emit = [&](int64_t f, int64_t len_g) {
+    const int p = (int)(f / G), j = (int)(f % G);
+    const int64_t gi = (int64_t)reg[p] * G + j;
+    const int64_t lo_ = ix.llo ? ix.llo[gi] : 0;
+    const int64_t cnt_ = ix.lsize ? ix.lsize[gi] : ix.gsize[gi];
+    const int64_t ll = min(max(len_g - lo_, (int64_t)0), cnt_);
+    if (ll <= 0) return;
+    const int pos = atomicAdd(&s_nemit, 1);
+    if (pos >= a.cap_w) return;
+    WorkItem w;
+    w.start = ix.lstart[gi];
+    w.len = (int32_t)ll;
+    w.flat = (int32_t)f;
+    w.base = 0.0;
+    w.score = 0.0;
+    W[pos] = w;
+  };
+  uint64_t begun_w = 0, scanned_w = 0;
+  for (int64_t f = tid; f < total; f += blockDim.x)
+    if (sscore[f] < wlo) emit(f, ssize[f]);
+  for (uint32_t i = tid; i < nw && !no_cut; i += blockDim.x) {
+    if (i <= lastw) {
+      begun_w += 1;
+      scanned_w += (uint64_t)wlen[i];
+      if (wlen[i] > 0) emit(wval[i], wlen[i]);
+    }
+  }
+  begun_w = block_sum((unsigned long long)begun_w, red64);
+  scanned_w = block_sum((unsigned long long)scanned_w, red64);
+  const int nemit = min(s_nemit, (int)a.cap_w);
+  {
+    const int grp = tid >> 3, ngrp = blockDim.x >> 3, gl = tid & 7;
+    for (int i0 = 0; i0 < nemit; i0 += ngrp) {
+      const int i = i0 + grp;
+      const int64_t f = i < nemit ? W[i].flat : 0;
+      const int p = (int)(f / G), j = (int)(f % G);
+      const int r = reg[p];
+      double base = qc2[p], score = qc2[p];
+      if (ix.grouping) {
+        const int64_t gi = (int64_t)r * G + j;
+        double qs2 = group8_sqdist64(ix.centroids + (int64_t)ix.nbr[gi] * d, qd, d);
+        const double al = (double)ix.alphas[r];
+        base = dadd(dmul(dsub(1.0, al), qc2[p]), dmul(al, qs2));
+        score = dadd(base, (double)ix.norm[gi]);
+      }
+      if (i < nemit && gl == 0) { W[i].base = base; W[i].score = score; }
+    }
+  }
+  if (tid == 0) {
+    a.nwork[b] = nemit;
+    int64_t* st = a.stats + (int64_t)b * 4;
+    st[0] = P;
+    st[1] = (int64_t)(nA + begun_w);
+    st[2] = total - (int64_t)kept;
+    st[3] = (int64_t)(wA + scanned_w);
+  }
+  if (a.sort_work) {
+    __syncthreads();
+    uint32_t wp2 = next_pow2(max(nemit, 1));
+    int64_t cp2 = 1;
+    while (cp2 < a.cap_w) cp2 <<= 1;
+    uint64_t* sk = a.skey + (int64_t)b * cp2;
+    uint32_t* sv = a.sval + (int64_t)b * cp2;
+    for (uint32_t i = tid; i < wp2; i += blockDim.x) {
+      sk[i] = (int)i < nemit ? f64_key(W[i].score) : kKeyPad;
+      sv[i] = (int)i < nemit ? (uint32_t)W[i].flat : 0xffffffffu;
+    }
+    __syncthreads();
+    bitonic_sort(sk, sv, wp2);
+    for (int i = tid; i < nemit; i += blockDim.x) {
+      uint64_t key = f64_key(W[i].score);
+      uint32_t fl = (uint32_t)W[i].flat;
+      int lo_i = 0, hi_i = nemit - 1;
+      while (lo_i < hi_i) {
+        int mid = (lo_i + hi_i) >> 1;
+        bool less = sk[mid] < key || (sk[mid] == key && sv[mid] < fl);
+        if (less) lo_i = mid + 1; else hi_i = mid;
+      }
+      a.order[(int64_t)b * a.cap_w + lo_i] = i;
+    }
+  }
 }
 
-void launch_plan(const PlanArgs& a, cudaStream_t s) {
-  size_t sm = plan_smem(a.ix.d);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    attr = true;
+size_t plan_smem(int d) {
+  (void)d;
+  return (size_t)PLAN_BUCKETS * 8 + SORTCAP * 8 + PLAN_BUCKETS * 4 + SORTCAP * 4 + SORTCAP * 4 + 16;
+}
+
+size_t plan_approx_smem(int d) {
+  return (size_t)PLAN_BUCKETS * 8 + SORTCAP * 8 + WCAP * 8 + PLAN_BUCKETS * 4 + SORTCAP * 4 +
+         SORTCAP * 4 + WCAP * 4 + WCAP * 4 + (size_t)d * 8 + 16;
+}
+
+int launch_plan(const PlanArgs& a, cudaStream_t s) {
+  if (a.D != nullptr && a.only != nullptr) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_plan_approx, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      attr = true;
+    }
+    k_plan_approx<<<a.nq, PLAN_THREADS, plan_approx_smem(a.ix.d), s>>>(a);
+    k_plan_score<<<a.nq, PLAN_THREADS, 0, s>>>(a);
+    k_plan_select<<<a.nq, PLAN_THREADS, plan_smem(a.ix.d), s>>>(a);
+    return 3;
   }
-  k_plan<<<a.nq, PLAN_THREADS, sm, s>>>(a);
+  PlanArgs e = a;
+  e.only = nullptr;
+  k_plan_score<<<a.nq, PLAN_THREADS, 0, s>>>(e);
+  k_plan_select<<<a.nq, PLAN_THREADS, plan_smem(a.ix.d), s>>>(e);
+  return 2;
 }
 
 }  // namespace givf
