@@ -99,6 +99,11 @@ int givf_index_create(const givf_index_desc* desc, int device, givf_index_t* out
 int givf_index_destroy(givf_index_t index);
 /* bytes of device memory held by the index arrays */
 int64_t givf_index_device_bytes(givf_index_t index);
+/* Cumulative counts of queries that left the fast path: out[0] = probe
+ * candidate sets the float64 re-check could not certify (exhaustive ranking
+ * ran instead), out[1] = approximate plans that fell back to the exact
+ * planner.  Synchronises the device. */
+int givf_index_counters(givf_index_t index, int64_t* out, int32_t n);
 
 /* queries (nq, dim) f32.  ids (nq, k) int32 padded with -1, dists (nq, k)
  * f32 padded with +inf, stats (nq) -- host or device; stream = cudaStream_t

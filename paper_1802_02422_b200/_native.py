@@ -21,6 +21,7 @@ EXPORTS = (
     "givf_index_create",
     "givf_index_destroy",
     "givf_index_device_bytes",
+    "givf_index_counters",
     "givf_search_topk",
     "givf_search_full",
     "givf_probe",
@@ -101,6 +102,7 @@ def load(path: str = LIB_PATH):
     lib.givf_index_destroy.argtypes = [vp]
     lib.givf_index_device_bytes.argtypes = [vp]
     lib.givf_index_device_bytes.restype = i64
+    lib.givf_index_counters.argtypes = [vp, vp, i32]
     lib.givf_search_topk.argtypes = [vp, vp, i64, ctypes.POINTER(SearchParamsC), i32, vp, vp, vp, vp]
     lib.givf_search_full.argtypes = [vp, vp, i64, ctypes.POINTER(SearchParamsC), i64, vp, vp, vp, vp]
     lib.givf_probe.argtypes = [vp, vp, i64, i32, vp, vp, vp]

@@ -200,6 +200,13 @@ int check_params(const givf_index* ix, const givf_search_params* p) {
   return GIVF_OK;
 }
 
+size_t l2_budget() {
+  const char* s = getenv("GIVF_L2_CHUNK_MB");
+  // measured on C2: per-chunk launch/tail costs outweigh L2 residency, so the
+  // cap is off unless requested
+  return (size_t)(s ? atoll(s) : (1ll << 20)) << 20;
+}
+
 size_t workspace_budget() {
   const char* s = getenv("GIVF_WORKSPACE_MB");
   size_t mb = s ? (size_t)atoll(s) : 3072;
@@ -228,13 +235,29 @@ struct Plan {
   ProbeShape ps;
 };
 
+// A-priori bounds on |s~ - (|c|^2 - 2 q.c)| in units of (cmax^2 + 2|q| cmax):
+//  SIMT fp32 FMA chain: ~(d + 4) ulp, x3 margin;
+//  tcgen05 bf16x3: 2^-16 split residual + fp32 tensor-core accumulation over
+//  3d/16 k-steps (alignment/truncation), ~6e-5 -> x4 margin.
 constexpr float kEpsScaleUlp = 5.9604645e-8f;  // 2^-24
 float probe_eps_scale(int d) { return 3.0f * (float)(d + 4) * kEpsScaleUlp; }
+constexpr float kEpsScaleTC = 2.5e-4f;
+
+bool use_tensor_cores(const IndexView& v) {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("GIVF_PROBE");
+    mode = (e && strcmp(e, "simt") == 0) ? 0 : 1;
+  }
+  return mode == 1 && v.csplit != nullptr;
+}
 
 // Probe for one chunk of queries: regions (nq, P) and qc2 (nq, P).  *D_out
-// receives the fp32 score matrix (nq, K) when the GEMM path ran, else null.
+// receives the fp32 score matrix (nq, K) when the GEMM path ran, else null;
+// *eps_out its error-bound scale.
 int run_probe(givf_index* ix, const Plan& pl, const float* dQ, int nq, int* regions,
-              double* qc2, Arena& ar, cudaStream_t st, const float** D_out = nullptr) {
+              double* qc2, Arena& ar, cudaStream_t st, const float** D_out = nullptr,
+              float* eps_out = nullptr) {
   const IndexView& v = ix->v;
   const int P = pl.P, K = v.K, d = v.d;
   if (D_out) *D_out = nullptr;
@@ -264,14 +287,26 @@ int run_probe(givf_index* ix, const Plan& pl, const float* dQ, int nq, int* regi
   int* cand = ar.take<int>((size_t)nq * pl.ps.cap);
   int* cand_n = ar.take<int>(nq);
   float* theta = ar.take<float>(nq);
-  staged(ST_GEMM, st, [&] { launch_probe_gemm(dQ, v.centroids, v.c2f, nq, K, d, D, K, st); });
+  const int ntiles = probe_tiles(K);
+  float* tmin = ar.take<float>((size_t)nq * ntiles);
+  const bool tc = use_tensor_cores(v);
+  if (tc) {
+    void* abf = ar.take<uint16_t>((size_t)nq * tc_kpad(d));
+    staged(ST_GEMM, st, [&] {
+      launch_split_bf16(dQ, nq, d, 0, abf, st);
+      launch_probe_gemm_tc(abf, v.csplit, v.c2f, nq, K, d, D, K, tmin, st);
+    }, 2);
+  } else {
+    staged(ST_GEMM, st, [&] { launch_probe_gemm(dQ, v.centroids, v.c2f, nq, K, d, D, K, tmin, st); });
+  }
   staged(ST_SELECT, st, [&] {
-    launch_probe_select(D, K, nq, K, pl.ps.Tmin, pl.ps.cap, cand, cand_n, theta, st);
+    launch_probe_select(D, K, nq, K, pl.ps.Tmin, pl.ps.cap, tmin, ntiles, cand, cand_n, theta, st);
   });
-  const float eps_scale = probe_eps_scale(d);
+  const float eps_scale = tc ? kEpsScaleTC : probe_eps_scale(d);
+  if (eps_out) *eps_out = eps_scale;
   staged(ST_RECHECK, st, [&] {
     launch_probe_recheck(dQ, v.centroids, nq, K, d, P, cand, cand_n, pl.ps.cap, theta, v.cmax,
-                         eps_scale, regions, qc2, failf, st);
+                         eps_scale, regions, qc2, failf, v.counters, st);
   });
   staged(ST_FULL, st, [&] {
     launch_probe_full(dQ, v.centroids, nq, K, d, P, 1, failf, slots, sk, sv, sk2, sv2, sdv,
@@ -283,7 +318,9 @@ int run_probe(givf_index* ix, const Plan& pl, const float* dQ, int nq, int* regi
 
 size_t probe_bytes_per_query(const Plan& pl) {
   size_t b = aligned_bytes<int>(1) * 4 + aligned_bytes<int>(pl.P) + aligned_bytes<double>(pl.P);
-  if (!pl.ps.exhaustive) b += (size_t)pl.K * 4 + (size_t)pl.ps.cap * 4;
+  if (!pl.ps.exhaustive)
+    b += (size_t)pl.K * 4 + (size_t)pl.ps.cap * 4 + aligned_bytes<float>(probe_tiles(pl.K)) +
+         (size_t)tc_kpad(pl.d) * 2 + 256;
   return b;
 }
 size_t probe_fixed_bytes(const Plan& pl) {
@@ -350,6 +387,12 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
   const size_t fixed = probe_fixed_bytes(pl) + (1 << 16);
   const size_t budget = workspace_budget();
   int64_t chunk = budget > fixed ? (int64_t)((budget - fixed) / per_q) : 1;
+  // Keep one chunk's probe scores + plan scratch resident in the 126 MB L2:
+  // they are written and re-read by the select / plan kernels right away.
+  const size_t hot = (pl.ps.exhaustive ? 0 : (size_t)pl.K * 4) + (size_t)pl.total * 20 +
+                     (size_t)pl.cap_w * 32;
+  chunk = std::min<int64_t>(chunk, std::max<int64_t>(128, (int64_t)(l2_budget() / hot)));
+  if (const char* e = getenv("GIVF_CHUNK_QUERIES")) chunk = std::max<int64_t>(1, atoll(e));
   chunk = std::max<int64_t>(1, std::min<int64_t>(chunk, nq));
   chunk = std::min<int64_t>(chunk, 65535);
   CUDA_TRY(ix->arena.reserve(fixed + per_q * (size_t)chunk + (1 << 20)));
@@ -370,7 +413,8 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
     int* regions = ar.take<int>((size_t)bq * pl.P);
     double* qc2 = ar.take<double>((size_t)bq * pl.P);
     const float* Dmat = nullptr;
-    rc = run_probe(ix, pl, dQ, bq, regions, qc2, ar, st, &Dmat);
+    float eps_scale = 0.f;
+    rc = run_probe(ix, pl, dQ, bq, regions, qc2, ar, st, &Dmat, &eps_scale);
     if (rc) return rc;
 
     PlanArgs pa{};
@@ -400,7 +444,7 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
     pa.D = Dmat;
     pa.ldD = v.K;
     pa.cmax = v.cmax;
-    pa.eps_scale = probe_eps_scale(v.d);
+    pa.eps_scale = eps_scale;
     pa.only = Dmat ? ar.take<int>(bq) : nullptr;
     int nk = 0;
     staged(ST_PLAN, st, [&] { nk = launch_plan(pa, st); }, 0);
@@ -456,8 +500,8 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
       CUDA_TRY(cudaMemcpyAsync(stats + q0, dstats, sizeof(int64_t) * 4 * bq,
                                cudaMemcpyDeviceToHost, st));
     }
-    // the arena is reused by the next chunk: finish this one first
-    if (q0 + chunk < nq) CUDA_TRY(cudaStreamSynchronize(st));
+    // the next chunk reuses the arena: its copies and kernels are ordered
+    // after this chunk's on the same stream, so no host synchronisation
   }
   if (!out_dev || !st_dev || !q_dev) CUDA_TRY(cudaStreamSynchronize(st));
   return GIVF_OK;
@@ -589,6 +633,28 @@ int givf_index_create(const givf_index_desc* ds, int device, givf_index_t* out) 
   if (ds->rotation) UP(ds->rotation, (size_t)d * d, rotation);
   UP(ctab, (size_t)256, ctab);
 #undef UP
+  if (e == cudaSuccess) {
+    unsigned long long* cnt = nullptr;
+    e = cudaMalloc(&cnt, 64);
+    if (e == cudaSuccess) {
+      ix->allocs.push_back(cnt);
+      e = cudaMemset(cnt, 0, 64);
+      v.counters = cnt;
+    }
+  }
+  if (e == cudaSuccess && tc_supported(d)) {
+    // bf16 split of the centroids for the tensor-core probe (probe_tc.cu)
+    void* cs = nullptr;
+    const size_t bytes = (size_t)K * tc_kpad(d) * 2;
+    e = cudaMalloc(&cs, bytes);
+    if (e == cudaSuccess) {
+      ix->allocs.push_back(cs);
+      ix->dev_bytes += (int64_t)bytes;
+      launch_split_bf16(v.centroids, K, d, 1, cs, 0);
+      e = cudaDeviceSynchronize();
+      v.csplit = cs;
+    }
+  }
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ix->stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
     givf_index_destroy(ix);
@@ -611,6 +677,16 @@ int givf_index_destroy(givf_index_t ix) {
 }
 
 int64_t givf_index_device_bytes(givf_index_t ix) { return ix ? ix->dev_bytes : 0; }
+
+int givf_index_counters(givf_index_t ix, int64_t* out, int32_t n) {
+  if (!ix || !out) return fail(GIVF_EINVAL, "null argument");
+  unsigned long long h[8] = {};
+  CUDA_TRY(cudaSetDevice(ix->device));
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpy(h, ix->v.counters, sizeof h, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < n && i < 8; ++i) out[i] = (int64_t)h[i];
+  return GIVF_OK;
+}
 
 int givf_search_topk(givf_index_t ix, const float* queries, int64_t nq,
                      const givf_search_params* params, int32_t k, int32_t* ids, float* dists,

@@ -41,18 +41,30 @@ struct IndexView {
   const float* codewords;     // (M, 256, d/M)
   const float* rotation;      // (d, d) or null
   const float* ctab;          // (256) dequantized constants, f32
+  const void* csplit;         // (K, tc_kpad(d)) bf16 [c_hi | c_lo | c_hi] or null
+  unsigned long long* counters;  // [0] probe fallbacks, [1] plan fallbacks (device)
 };
 
+// probe_tc.cu: tcgen05 bf16x3 probe GEMM
+int tc_kpad(int d);
+bool tc_supported(int d);
+size_t tc_smem_bytes(int d);
+void launch_split_bf16(const float* x, int rows, int d, int centroid, void* out, cudaStream_t s);
+bool launch_probe_gemm_tc(const void* Abf, const void* Bbf, const float* c2, int nq, int K, int d,
+                          float* D, int64_t ldD, float* tmin, cudaStream_t s);
+
 // probe.cu
+int probe_tiles(int K);  // per-query tile minima the GEMM epilogue emits
 void launch_probe_gemm(const float* Q, const float* C, const float* c2, int nq, int K, int d,
-                       float* D, int64_t ldD, cudaStream_t s);
+                       float* D, int64_t ldD, float* tmin, cudaStream_t s);
 void launch_probe_select(const float* D, int64_t ldD, int nq, int K, int Tmin, int cap,
-                         int* cand, int* cand_n, float* theta, cudaStream_t s);
+                         const float* tmin, int ntiles, int* cand, int* cand_n, float* theta,
+                         cudaStream_t s);
 size_t probe_recheck_smem(int d, int P, int cap);
 void launch_probe_recheck(const float* Q, const float* C, int nq, int K, int d, int P,
                           const int* cand, const int* cand_n, int cap, const float* theta,
                           float cmax, float eps_scale, int* regions, double* qc2, int* fail,
-                          cudaStream_t s);
+                          unsigned long long* fail_count, cudaStream_t s);
 void launch_probe_full(const float* Q, const float* C, int nq, int K, int d, int P, int mode,
                        const int* fail, int nslots, uint64_t* sk, uint32_t* sv, uint64_t* sk2,
                        uint32_t* sv2, double* sdv, int* regions, double* qc2, cudaStream_t s);

@@ -692,7 +692,10 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan_approx(PlanArgs a) {
     }
   }
   if (flag) {
-    if (tid == 0) a.only[b] = 1;
+    if (tid == 0) {
+      a.only[b] = 1;
+      if (ix.counters) atomicAdd(&ix.counters[1], 1ull);
+    }
     return;
   }
   if (tid == 0) a.only[b] = 0;

@@ -29,7 +29,7 @@ constexpr int PG_BM = 64, PG_BN = 128, PG_BK = 16;
 __global__ void __launch_bounds__(256)
 k_probe_gemm(const float* __restrict__ Q, const float* __restrict__ C,
              const float* __restrict__ c2, int nq, int K, int d,
-             float* __restrict__ D, int64_t ldD) {
+             float* __restrict__ D, int64_t ldD, float* __restrict__ tmin) {
   __shared__ float As[PG_BK][PG_BM + 4];
   __shared__ float Bs[PG_BK][PG_BN + 4];
   const int tid = threadIdx.x;
@@ -72,15 +72,26 @@ k_probe_gemm(const float* __restrict__ Q, const float* __restrict__ C,
     }
     __syncthreads();
   }
+  // epilogue: scores + the per-(query, 128-centroid tile) minimum that lets
+  // k_probe_select bound the T-th smallest score without a histogram pass
+  const int ntiles = (K + PG_BN - 1) / PG_BN;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     int qr = q0 + ty * 4 + i;
-    if (qr >= nq) continue;
+    float mn = __int_as_float(0x7f800000);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       int cr = c0 + tx * 8 + j;
-      if (cr < K) D[(int64_t)qr * ldD + cr] = fmaf(-2.f, acc[i][j], c2[cr]);
+      if (cr < K) {
+        float v = fmaf(-2.f, acc[i][j], c2[cr]);
+        mn = fminf(mn, v);
+        if (qr < nq) D[(int64_t)qr * ldD + cr] = v;
+      }
     }
+    // 16 threads (tx) share a row: reduce within each half-warp
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    if (tx == 0 && qr < nq && tmin) tmin[(int64_t)qr * ntiles + blockIdx.x] = mn;
   }
 }
 
@@ -91,23 +102,14 @@ k_probe_gemm(const float* __restrict__ Q, const float* __restrict__ C,
 constexpr int SEL_THREADS = 512;
 constexpr int SEL_BUCKETS = 2048;
 
-__global__ void __launch_bounds__(SEL_THREADS)
-k_probe_select(const float* __restrict__ D, int64_t ldD, int K, int Tmin, int cap,
-               int* __restrict__ cand, int* __restrict__ cand_n,
-               float* __restrict__ theta) {
-  __shared__ uint32_t hist[SEL_BUCKETS];
+// Generic path: bucketed refinement over the whole row (any K, any ties).
+__device__ void select_bucketed(const float* __restrict__ row, int K, int Tmin, int cap,
+                                int* __restrict__ out, int* __restrict__ n_out,
+                                float* __restrict__ theta_out, uint32_t* hist) {
   __shared__ uint32_t red[40];
   __shared__ uint32_t s_b, s_before, s_through;
   __shared__ uint32_t cnt_lt, cnt_eq;
-  const float* row = D + (int64_t)blockIdx.x * ldD;
-  int* out = cand + (int64_t)blockIdx.x * cap;
   const int tid = threadIdx.x;
-
-  if (K <= cap) {
-    for (int i = tid; i < K; i += blockDim.x) out[i] = i;
-    if (tid == 0) { cand_n[blockIdx.x] = K; theta[blockIdx.x] = __int_as_float(0x7f800000); }
-    return;
-  }
   uint32_t mn = 0xffffffffu, mx = 0u;
   for (int i = tid; i < K; i += blockDim.x) {
     uint32_t k = f32_key(row[i]);
@@ -184,8 +186,85 @@ k_probe_select(const float* __restrict__ D, int64_t ldD, int K, int Tmin, int ca
   ex = block_min(ex, red);
   if (tid == 0) {
     uint32_t n = cnt_lt + (degenerate ? min(cnt_eq, (uint32_t)cap - deg_before) : 0u);
-    cand_n[blockIdx.x] = (int)n;
-    theta[blockIdx.x] = ex == 0xffffffffu ? __int_as_float(0x7f800000) : key_f32(ex);
+    *n_out = (int)n;
+    *theta_out = ex == 0xffffffffu ? __int_as_float(0x7f800000) : key_f32(ex);
+  }
+}
+
+// Fast path: the GEMM epilogue left the minimum of every 128-centroid tile.
+// At least Tmin scores are <= the Tmin-th smallest tile minimum theta_up, so
+// one pass collecting {s~ <= theta_up} yields a superset of the Tmin smallest;
+// theta = the smallest score left out.  Falls back to select_bucketed when
+// the collection overflows its buffer.
+constexpr int SEL_COLLECT = 4096;
+
+__global__ void __launch_bounds__(SEL_THREADS)
+k_probe_select(const float* __restrict__ D, int64_t ldD, int K, int Tmin, int cap,
+               const float* __restrict__ tmin, int ntiles,
+               int* __restrict__ cand, int* __restrict__ cand_n, float* __restrict__ theta) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ uint32_t red[40];
+  __shared__ uint32_t s_cnt;
+  const float* row = D + (int64_t)blockIdx.x * ldD;
+  int* out = cand + (int64_t)blockIdx.x * cap;
+  const int tid = threadIdx.x;
+
+  if (K <= cap) {
+    for (int i = tid; i < K; i += blockDim.x) out[i] = i;
+    if (tid == 0) { cand_n[blockIdx.x] = K; theta[blockIdx.x] = __int_as_float(0x7f800000); }
+    return;
+  }
+  uint32_t* hist = reinterpret_cast<uint32_t*>(dsm);  // SEL_BUCKETS, aliases tk below
+  if (tmin == nullptr || ntiles < Tmin) {
+    select_bucketed(row, K, Tmin, cap, out, cand_n + blockIdx.x, theta + blockIdx.x, hist);
+    return;
+  }
+  // 1. theta_up = Tmin-th smallest tile minimum (bitonic over <= 8192 keys)
+  uint32_t* tk = reinterpret_cast<uint32_t*>(dsm);
+  uint64_t* ck = reinterpret_cast<uint64_t*>(dsm + 8192 * 4);
+  const uint32_t tp2 = next_pow2((uint32_t)ntiles);
+  const float* trow = tmin + (int64_t)blockIdx.x * ntiles;
+  for (uint32_t i = tid; i < tp2; i += blockDim.x) tk[i] = i < (uint32_t)ntiles ? f32_key(trow[i]) : 0xffffffffu;
+  __syncthreads();
+  bitonic_sort_keys(tk, tp2);
+  const uint32_t up = tk[Tmin - 1];
+  if (tid == 0) s_cnt = 0;
+  __syncthreads();
+  // 2. one pass over the row: collect keys <= up, track the smallest key above
+  uint32_t ex = 0xffffffffu;
+  for (int i = tid; i < K; i += blockDim.x) {
+    uint32_t k = f32_key(row[i]);
+    if (k <= up) {
+      uint32_t p = atomicAdd(&s_cnt, 1u);
+      if (p < SEL_COLLECT) ck[p] = ((uint64_t)k << 32) | (uint32_t)i;
+    } else {
+      ex = min(ex, k);
+    }
+  }
+  ex = block_min(ex, red);  // also orders the collection before its use
+  const uint32_t n = s_cnt;
+  if (n > (uint32_t)SEL_COLLECT) {
+    __syncthreads();
+    select_bucketed(row, K, Tmin, cap, out, cand_n + blockIdx.x, theta + blockIdx.x, hist);
+    return;
+  }
+  if (n <= (uint32_t)cap) {
+    for (uint32_t i = tid; i < n; i += blockDim.x) out[i] = (int)(uint32_t)ck[i];
+    if (tid == 0) {
+      cand_n[blockIdx.x] = (int)n;
+      theta[blockIdx.x] = ex == 0xffffffffu ? __int_as_float(0x7f800000) : key_f32(ex);
+    }
+    return;
+  }
+  // 3. more than cap collected: keep the cap smallest, theta = the next one
+  const uint32_t np2 = next_pow2(n);
+  for (uint32_t i = n + tid; i < np2; i += blockDim.x) ck[i] = kKeyPad;
+  __syncthreads();
+  bitonic_sort_keys(ck, np2);
+  for (int i = tid; i < cap; i += blockDim.x) out[i] = (int)(uint32_t)ck[i];
+  if (tid == 0) {
+    cand_n[blockIdx.x] = cap;
+    theta[blockIdx.x] = key_f32((uint32_t)(ck[cap] >> 32));
   }
 }
 
@@ -252,7 +331,8 @@ __global__ void __launch_bounds__(256)
 k_probe_recheck(const float* __restrict__ Q, const float* __restrict__ C, int K, int d,
                 int P, const int* __restrict__ cand, const int* __restrict__ cand_n,
                 int cap, const float* __restrict__ theta, float cmax, float eps_scale,
-                int* __restrict__ regions, double* __restrict__ qc2, int* __restrict__ fail) {
+                int* __restrict__ regions, double* __restrict__ qc2, int* __restrict__ fail,
+                unsigned long long* fail_count) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int capp2 = (int)next_pow2((uint32_t)cap);
   const int pp2 = (int)next_pow2((uint32_t)P);
@@ -296,7 +376,10 @@ k_probe_recheck(const float* __restrict__ Q, const float* __restrict__ C, int K,
     double th = (double)theta[b];
     bool ok = (n >= P) && (dp - q2 < th - eps);
     if (!ok) {
-      if (threadIdx.x == 0) fail[b] = 1;
+      if (threadIdx.x == 0) {
+        fail[b] = 1;
+        if (fail_count) atomicAdd(fail_count, 1ull);
+      }
       return;
     }
   }
@@ -345,15 +428,25 @@ k_probe_full(const float* __restrict__ Q, const float* __restrict__ C, int nq, i
 }
 
 // ----------------------------------------------------------------- launchers
+int probe_tiles(int K) { return (K + PG_BN - 1) / PG_BN; }
+
 void launch_probe_gemm(const float* Q, const float* C, const float* c2, int nq, int K, int d,
-                       float* D, int64_t ldD, cudaStream_t s) {
+                       float* D, int64_t ldD, float* tmin, cudaStream_t s) {
   dim3 grid((K + PG_BN - 1) / PG_BN, (nq + PG_BM - 1) / PG_BM);
-  k_probe_gemm<<<grid, 256, 0, s>>>(Q, C, c2, nq, K, d, D, ldD);
+  k_probe_gemm<<<grid, 256, 0, s>>>(Q, C, c2, nq, K, d, D, ldD, tmin);
 }
 
 void launch_probe_select(const float* D, int64_t ldD, int nq, int K, int Tmin, int cap,
-                         int* cand, int* cand_n, float* theta, cudaStream_t s) {
-  k_probe_select<<<nq, SEL_THREADS, 0, s>>>(D, ldD, K, Tmin, cap, cand, cand_n, theta);
+                         const float* tmin, int ntiles, int* cand, int* cand_n, float* theta,
+                         cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_probe_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    attr = true;
+  }
+  if (ntiles > 8192) tmin = nullptr;  // tile keys must fit the 32 KB staging area
+  k_probe_select<<<nq, SEL_THREADS, 8192 * 4 + SEL_COLLECT * 8, s>>>(D, ldD, K, Tmin, cap, tmin,
+                                                                      ntiles, cand, cand_n, theta);
 }
 
 size_t probe_recheck_smem(int d, int P, int cap) {
@@ -366,7 +459,7 @@ size_t probe_recheck_smem(int d, int P, int cap) {
 void launch_probe_recheck(const float* Q, const float* C, int nq, int K, int d, int P,
                           const int* cand, const int* cand_n, int cap, const float* theta,
                           float cmax, float eps_scale, int* regions, double* qc2, int* fail,
-                          cudaStream_t s) {
+                          unsigned long long* fail_count, cudaStream_t s) {
   size_t sm = probe_recheck_smem(d, P, cap);
   static bool attr = false;
   if (!attr) {
@@ -374,7 +467,7 @@ void launch_probe_recheck(const float* Q, const float* C, int nq, int K, int d, 
     attr = true;
   }
   k_probe_recheck<<<nq, 256, sm, s>>>(Q, C, K, d, P, cand, cand_n, cap, theta, cmax, eps_scale,
-                                      regions, qc2, fail);
+                                      regions, qc2, fail, fail_count);
 }
 
 void launch_probe_full(const float* Q, const float* C, int nq, int K, int d, int P, int mode,

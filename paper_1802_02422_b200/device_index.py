@@ -176,6 +176,12 @@ class DeviceIndex:
     def device_bytes(self) -> int:
         return int(_native.load().givf_index_device_bytes(self._h))
 
+    def fallback_counts(self) -> dict:
+        """Queries that left the fast path so far (probe re-check / planner)."""
+        out = np.zeros(2, np.int64)
+        _native.check(_native.load().givf_index_counters(self._h, out.ctypes.data, 2))
+        return {"probe": int(out[0]), "plan": int(out[1])}
+
     def close(self):
         if getattr(self, "_h", None):
             _native.load().givf_index_destroy(self._h)
