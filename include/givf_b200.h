@@ -121,6 +121,12 @@ int givf_search_full(givf_index_t index, const float* queries, int64_t nq,
                      const givf_search_params* params, int64_t capacity, int32_t* ids,
                      float* dists, givf_search_stats* stats, void* stream);
 
+/* K1a alone (parity / accuracy checks): approximate region scores
+ * s~[q, c] = |c|^2 - 2 q.c, (nq, k) f32, and the scale of their a-priori
+ * error bound: |s~ - exact| <= eps_scale * (max|c|^2 + 2 |q| max|c|). */
+int givf_probe_scores(givf_index_t index, const float* queries, int64_t nq, float* scores,
+                      float* eps_scale, void* stream);
+
 /* Region probe: region ids (nq, nprobe) int32 and float64 qc2 (nq, nprobe). */
 int givf_probe(givf_index_t index, const float* queries, int64_t nq, int32_t nprobe,
                int32_t* regions, double* qc2, void* stream);

@@ -24,6 +24,7 @@ EXPORTS = (
     "givf_index_counters",
     "givf_search_topk",
     "givf_search_full",
+    "givf_probe_scores",
     "givf_probe",
     "givf_merge_topk",
     "givf_kernel_launches",
@@ -106,6 +107,7 @@ def load(path: str = LIB_PATH):
     lib.givf_search_topk.argtypes = [vp, vp, i64, ctypes.POINTER(SearchParamsC), i32, vp, vp, vp, vp]
     lib.givf_search_full.argtypes = [vp, vp, i64, ctypes.POINTER(SearchParamsC), i64, vp, vp, vp, vp]
     lib.givf_probe.argtypes = [vp, vp, i64, i32, vp, vp, vp]
+    lib.givf_probe_scores.argtypes = [vp, vp, i64, vp, vp, vp]
     lib.givf_merge_topk.argtypes = [vp, vp, i32, i64, i32, vp, vp, ctypes.c_int, vp]
     lib.givf_kernel_launches.restype = i64
     lib.givf_profile_enable.argtypes = [ctypes.c_int]

@@ -702,6 +702,47 @@ int givf_search_full(givf_index_t ix, const float* queries, int64_t nq,
   return run_search(ix, queries, nq, params, OUT_FULL, capacity, ids, dists, stats, stream);
 }
 
+int givf_probe_scores(givf_index_t ix, const float* queries, int64_t nq, float* scores,
+                      float* eps_scale_out, void* stream) {
+  if (!ix || !queries || !scores) return fail(GIVF_EINVAL, "null argument");
+  if (nq == 0) return GIVF_OK;
+  std::lock_guard<std::mutex> lock(ix->mu);
+  CUDA_TRY(cudaSetDevice(ix->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const IndexView& v = ix->v;
+  const int K = v.K, d = v.d;
+  const bool q_dev = is_device_ptr(queries), o_dev = is_device_ptr(scores);
+  const size_t bytes = (size_t)nq * (d * 4 + (size_t)K * 4 + tc_kpad(d) * 2 + probe_tiles(K) * 4) +
+                       (1 << 20);
+  CUDA_TRY(ix->arena.reserve(bytes));
+  Arena& ar = ix->arena;
+  ar.reset();
+  const float* dQ = queries;
+  if (!q_dev) {
+    float* t = ar.take<float>((size_t)nq * d);
+    CUDA_TRY(cudaMemcpyAsync(t, queries, sizeof(float) * nq * d, cudaMemcpyHostToDevice, st));
+    dQ = t;
+  }
+  float* D = o_dev ? scores : ar.take<float>((size_t)nq * K);
+  float* tmin = ar.take<float>((size_t)nq * probe_tiles(K));
+  const bool tc = use_tensor_cores(v);
+  if (tc) {
+    void* abf = ar.take<uint16_t>((size_t)nq * tc_kpad(d));
+    launch_split_bf16(dQ, (int)nq, d, 0, abf, st);
+    launch_probe_gemm_tc(abf, v.csplit, v.c2f, (int)nq, K, d, D, K, tmin, st);
+    g_launches += 2;
+  } else {
+    launch_probe_gemm(dQ, v.centroids, v.c2f, (int)nq, K, d, D, K, tmin, st);
+    g_launches += 1;
+  }
+  KCHECK();
+  if (!o_dev)
+    CUDA_TRY(cudaMemcpyAsync(scores, D, sizeof(float) * nq * K, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (eps_scale_out) *eps_scale_out = tc ? kEpsScaleTC : probe_eps_scale(d);
+  return GIVF_OK;
+}
+
 int givf_probe(givf_index_t ix, const float* queries, int64_t nq, int32_t nprobe,
                int32_t* regions, double* qc2, void* stream) {
   if (!ix) return fail(GIVF_EINVAL, "null argument");

@@ -194,6 +194,21 @@ def probe(index, queries, nprobe: int, device: int = 0):
     return regions, qc2
 
 
+def probe_scores(index, queries, device: int = 0):
+    """Approximate region scores |c|^2 - 2 q.c from the probe GEMM (tensor
+    cores unless GIVF_PROBE=simt) and their error-bound scale."""
+    dev = device_index(index, device)
+    q = np.ascontiguousarray(np.asarray(queries, dtype=np.float32))
+    if q.ndim == 1:
+        q = q[None, :]
+    _check_query_dim(dev, q)
+    out = np.empty((q.shape[0], dev.k), np.float32)
+    eps = ctypes.c_float(0.0)
+    _native.check(_native.load().givf_probe_scores(dev.handle, _vp(q), q.shape[0], _vp(out),
+                                                  ctypes.byref(eps), None))
+    return out, float(eps.value)
+
+
 def decomposed_distance(query, centroid, neighbor, alpha, code, tables, const_term):
     """Scalar float64 evaluation of the expanded distance form for one point
     (search.py:166-183); `tables` is an inner-product lookup table object with

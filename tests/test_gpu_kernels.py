@@ -1,0 +1,165 @@
+"""GPU checks of individual kernels and of the certified fast paths:
+tensor-core probe accuracy vs its a-priori bound, SIMT/tensor-core
+equivalence, forced fallbacks, and parity on a GPU-built index."""
+
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import golden_io
+from parity import assert_topk_equal
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _arrays(centroids, seed=0, m=8):
+    from paper_1802_02422_b200.device_index import IndexArrays
+
+    k, d = centroids.shape
+    rng = np.random.default_rng(seed)
+    return IndexArrays(
+        centroids=np.ascontiguousarray(centroids, np.float32), alphas=np.zeros(k, np.float32),
+        neighbor_ids=None, norm_terms=None, group_sizes=np.zeros((k, 1), np.int32),
+        region_offsets=np.zeros(k + 1, np.int64), point_ids=np.zeros(0, np.int32),
+        codes=np.zeros((0, m), np.uint8), const_bytes=np.zeros(0, np.uint8),
+        codewords=rng.standard_normal((m, 256, d // m)).astype(np.float32), rotation=None,
+        const_lo=0.0, const_hi=1.0, grouping=False)
+
+
+@pytest.mark.parametrize("scale", [1.0, 37.0])
+def test_probe_scores_within_bound(scale):
+    from paper_1802_02422_b200.query import probe_scores
+
+    rng = np.random.default_rng(1)
+    c = (rng.standard_normal((5000, 96)) * scale).astype(np.float32)
+    q = (rng.standard_normal((300, 96)) * scale).astype(np.float32)
+    s, eps_scale = probe_scores(_arrays(c), q)
+    c64, q64 = c.astype(np.float64), q.astype(np.float64)
+    exact = (c64 * c64).sum(1)[None, :] - 2.0 * q64 @ c64.T
+    cmax = np.sqrt((c64 * c64).sum(1).max())
+    bound = eps_scale * (cmax**2 + 2.0 * np.linalg.norm(q64, axis=1) * cmax)
+    ratio = np.abs(s - exact) / bound[:, None]
+    print(f"max |err| / bound = {ratio.max():.3e}")
+    assert ratio.max() < 0.25  # the bound holds with a 4x margin
+
+
+def test_simt_and_tensor_core_paths_agree():
+    code = (
+        "import sys, json, numpy as np; sys.path.insert(0, %r); sys.path.insert(0, %r);"
+        "import golden_io; from paper_1802_02422_b200 import SearchParams, search_batch;"
+        "fx = golden_io.load('c1like_m16');"
+        "i, d, s = search_batch(fx.index, fx.queries, SearchParams(nprobe=32, tau=0.5, candidates=3000), k=50);"
+        "print(json.dumps([i.tolist(), d.tolist(), s.tolist()]))" % (ROOT, os.path.join(ROOT, "tests")))
+    outs = []
+    for mode in ("simt", "tc"):
+        env = dict(os.environ, GIVF_PROBE=mode)
+        out = subprocess.check_output([sys.executable, "-c", code], env=env, cwd=ROOT)
+        outs.append(json.loads(out.decode().strip().splitlines()[-1]))
+    assert outs[0][0] == outs[1][0]
+    assert outs[0][2] == outs[1][2]
+    np.testing.assert_array_equal(np.array(outs[0][1]), np.array(outs[1][1]))
+
+
+def test_near_duplicate_centroids_take_the_fallback_and_stay_exact():
+    """Pairs of centroids 1e-7 apart make the fp32 scores unable to certify
+    the probe boundary or the pruning cut; the exhaustive / exact paths must
+    take over and the results must still equal the oracle."""
+    from types import SimpleNamespace
+
+    from oracle import search_oracle as so
+    from paper_1802_02422_b200 import SearchParams, search_batch
+    from paper_1802_02422_b200.device_index import DeviceIndex
+
+    fx = golden_io.load("c1like_m8")
+    ix = SimpleNamespace(**vars(fx.index))
+    c = ix.centroids.copy()
+    c[1::2] = c[0::2] + np.float32(1e-7)
+    ix.centroids = c
+    dev = DeviceIndex(ix)
+    for p in (SearchParams(nprobe=31, tau=0.5, candidates=4000),
+              SearchParams(nprobe=16, tau=0.7, candidates=1500)):
+        ids, d, st = search_batch(dev, fx.queries, p, k=60)
+        wi, wd, ws = so.search_topk(ix, fx.queries, so.Params(**vars(p)), 60)
+        np.testing.assert_array_equal(st, ws)
+        for i in range(len(fx.queries)):
+            assert_topk_equal(ids[i], d[i], wi[i], wd[i])
+    print("fallbacks", dev.fallback_counts())
+
+
+def _sphere_index(seed=0, k=4096, d=96, g=8, m=16, on_sphere=1024):
+    """Regions whose centroids are all (numerically) equidistant from the
+    query origin, with alpha = 0 and zero norm terms: no fp32 score can
+    separate them, so both certified fast paths must hand over."""
+    from paper_1802_02422_b200.device_index import IndexArrays
+
+    rng = np.random.default_rng(seed)
+    u = rng.standard_normal((k, d))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    c = np.where(np.arange(k)[:, None] < on_sphere, 0.5 * u, 3.0 * u).astype(np.float32)
+    sizes = rng.integers(0, 5, (k, g)).astype(np.int32)
+    offs = np.zeros(k + 1, np.int64)
+    np.cumsum(sizes.sum(1), out=offs[1:])
+    n = int(offs[-1])
+    return IndexArrays(
+        centroids=c, alphas=np.zeros(k, np.float32),
+        neighbor_ids=rng.integers(0, k, (k, g)).astype(np.int32),
+        norm_terms=np.zeros((k, g), np.float32), group_sizes=sizes, region_offsets=offs,
+        point_ids=rng.permutation(n).astype(np.int32),
+        codes=rng.integers(0, 256, (n, m)).astype(np.uint8),
+        const_bytes=rng.integers(0, 256, n).astype(np.uint8),
+        codewords=(0.1 * rng.standard_normal((m, 256, d // m))).astype(np.float32),
+        rotation=None, const_lo=-0.5, const_hi=0.5, grouping=True)
+
+
+def test_equidistant_regions_force_both_fallbacks():
+    from oracle import search_oracle as so
+    from paper_1802_02422_b200 import SearchParams, search_batch
+    from paper_1802_02422_b200.device_index import DeviceIndex
+
+    arr = _sphere_index()
+    rng = np.random.default_rng(9)
+    q = (1e-3 * rng.standard_normal((6, arr.dim))).astype(np.float32)
+    dev = DeviceIndex(arr)
+    p = SearchParams(nprobe=100, tau=0.5, candidates=600)
+    ids, d, st = search_batch(dev, q, p, k=50)
+    wi, wd, ws = so.search_topk(arr, q, so.Params(**vars(p)), 50)
+    np.testing.assert_array_equal(st, ws)
+    for i in range(q.shape[0]):
+        assert_topk_equal(ids[i], d[i], wi[i], wd[i])
+    counts = dev.fallback_counts()
+    print("fallbacks", counts)
+    assert counts["probe"] > 0 and counts["plan"] > 0
+
+
+@pytest.fixture(scope="module")
+def built_index():
+    import torch
+
+    from paper_1802_02422_b200.builder import BuildSpec, SynthSpec, build_synthetic
+
+    torch.manual_seed(0)
+    data = SynthSpec(d=96, n_clusters=1500, sigma=0.3, noise="total", seed=3)
+    spec = BuildSpec(n=300_000, k=2048, l=32, m=16, n_learn=60_000, kmeans_iters=6, pq_iters=6, seed=3)
+    arr, q, gt = build_synthetic(data, spec, 120, device="cuda", log=lambda *_: None)
+    return arr, q, gt
+
+
+@pytest.mark.parametrize("nprobe,tau,cand", [(64, 0.5, 10_000), (128, 0.25, 3000), (16, 1.0, 100_000)])
+def test_parity_on_gpu_built_index(built_index, nprobe, tau, cand):
+    from oracle import search_oracle as so
+    from paper_1802_02422_b200 import SearchParams, search_batch
+
+    arr, q, gt = built_index
+    p = SearchParams(nprobe=nprobe, tau=tau, candidates=cand)
+    ids, d, st = search_batch(arr, q, p, k=100)
+    wi, wd, ws = so.search_topk(arr, q, so.Params(**vars(p)), 100)
+    np.testing.assert_array_equal(st, ws)
+    for i in range(q.shape[0]):
+        assert_topk_equal(ids[i], d[i], wi[i], wd[i])
+    r10 = so.recall_at_r(list(ids), gt, 10)
+    assert r10 == so.recall_at_r(list(wi), gt, 10)
