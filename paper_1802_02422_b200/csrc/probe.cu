@@ -232,14 +232,26 @@ k_probe_select(const float* __restrict__ D, int64_t ldD, int K, int Tmin, int ca
   __syncthreads();
   // 2. one pass over the row: collect keys <= up, track the smallest key above
   uint32_t ex = 0xffffffffu;
-  for (int i = tid; i < K; i += blockDim.x) {
-    uint32_t k = f32_key(row[i]);
+  auto take = [&](float v, int i) {
+    uint32_t k = f32_key(v);
     if (k <= up) {
       uint32_t p = atomicAdd(&s_cnt, 1u);
       if (p < SEL_COLLECT) ck[p] = ((uint64_t)k << 32) | (uint32_t)i;
     } else {
       ex = min(ex, k);
     }
+  };
+  if ((K & 3) == 0 && (reinterpret_cast<uintptr_t>(row) & 15) == 0) {
+    const float4* r4 = reinterpret_cast<const float4*>(row);
+    for (int i = tid; i < (K >> 2); i += blockDim.x) {  // 16-byte loads, 4 scores each
+      const float4 v = __ldg(r4 + i);
+      take(v.x, 4 * i);
+      take(v.y, 4 * i + 1);
+      take(v.z, 4 * i + 2);
+      take(v.w, 4 * i + 3);
+    }
+  } else {
+    for (int i = tid; i < K; i += blockDim.x) take(row[i], i);
   }
   ex = block_min(ex, red);  // also orders the collection before its use
   const uint32_t n = s_cnt;

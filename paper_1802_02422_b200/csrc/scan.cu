@@ -26,19 +26,54 @@ constexpr int SCAN_THREADS = 256;
 constexpr int CHUNK = 1024;
 constexpr int WIN = SCAN_THREADS;
 
+// A code row held in registers as 32-bit words (vector loads for M in
+// {4, 8, 16, 32}) so the scan loop can keep the next rows' loads in flight.
 template <int M>
-struct CodeSum {
-  // generic M: numpy pairwise order over an M-element row
-  static GIVF_DEV float run(const uint8_t* __restrict__ code, const float* lut) {
-    float e[M];
+struct CodeVec {
+  static constexpr int W = (M + 3) / 4;
+  uint32_t w[W];
+  GIVF_DEV uint32_t byte(int j) const { return (w[j >> 2] >> ((j & 3) * 8)) & 0xffu; }
+};
+
+template <int M>
+GIVF_DEV CodeVec<M> load_code(const uint8_t* __restrict__ codes, int64_t row) {
+  CodeVec<M> v;
+  if constexpr (M == 16) {
+    uint4 x = __ldg(reinterpret_cast<const uint4*>(codes + row * 16));
+    v.w[0] = x.x; v.w[1] = x.y; v.w[2] = x.z; v.w[3] = x.w;
+  } else if constexpr (M == 8) {
+    uint2 x = __ldg(reinterpret_cast<const uint2*>(codes + row * 8));
+    v.w[0] = x.x; v.w[1] = x.y;
+  } else if constexpr (M == 4) {
+    v.w[0] = __ldg(reinterpret_cast<const uint32_t*>(codes + row * 4));
+  } else if constexpr (M == 32) {
+    const uint4* p = reinterpret_cast<const uint4*>(codes + row * 32);
+    uint4 x = __ldg(p), y = __ldg(p + 1);
+    v.w[0] = x.x; v.w[1] = x.y; v.w[2] = x.z; v.w[3] = x.w;
+    v.w[4] = y.x; v.w[5] = y.y; v.w[6] = y.z; v.w[7] = y.w;
+  } else {
 #pragma unroll
-    for (int j = 0; j < M; ++j) e[j] = lut[j * 256 + code[j]];
-    if (M < 8) {
-      float r = e[0];
+    for (int i = 0; i < CodeVec<M>::W; ++i) v.w[i] = 0;
 #pragma unroll
-      for (int j = 1; j < M; ++j) r = __fadd_rn(r, e[j]);
-      return r;
-    }
+    for (int j = 0; j < M; ++j) v.w[j >> 2] |= (uint32_t)__ldg(codes + row * M + j) << ((j & 3) * 8);
+  }
+  return v;
+}
+
+// ip = sum of the M LUT entries in numpy's float32 reduction order: M < 8 a
+// left-to-right sum; otherwise 8 running lanes r_j += e_{j+8i}, then
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the tail in order.
+template <int M>
+GIVF_DEV float code_sum(const CodeVec<M>& code, const float* lut) {
+  float e[M];
+#pragma unroll
+  for (int j = 0; j < M; ++j) e[j] = lut[j * 256 + code.byte(j)];
+  if constexpr (M < 8) {
+    float r = e[0];
+#pragma unroll
+    for (int j = 1; j < M; ++j) r = __fadd_rn(r, e[j]);
+    return r;
+  } else {
     float r[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) r[j] = e[j];
@@ -53,42 +88,12 @@ struct CodeSum {
     for (int j = body; j < M; ++j) s = __fadd_rn(s, e[j]);
     return s;
   }
-};
-
-template <int M>
-GIVF_DEV float code_ip(const uint8_t* __restrict__ codes, int64_t row, const float* lut) {
-  if constexpr (M == 16) {
-    uint4 v = __ldg(reinterpret_cast<const uint4*>(codes + row * 16));
-    uint8_t c[16];
-    *reinterpret_cast<uint4*>(c) = v;
-    return CodeSum<16>::run(c, lut);
-  } else if constexpr (M == 8) {
-    uint2 v = __ldg(reinterpret_cast<const uint2*>(codes + row * 8));
-    uint8_t c[8];
-    *reinterpret_cast<uint2*>(c) = v;
-    return CodeSum<8>::run(c, lut);
-  } else if constexpr (M == 4) {
-    uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(codes + row * 4));
-    uint8_t c[4];
-    *reinterpret_cast<uint32_t*>(c) = v;
-    return CodeSum<4>::run(c, lut);
-  } else if constexpr (M == 32) {
-    const uint4* p = reinterpret_cast<const uint4*>(codes + row * 32);
-    uint8_t c[32];
-    *reinterpret_cast<uint4*>(c) = __ldg(p);
-    *reinterpret_cast<uint4*>(c + 16) = __ldg(p + 1);
-    return CodeSum<32>::run(c, lut);
-  } else {
-    uint8_t c[M];
-#pragma unroll
-    for (int j = 0; j < M; ++j) c[j] = __ldg(codes + row * M + j);
-    return CodeSum<M>::run(c, lut);
-  }
 }
 
 // Shared memory layout of k_scan (dynamic):
 //   lut f32[M*256] | ctab f64[256] | qrot f32[d] | wstart i64[WIN] | wbase f64[WIN]
-//   | woff i32[WIN] | wlen i32[WIN] | rowv i64[CHUNK] | segv u16[CHUNK] | buf u64[bufcap]
+//   | woff i32[WIN] | wlen i32[WIN] | rowv i64[CHUNK] | segv u16[CHUNK]
+//   | buf u64[bufcap] | rowbuf i64[bufcap]
 struct ScanSmem {
   float* lut;
   double* ctab;
@@ -100,9 +105,10 @@ struct ScanSmem {
   int64_t* rowv;
   uint16_t* segv;
   uint64_t* buf;
+  int64_t* rowbuf;
 };
 
-GIVF_DEV ScanSmem carve(unsigned char* p, int M, int d) {
+GIVF_DEV ScanSmem carve(unsigned char* p, int M, int d, int bufcap) {
   ScanSmem s;
   s.lut = reinterpret_cast<float*>(p);
   s.ctab = reinterpret_cast<double*>(s.lut + M * 256);
@@ -115,12 +121,13 @@ GIVF_DEV ScanSmem carve(unsigned char* p, int M, int d) {
   s.rowv = reinterpret_cast<int64_t*>(s.wlen + WIN);
   s.segv = reinterpret_cast<uint16_t*>(s.rowv + CHUNK);
   s.buf = reinterpret_cast<uint64_t*>(s.segv + CHUNK);
+  s.rowbuf = reinterpret_cast<int64_t*>(s.buf + bufcap);
   return s;
 }
 
 static size_t scan_smem_bytes(int M, int d, int bufcap) {
   return (size_t)M * 256 * 4 + 256 * 8 + (((size_t)d * 4 + 15) & ~(size_t)15) + WIN * 8 + WIN * 8 +
-         WIN * 4 + WIN * 4 + CHUNK * 8 + CHUNK * 2 + (size_t)bufcap * 8 + 64;
+         WIN * 4 + WIN * 4 + CHUNK * 8 + CHUNK * 2 + (size_t)bufcap * 16 + 64;
 }
 
 // LUT of one query (pq.py:147-169): optional rotation q' = R q, then
@@ -151,10 +158,10 @@ __device__ void build_lut(const IndexView& ix, const float* __restrict__ q, Scan
 }
 
 template <int M>
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan(ScanArgs a, int bufcap) {
+__global__ void __launch_bounds__(SCAN_THREADS, (M <= 16 ? 3 : 1)) k_scan(ScanArgs a, int bufcap) {
   extern __shared__ __align__(16) unsigned char dsm[];
   const IndexView& ix = a.ix;
-  ScanSmem s = carve(dsm, M, ix.d);
+  ScanSmem s = carve(dsm, M, ix.d, bufcap);
   __shared__ int32_t red32[40];
   __shared__ int s_count;
   __shared__ int s_nfit;
@@ -168,31 +175,67 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(ScanArgs a, int bufcap) {
   const int nseg = a.nwork[b];
   uint64_t* fk = a.mode == 1 ? a.full_keys + (int64_t)b * a.cap_full_p2 : nullptr;
   int64_t code_base = 0;
+  // shrink the candidate buffer as soon as it holds 2k keys (cheap radix
+  // select) so the threshold tightens early, and always before it can
+  // overflow during the next chunk
+  const int shrink_at = min(bufcap - CHUNK, max(2 * a.k, 128));
 
-  // Candidates are appended while their distance key is <= thr (the k-th
-  // smallest key seen so far, ties kept); ids are loaded only for them.
+  // top-k: candidates are appended while their distance key is <= thr (the
+  // k-th smallest key kept so far, ties included).  Only the key and the row
+  // are stored; ids are read for the final buffer (and for exact-tie
+  // decisions once thr64 is set).
   uint32_t thr = 0xffffffffu;
   uint64_t thr64 = kKeyPad;
-  auto process = [&](int64_t row, double base, int64_t pos) {
-    float ip = code_ip<M>(ix.codes, row, s.lut);
-    double c = s.ctab[__ldg(ix.cbytes + row)];
-    float dist = (float)dadd(dsub(base, 2.0 * (double)ip), c);
+  auto dist_of = [&](float ip, double base, uint8_t cb) -> float {
+    return (float)dadd(dsub(base, 2.0 * (double)ip), s.ctab[cb]);
+  };
+  auto consider = [&](int64_t row, float dist, int64_t pos) {
     if (a.mode == 1) {
       fk[pos] = dist_id_key(dist, __ldg(ix.pids + row));
-    } else {
-      uint32_t dk = f32_key(dist);
-      if (dk <= thr) {
-        uint64_t key = ((uint64_t)dk << 32) | (uint32_t)__ldg(ix.pids + row);
-        if (key < thr64) s.buf[atomicAdd(&s_count, 1)] = key;
+      return;
+    }
+    const uint32_t dk = f32_key(dist);
+    if (dk > thr) return;
+    if (dk == thr && thr64 != kKeyPad &&
+        (((uint64_t)dk << 32) | (uint32_t)__ldg(ix.pids + row)) >= thr64)
+      return;
+    const int slot = atomicAdd(&s_count, 1);
+    s.buf[slot] = (uint64_t)dk << 32;
+    s.rowbuf[slot] = row;
+  };
+  // Software-pipelined sweep over n codes: each thread owns codes v, v+T,
+  // ...; the loads of its next two codes are in flight while the current two
+  // are summed (4 code rows + 4 constant bytes outstanding per thread).
+  struct Slot {
+    int64_t row;
+    double base;
+    CodeVec<M> code;
+    uint8_t cb;
+    bool ok;
+  };
+  auto sweep = [&](int n, int64_t pos0, auto row_of, auto base_of) {
+    auto fetch = [&](Slot& sl, int vv) {
+      sl.ok = vv < n;
+      if (sl.ok) {
+        sl.row = row_of(vv);
+        sl.base = base_of(vv);
+        sl.code = load_code<M>(ix.codes, sl.row);
+        sl.cb = __ldg(ix.cbytes + sl.row);
       }
+    };
+    Slot cur;
+    fetch(cur, tid);
+    for (int v = tid; v < n; v += SCAN_THREADS) {
+      Slot nxt;
+      fetch(nxt, v + SCAN_THREADS);  // next row's loads overlap this row's sums
+      consider(cur.row, dist_of(code_sum<M>(cur.code, s.lut), cur.base, cur.cb), pos0 + v);
+      cur = nxt;
     }
   };
-  // Keep room for one more chunk of appends: radix-select the k-th smallest
-  // distance key of the buffer (4 x 8-bit digits) and compact to keys <= it.
   auto maybe_shrink = [&]() {
     __syncthreads();
     const int cnt = s_count;
-    if (a.mode != 0 || cnt <= bufcap - CHUNK) return;
+    if (a.mode != 0 || cnt <= shrink_at) return;
     uint32_t* hist = reinterpret_cast<uint32_t*>(s.rowv);  // free between chunks
     uint32_t prefix = 0, mask = 0, need = (uint32_t)a.k;
     for (int shift = 24; shift >= 0; shift -= 8) {
@@ -234,10 +277,11 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(ScanArgs a, int bufcap) {
     for (int t0 = 0; t0 < cnt; t0 += blockDim.x) {
       const int i = t0 + tid;
       uint64_t v = i < cnt ? s.buf[i] : kKeyPad;
+      int64_t rw = i < cnt ? s.rowbuf[i] : 0;
       int keep = (i < cnt && (uint32_t)(v >> 32) <= prefix) ? 1 : 0;
       int tot;
       int pos = block_exclusive_scan(keep, red32, &tot);
-      if (keep) s.buf[base + pos] = v;
+      if (keep) { s.buf[base + pos] = v; s.rowbuf[base + pos] = rw; }
       base += tot;
       __syncthreads();
     }
@@ -246,12 +290,22 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(ScanArgs a, int bufcap) {
     __syncthreads();
     if (base > bufcap - CHUNK) {  // > CHUNK exact distance ties: order them by id
       const uint32_t np2 = next_pow2((uint32_t)base);
-      for (uint32_t i = base + tid; i < np2; i += blockDim.x) s.buf[i] = kKeyPad;
+      for (uint32_t i = tid; i < np2; i += blockDim.x) {
+        uint64_t v = kKeyPad;
+        if (i < (uint32_t)base) {
+          v = s.buf[i];
+          if (s.rowbuf[i] >= 0) v |= (uint32_t)__ldg(ix.pids + s.rowbuf[i]);
+        }
+        s.buf[i] = v;
+      }
       __syncthreads();
+      // rows are no longer needed for these: keys now carry the ids
       bitonic_sort_keys(s.buf, np2);
       thr64 = s.buf[a.k - 1];
       thr = (uint32_t)(thr64 >> 32);
       if (tid == 0) s_count = a.k;
+      // mark the kept keys as resolved: rowbuf = -1
+      for (int i = tid; i < a.k; i += blockDim.x) s.rowbuf[i] = -1;
       __syncthreads();
     }
   };
@@ -278,8 +332,9 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(ScanArgs a, int bufcap) {
       const double bs = s.wbase[0];
       const int ln = s.wlen[0];
       for (int piece = 0; piece < ln; piece += CHUNK) {
-        int n = min(CHUNK, ln - piece);
-        for (int v = tid; v < n; v += blockDim.x) process(st + piece + v, bs, code_base + piece + v);
+        const int n = min(CHUNK, ln - piece);
+        sweep(n, code_base + piece, [&](int vv) { return st + piece + vv; },
+              [&](int) { return bs; });
         maybe_shrink();
       }
       code_base += ln;
@@ -296,8 +351,8 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(ScanArgs a, int bufcap) {
       }
     }
     __syncthreads();
-    for (int v = tid; v < chunk_total; v += blockDim.x)
-      process(s.rowv[v], s.wbase[s.segv[v]], code_base + v);
+    sweep(chunk_total, code_base, [&](int vv) { return s.rowv[vv]; },
+          [&](int vv) { return s.wbase[s.segv[vv]]; });
     maybe_shrink();
     code_base += chunk_total;
     seg0 += nfit;
@@ -307,7 +362,15 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(ScanArgs a, int bufcap) {
     __syncthreads();
     const int cnt = s_count;
     uint32_t np2 = next_pow2((uint32_t)max(cnt, 1));
-    for (uint32_t i = cnt + tid; i < np2; i += blockDim.x) s.buf[i] = kKeyPad;
+    for (uint32_t i = tid; i < np2; i += blockDim.x) {
+      uint64_t v = kKeyPad;
+      if ((int)i < cnt) {
+        v = s.buf[i];
+        const int64_t rw = s.rowbuf[i];
+        if (rw >= 0) v |= (uint32_t)__ldg(ix.pids + rw);  // resolve the id
+      }
+      s.buf[i] = v;
+    }
     __syncthreads();
     bitonic_sort_keys(s.buf, np2);
     for (int i = tid; i < a.k; i += blockDim.x) {
