@@ -33,7 +33,8 @@ namespace givf {
 namespace tc {
 
 constexpr int BM = 128, BN = 256, BK = 64;  // BK bf16 = 128 B = one swizzle row
-constexpr int STAGES = 4;
+constexpr int STAGES = 3;
+constexpr uint32_t STAGE_OUT = 4 * 2 * 4096;  // epilogue TMA-store staging, 4 warps x 2
 constexpr int THREADS = 192;
 constexpr uint32_t A_CHUNK = BM * BK * 2;   // 16 KB
 constexpr uint32_t B_CHUNK = BN * BK * 2;   // 32 KB
@@ -133,6 +134,7 @@ struct Smem {
 // smem: [A resident: KC x 16 KB][B ring: STAGES x 32 KB][barriers]
 __global__ void __launch_bounds__(tc::THREADS, 1)
 k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                const __grid_constant__ CUtensorMap mapD, int use_tma_store,
                 const float* __restrict__ c2, int nq, int K, int KC, int nsplit,
                 float* __restrict__ D, int64_t ldD, float* __restrict__ tmin) {
   using namespace tc;
@@ -141,7 +143,7 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
       (reinterpret_cast<uintptr_t>(dsm) + 1023) & ~(uintptr_t)1023);
   unsigned char* smA = base;
   unsigned char* smB = base + (size_t)KC * A_CHUNK;
-  Smem* sm = reinterpret_cast<Smem*>(smB + (size_t)STAGES * B_CHUNK);
+  Smem* sm = reinterpret_cast<Smem*>(smB + (size_t)STAGES * B_CHUNK + STAGE_OUT);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m_blocks = (nq + BM - 1) / BM;
@@ -234,6 +236,10 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
     // ------------------------------------------------ epilogue (warps 2..5)
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int ntiles128 = (K + 127) / 128;
+    // per-warp double-buffered 32x32 fp32 staging tiles for the TMA store
+    // (SWIZZLE_128B: the 16-byte chunk k of row r sits at chunk k ^ (r & 7))
+    unsigned char* stage_base = smB + (size_t)STAGES * B_CHUNK + (size_t)(warp - 2) * 2 * 4096;
+    uint32_t sbuf = 0;
     uint32_t acc = 0, acc_phase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int mb = u / nsplit, sp = u % nsplit;
@@ -250,14 +256,48 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
           tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN + c * 32, r);
           const int col0 = t * BN + c * 32;
           float v[32];
+          if (col0 + 32 <= K) {
+            const float4* c24 = reinterpret_cast<const float4*>(c2 + col0);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int col = col0 + i;
-            v[i] = col < K ? fmaf(-2.f, __uint_as_float(r[i]), __ldg(c2 + col))
-                           : __int_as_float(0x7f800000);
-            mn = fminf(mn, v[i]);
+            for (int i = 0; i < 8; ++i) {
+              const float4 cc = __ldg(c24 + i);  // warp-uniform: one broadcast per load
+              v[4 * i] = fmaf(-2.f, __uint_as_float(r[4 * i]), cc.x);
+              v[4 * i + 1] = fmaf(-2.f, __uint_as_float(r[4 * i + 1]), cc.y);
+              v[4 * i + 2] = fmaf(-2.f, __uint_as_float(r[4 * i + 2]), cc.z);
+              v[4 * i + 3] = fmaf(-2.f, __uint_as_float(r[4 * i + 3]), cc.w);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const int col = col0 + i;
+              v[i] = col < K ? fmaf(-2.f, __uint_as_float(r[i]), __ldg(c2 + col))
+                             : __int_as_float(0x7f800000);
+            }
           }
-          if (q < nq) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) mn = fminf(mn, v[i]);
+          if (use_tma_store) {
+            // wait until the store issued from this buffer two chunks ago has
+            // finished reading shared memory, then stage and issue
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            __syncwarp();
+            unsigned char* sb = stage_base + sbuf * 4096;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              *reinterpret_cast<float4*>(sb + lane * 128 + ((k ^ (lane & 7)) * 16)) =
+                  make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                      reinterpret_cast<uint64_t>(&mapD)),
+                  "r"(col0), "r"(mb * BM + quarter * 32), "r"(smem_u32(sb))
+                  : "memory");
+              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            sbuf ^= 1;
+          } else if (q < nq) {
             if (col0 + 32 <= K) {
               float4* dst = reinterpret_cast<float4*>(drow + col0);
 #pragma unroll
@@ -281,6 +321,7 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
+    if (use_tma_store && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   fence_before();
   __syncthreads();
@@ -342,6 +383,21 @@ bool make_map(CUtensorMap* m, const void* ptr, int64_t rows, int Kp, int box_row
   return r == CUDA_SUCCESS;
 }
 
+// fp32 score matrix (rows x cols, pitch ld floats) written in 32 x 32 boxes
+// from SWIZZLE_128B staging tiles.
+bool make_map_f32_out(CUtensorMap* m, void* ptr, int64_t rows, int cols, int64_t ld) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ptr, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -368,14 +424,19 @@ void launch_split_bf16(const float* x, int rows, int d, int centroid, void* out,
 
 size_t tc_smem_bytes(int d) {
   const int KC = tc_kpad(d) / tc::BK;
-  return 1024 + (size_t)KC * tc::A_CHUNK + (size_t)tc::STAGES * tc::B_CHUNK + sizeof(tc::Smem) + 64;
+  return 1024 + (size_t)KC * tc::A_CHUNK + (size_t)tc::STAGES * tc::B_CHUNK + tc::STAGE_OUT +
+         sizeof(tc::Smem) + 64;
 }
 
 bool launch_probe_gemm_tc(const void* Abf, const void* Bbf, const float* c2, int nq, int K, int d,
                           float* D, int64_t ldD, float* tmin, cudaStream_t s) {
   const int Kp = tc_kpad(d);
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, md;
   if (!make_map(&ma, Abf, nq, Kp, tc::BM) || !make_map(&mb, Bbf, K, Kp, tc::BN)) return false;
+  // s~ rows go out through TMA stores when the row pitch allows it
+  int use_tma_store = (ldD % 4 == 0) ? 1 : 0;
+  if (use_tma_store && !make_map_f32_out(&md, D, nq, K, ldD)) use_tma_store = 0;
+  if (!use_tma_store) md = ma;  // unused
   const int KC = Kp / tc::BK;
   const int m_blocks = (nq + tc::BM - 1) / tc::BM;
   const int n_tiles = (K + tc::BN - 1) / tc::BN;
@@ -389,7 +450,8 @@ bool launch_probe_gemm_tc(const void* Abf, const void* Bbf, const float* c2, int
     cudaFuncSetAttribute(k_probe_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = smem;
   }
-  k_probe_gemm_tc<<<grid, tc::THREADS, smem, s>>>(ma, mb, c2, nq, K, KC, nsplit, D, ldD, tmin);
+  k_probe_gemm_tc<<<grid, tc::THREADS, smem, s>>>(ma, mb, md, use_tma_store, c2, nq, K, KC, nsplit,
+                                                  D, ldD, tmin);
   return true;
 }
 
