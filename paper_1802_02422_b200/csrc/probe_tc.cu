@@ -34,7 +34,8 @@ namespace tc {
 
 constexpr int BM = 128, BN = 256, BK = 64;  // BK bf16 = 128 B = one swizzle row
 constexpr int STAGES = 3;
-constexpr uint32_t STAGE_OUT = 4 * 2 * 4096;  // epilogue TMA-store staging, 4 warps x 2
+// epilogue smem: TMA-store staging (4 warps x 2 x 4 KB) + per-warp |c|^2 tile
+constexpr uint32_t STAGE_OUT = 4 * 2 * 4096 + 4 * 256 * 4;
 constexpr int THREADS = 192;
 constexpr uint32_t A_CHUNK = BM * BK * 2;   // 16 KB
 constexpr uint32_t B_CHUNK = BN * BK * 2;   // 32 KB
@@ -239,6 +240,8 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
     // per-warp double-buffered 32x32 fp32 staging tiles for the TMA store
     // (SWIZZLE_128B: the 16-byte chunk k of row r sits at chunk k ^ (r & 7))
     unsigned char* stage_base = smB + (size_t)STAGES * B_CHUNK + (size_t)(warp - 2) * 2 * 4096;
+    float* c2s = reinterpret_cast<float*>(smB + (size_t)STAGES * B_CHUNK + 4 * 2 * 4096) +
+                 (warp - 2) * BN;
     uint32_t sbuf = 0;
     uint32_t acc = 0, acc_phase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -246,8 +249,19 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
       const int t0 = sp * per_split, t1 = min(n_tiles, t0 + per_split);
       const int q = mb * BM + quarter * 32 + lane;
       for (int t = t0; t < t1; ++t) {
+        // this tile's |c|^2 column terms: issued before the accumulator wait
+        // so their latency hides behind it, then kept in a per-warp smem copy
+        float c2r[BN / 32];
+#pragma unroll
+        for (int c = 0; c < BN / 32; ++c) {
+          const int col = t * BN + c * 32 + lane;
+          c2r[c] = col < K ? __ldg(c2 + col) : 0.f;
+        }
         mbar_wait(&sm->tm_full[acc], acc_phase);
         fence_after();
+#pragma unroll
+        for (int c = 0; c < BN / 32; ++c) c2s[c * 32 + lane] = c2r[c];
+        __syncwarp();
         float* drow = D + (int64_t)q * ldD;
         float mn = __int_as_float(0x7f800000);
 #pragma unroll 1
@@ -257,10 +271,10 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
           const int col0 = t * BN + c * 32;
           float v[32];
           if (col0 + 32 <= K) {
-            const float4* c24 = reinterpret_cast<const float4*>(c2 + col0);
+            const float4* c24 = reinterpret_cast<const float4*>(c2s + c * 32);
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-              const float4 cc = __ldg(c24 + i);  // warp-uniform: one broadcast per load
+              const float4 cc = c24[i];  // smem broadcast
               v[4 * i] = fmaf(-2.f, __uint_as_float(r[4 * i]), cc.x);
               v[4 * i + 1] = fmaf(-2.f, __uint_as_float(r[4 * i + 1]), cc.y);
               v[4 * i + 2] = fmaf(-2.f, __uint_as_float(r[4 * i + 2]), cc.z);
