@@ -137,6 +137,28 @@ struct givf_index {
   int64_t dev_bytes = 0;
   Arena arena;
   std::mutex mu;
+  // internal pipeline streams (chunks of one call run on them round-robin)
+  std::vector<cudaStream_t> pstreams;
+  std::vector<cudaEvent_t> ev_done;
+  cudaEvent_t ev_start = nullptr;
+
+  cudaError_t ensure_streams(int n) {
+    if (!ev_start) {
+      cudaError_t e = cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+    }
+    while ((int)pstreams.size() < n) {
+      cudaStream_t s;
+      cudaEvent_t ev;
+      cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+      if (e != cudaSuccess) return e;
+      e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+      pstreams.push_back(s);
+      ev_done.push_back(ev);
+    }
+    return cudaSuccess;
+  }
 };
 
 namespace {
@@ -207,9 +229,14 @@ size_t l2_budget() {
   return (size_t)(s ? atoll(s) : (1ll << 20)) << 20;
 }
 
+int nstreams_default() {
+  const char* s = getenv("GIVF_STREAMS");
+  return std::max(1, std::min(8, s ? atoi(s) : 2));
+}
+
 size_t workspace_budget() {
   const char* s = getenv("GIVF_WORKSPACE_MB");
-  size_t mb = s ? (size_t)atoll(s) : 3072;
+  size_t mb = s ? (size_t)atoll(s) : 4096;
   return std::max<size_t>(mb, 64) << 20;
 }
 
@@ -392,14 +419,30 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
   const size_t hot = (pl.ps.exhaustive ? 0 : (size_t)pl.K * 4) + (size_t)pl.total * 20 +
                      (size_t)pl.cap_w * 32;
   chunk = std::min<int64_t>(chunk, std::max<int64_t>(128, (int64_t)(l2_budget() / hot)));
+  // Chunks run round-robin on `ns` internal streams with disjoint arena
+  // slices, so one chunk's latency-bound kernels overlap another's and the
+  // kernel tails fill in; the caller's stream is fenced on both ends.
+  int ns = nstreams_default();
+  chunk = std::max<int64_t>(1, chunk / ns);
   if (const char* e = getenv("GIVF_CHUNK_QUERIES")) chunk = std::max<int64_t>(1, atoll(e));
   chunk = std::max<int64_t>(1, std::min<int64_t>(chunk, nq));
   chunk = std::min<int64_t>(chunk, 65535);
-  CUDA_TRY(ix->arena.reserve(fixed + per_q * (size_t)chunk + (1 << 20)));
+  const int64_t nchunks = (nq + chunk - 1) / chunk;
+  ns = (int)std::min<int64_t>(ns, nchunks);
+  const size_t slice = ((fixed + per_q * (size_t)chunk + (1 << 20)) + 4095) & ~(size_t)4095;
+  CUDA_TRY(ix->arena.reserve(slice * ns));
+  CUDA_TRY(ix->ensure_streams(ns));
+  CUDA_TRY(cudaEventRecord(ix->ev_start, st));
+  for (int i = 0; i < ns; ++i) CUDA_TRY(cudaStreamWaitEvent(ix->pstreams[i], ix->ev_start, 0));
+  const cudaStream_t caller = st;
 
-  for (int64_t q0 = 0; q0 < nq; q0 += chunk) {
+  for (int64_t q0 = 0, ci = 0; q0 < nq; q0 += chunk, ++ci) {
     const int bq = (int)std::min<int64_t>(chunk, nq - q0);
-    Arena& ar = ix->arena;
+    const int si = (int)(ci % ns);
+    st = ix->pstreams[si];
+    Arena ar;
+    ar.base = static_cast<char*>(ix->arena.base) + slice * si;
+    ar.cap = slice;
     ar.reset();
     const float* dQ;
     if (q_dev) {
@@ -500,10 +543,14 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
       CUDA_TRY(cudaMemcpyAsync(stats + q0, dstats, sizeof(int64_t) * 4 * bq,
                                cudaMemcpyDeviceToHost, st));
     }
-    // the next chunk reuses the arena: its copies and kernels are ordered
-    // after this chunk's on the same stream, so no host synchronisation
+    // chunk ci + ns reuses this arena slice on the same stream: ordered after
+    // this chunk's copies and kernels, so no host synchronisation
   }
-  if (!out_dev || !st_dev || !q_dev) CUDA_TRY(cudaStreamSynchronize(st));
+  for (int i = 0; i < ns; ++i) {
+    CUDA_TRY(cudaEventRecord(ix->ev_done[i], ix->pstreams[i]));
+    CUDA_TRY(cudaStreamWaitEvent(caller, ix->ev_done[i], 0));
+  }
+  if (!out_dev || !st_dev || !q_dev) CUDA_TRY(cudaStreamSynchronize(caller));
   return GIVF_OK;
 }
 
@@ -672,6 +719,12 @@ int givf_index_destroy(givf_index_t ix) {
   for (void* p : ix->allocs) cudaFree(p);
   if (ix->arena.base) cudaFree(ix->arena.base);
   if (ix->stream) cudaStreamDestroy(ix->stream);
+  for (auto s : ix->pstreams) {
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+  }
+  for (auto e : ix->ev_done) cudaEventDestroy(e);
+  if (ix->ev_start) cudaEventDestroy(ix->ev_start);
   delete ix;
   return GIVF_OK;
 }

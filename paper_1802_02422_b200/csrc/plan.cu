@@ -27,6 +27,7 @@ namespace givf {
 constexpr int PLAN_THREADS = 256;
 constexpr int PLAN_BUCKETS = 1024;
 constexpr int SORTCAP = 1024;
+constexpr int SORT_SMALL = 128;  // boundary buckets up to this size are sorted directly
 constexpr int PLAN_SREG = 2048;  // probed regions staged in shared memory
 
 GIVF_DEV double key_to_f64(uint64_t k) {
@@ -278,7 +279,9 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan_select(PlanArgs a) {
     taken_c += s_bc_before;
     taken_w += s_bw_before;
     __syncthreads();
-    if (cnt_b <= (uint32_t)SORTCAP) {
+    // another histogram pass over all items is far cheaper than a large
+    // bitonic sort: refine until the boundary bucket is small
+    if (cnt_b <= (uint32_t)SORT_SMALL || (shift == 0 && cnt_b <= (uint32_t)SORTCAP)) {
       bucket_lo = bl;
       bucket_hi = bh;
       break;
@@ -486,25 +489,30 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan_approx(PlanArgs a) {
             1e-12 * ((double)a.cmax + qn) * ((double)a.cmax + qn)
       : 0.0;
 
-  // ---- 1. approximate scores
+  // ---- 1. approximate scores: one warp per probed region, lanes over its
+  // groups (region terms loaded once, neighbor/norm/size rows coalesced)
   unsigned long long kmin = ~0ull, kmax = 0ull;
-  for (int64_t f = tid; f < total; f += blockDim.x) {
-    const int p = (int)(f / G), j = (int)(f % G);
-    const int r = reg[p];
-    double score;
-    if (ix.grouping) {
-      const int64_t gi = (int64_t)r * G + j;
-      const double qs2 = dadd((double)__ldg(Drow + ix.nbr[gi]), q2);
-      const double al = (double)ix.alphas[r];
-      score = dadd(dadd(dmul(dsub(1.0, al), qc2[p]), dmul(al, qs2)), (double)ix.norm[gi]);
-    } else {
-      score = qc2[p];
+  {
+    const int warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
+    for (int p = warp; p < P; p += nwarps) {
+      const int r = reg[p];
+      const double qc = qc2[p];
+      const double al = ix.grouping ? (double)ix.alphas[r] : 0.0;
+      const double oma_qc = dmul(dsub(1.0, al), qc);
+      for (int j = lane; j < G; j += 32) {
+        const int64_t gi = (int64_t)r * G + j, f = (int64_t)p * G + j;
+        double score = qc;
+        if (ix.grouping) {
+          const double qs2 = dadd((double)__ldg(Drow + ix.nbr[gi]), q2);
+          score = dadd(dadd(oma_qc, dmul(al, qs2)), (double)ix.norm[gi]);
+        }
+        sscore[f] = score;
+        ssize[f] = ix.gsize[gi];
+        unsigned long long k = f64_key(score);
+        kmin = min(kmin, k);
+        kmax = max(kmax, k);
+      }
     }
-    sscore[f] = score;
-    ssize[f] = ix.gsize[(int64_t)r * G + j];
-    unsigned long long k = f64_key(score);
-    kmin = min(kmin, k);
-    kmax = max(kmax, k);
   }
   __syncthreads();
   kmin = block_min(kmin, red64);
@@ -568,7 +576,9 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan_approx(PlanArgs a) {
     taken_c += s_bc_before;
     taken_w += s_bw_before;
     __syncthreads();
-    if (cnt_b <= (uint32_t)SORTCAP) {
+    // another histogram pass over all items is far cheaper than a large
+    // bitonic sort: refine until the boundary bucket is small
+    if (cnt_b <= (uint32_t)SORT_SMALL || (shift == 0 && cnt_b <= (uint32_t)SORTCAP)) {
       bucket_lo = bl;
       bucket_hi = bh;
       break;
