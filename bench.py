@@ -157,7 +157,9 @@ class ClockSampler:
 def _cpu_worker(args):
     """Oracle port of the reference path on one core over a query slice."""
     arr_path, qi, params, deadline = args
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    from threadpoolctl import threadpool_limits
+
+    threadpool_limits(1)  # one BLAS thread per forked worker (no oversubscription)
     from oracle import search_oracle as so
 
     arr = _CPU_STATE["arr"]
@@ -285,6 +287,9 @@ def run_ours(args, w):
     recall = {r: recall_at_r(list(ids_h), gt, r) for r in (1, 10, 100)}
 
     # ---- per-stage kernel time (separate pass, events on the launching stream)
+    # one internal stream here, so each kernel's event-timed duration is its own
+    saved_streams = os.environ.get("GIVF_STREAMS")
+    os.environ["GIVF_STREAMS"] = "1"
     _native.profile_enable(True)
     _native.profile_read()
     prof_steps = max(1, min(3, args.steps))
@@ -294,6 +299,10 @@ def run_ours(args, w):
     torch.cuda.synchronize()
     stages = _native.profile_read()
     _native.profile_enable(False)
+    if saved_streams is None:
+        os.environ.pop("GIVF_STREAMS", None)
+    else:
+        os.environ["GIVF_STREAMS"] = saved_streams
 
     # ---- end to end through the public API with host buffers (pinned)
     from paper_1802_02422_b200.query import search_batch
@@ -321,9 +330,12 @@ def run_ours(args, w):
         return None
     m = w["m"]
     scanned_local = float(stats_h[:, 3].sum()) / world  # ~ rows this rank scans
+    # algorithmic bytes: codes_scanned x (M + 1) per query (M code bytes + the
+    # constant byte), summed over the step, over the scan kernels' summed time
     scan_ms, scan_n = stages["scan"]
+    scan_ms_step = scan_ms / prof_steps
     scan_bytes = scanned_local * (m + 1)
-    scan_gbs = scan_bytes / (scan_ms / max(scan_n, 1) / 1e3) / 1e9 if scan_n else None
+    scan_gbs = scan_bytes / (scan_ms_step / 1e3) / 1e9 if scan_n else None
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -371,13 +383,15 @@ def run_ours(args, w):
             "unit": "GB/s",
             "frac": (scan_gbs / hbm_peak) if scan_gbs else None,
             "traffic": traffic,
-            "algorithmic_bytes_per_launch": scan_bytes,
-            "avg_launch_ms": scan_ms / max(scan_n, 1),
+            "algorithmic_bytes_per_step": scan_bytes,
+            "launches_per_step": scan_n / prof_steps,
+            "kernel_ms_per_step": scan_ms_step,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
         },
         "roofline_probe": {
-            "kernel": "probe_gemm (K1a, SIMT fp32 in this build)",
-            "achieved_tflops": (probe_flops / (gemm_ms / max(gemm_n, 1) / 1e3) / 1e12) if gemm_n else None,
+            "kernel": "probe_gemm (K1a: bf16x3 tcgen05 GEMM + split kernel); 2*K*d flops per query",
+            "achieved_tflops": (probe_flops / (gemm_ms / prof_steps / 1e3) / 1e12) if gemm_n else None,
+            "tensor_flops_per_step_bf16x3": probe_flops * 3 * (288 + 32) / 288,
             "unit": "TFLOP/s",
         },
         "stage_ms_per_step": step_stage_ms,
