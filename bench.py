@@ -346,7 +346,10 @@ def run_ours(args, w):
     tr_path = os.path.join(ROOT, "profiles", f"ncu_scan_traffic_{args.workload}.json")
     if os.path.exists(tr_path):
         try:
-            traffic = json.load(open(tr_path)).get("dram_bytes_per_launch")
+            tr = json.load(open(tr_path))
+            # ncu DRAM bytes of one captured scan launch, scaled to this step's
+            # queries (same per-query work) so it compares with `achieved`
+            traffic = tr["dram_bytes_per_launch"] / tr["queries_per_launch"] * nq / world
         except Exception:  # noqa: BLE001
             traffic = None
     gemm_ms, gemm_n = stages["probe_gemm"]
