@@ -1,7 +1,7 @@
 # Builds the sm_100a search library (C ABI: include/givf_b200.h) in-tree.
 NVCC ?= nvcc
 ARCH ?= -gencode arch=compute_100a,code=sm_100a
-NVFLAGS = $(ARCH) -O3 -lineinfo -std=c++17 -Iinclude -Xcompiler -fPIC,-ffp-contract=off \
+NVFLAGS = $(ARCH) $(EXTRA) -O3 -lineinfo -std=c++17 -Iinclude -Xcompiler -fPIC,-ffp-contract=off \
           --expt-relaxed-constexpr -Xptxas --warn-on-spills
 SRC = $(wildcard paper_1802_02422_b200/csrc/*.cu)
 HDR = $(wildcard paper_1802_02422_b200/csrc/*.cuh paper_1802_02422_b200/csrc/*.h) include/givf_b200.h

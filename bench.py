@@ -259,6 +259,7 @@ def run_ours(args, w):
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     launches0 = _native.kernel_launches()
+    fb0 = sx.dev.fallback_counts()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -272,6 +273,8 @@ def run_ours(args, w):
     if world > 1:
         torch.distributed.barrier()
     launches = _native.kernel_launches() - launches0
+    fb1 = sx.dev.fallback_counts()
+    fallbacks = {k_: (fb1[k_] - fb0[k_]) / args.steps for k_ in fb0}
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = float(np.sum(step_ms))
     if world > 1:
@@ -399,6 +402,7 @@ def run_ours(args, w):
         },
         "stage_ms_per_step": step_stage_ms,
         "gpu_launches": int(launches),
+        "fallback_queries_per_step": fallbacks,
         "e2e": {"value": e2e_qps, "unit": "queries/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
         "clocks": clocks.summary(),

@@ -229,6 +229,11 @@ size_t l2_budget() {
   return (size_t)(s ? atoll(s) : (1ll << 20)) << 20;
 }
 
+bool use_async_scan() {
+  const char* s = getenv("GIVF_SCAN");
+  return s && strcmp(s, "async") == 0;  // measured slower on C2 so far: opt-in
+}
+
 int nstreams_default() {
   const char* s = getenv("GIVF_STREAMS");
   return std::max(1, std::min(8, s ? atoi(s) : 2));
@@ -489,6 +494,9 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
     pa.cmax = v.cmax;
     pa.eps_scale = eps_scale;
     pa.only = Dmat ? ar.take<int>(bq) : nullptr;
+    // the approximate planner's keys alias the exact scratch, which the exact
+    // kernels only write after the approximate planner has finished
+    pa.akey = reinterpret_cast<uint32_t*>(pa.sbase);
     int nk = 0;
     staged(ST_PLAN, st, [&] { nk = launch_plan(pa, st); }, 0);
     g_launches += nk;
@@ -519,7 +527,9 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
         sa.full_keys = ar.take<uint64_t>((size_t)bq * full_p2);
         sa.cap_full_p2 = full_p2;
       }
-      staged(ST_SCAN, st, [&] { launch_scan(sa, st); });
+      staged(ST_SCAN, st, [&] {
+        if (!(use_async_scan() && launch_scan_async(sa, st))) launch_scan(sa, st);
+      });
       KCHECK();
       if (om == OUT_FULL) {
         staged(ST_FINISH, st, [&] {
@@ -682,10 +692,10 @@ int givf_index_create(const givf_index_desc* ds, int device, givf_index_t* out) 
 #undef UP
   if (e == cudaSuccess) {
     unsigned long long* cnt = nullptr;
-    e = cudaMalloc(&cnt, 64);
+    e = cudaMalloc(&cnt, 256);
     if (e == cudaSuccess) {
       ix->allocs.push_back(cnt);
-      e = cudaMemset(cnt, 0, 64);
+      e = cudaMemset(cnt, 0, 256);
       v.counters = cnt;
     }
   }
@@ -733,11 +743,11 @@ int64_t givf_index_device_bytes(givf_index_t ix) { return ix ? ix->dev_bytes : 0
 
 int givf_index_counters(givf_index_t ix, int64_t* out, int32_t n) {
   if (!ix || !out) return fail(GIVF_EINVAL, "null argument");
-  unsigned long long h[8] = {};
+  unsigned long long h[32] = {};
   CUDA_TRY(cudaSetDevice(ix->device));
   CUDA_TRY(cudaDeviceSynchronize());
   CUDA_TRY(cudaMemcpy(h, ix->v.counters, sizeof h, cudaMemcpyDeviceToHost));
-  for (int i = 0; i < n && i < 8; ++i) out[i] = (int64_t)h[i];
+  for (int i = 0; i < n && i < 32; ++i) out[i] = (int64_t)h[i];
   return GIVF_OK;
 }
 

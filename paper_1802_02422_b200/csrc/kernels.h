@@ -94,7 +94,12 @@ struct PlanArgs {
   int64_t ldD;
   float cmax, eps_scale;
   int* only;            // (nq) fallback flags: exact kernels run where only[b] != 0
+  uint32_t* akey;       // (nq, P*G) scratch: float32 order key of the approximate score
+  int defer_rescore;    // set by launch_plan_approx: base/score by k_plan_rescore
 };
+// plan_approx.cu: approximate-first planner (sets only[b] for the queries it
+// cannot certify); returns kernels launched.
+int launch_plan_approx(const PlanArgs& a, cudaStream_t s);
 // Launches the approximate-first planner (when a.D is set) followed by the
 // exact planner for the queries it could not certify; returns kernels launched.
 int launch_plan(const PlanArgs& a, cudaStream_t s);
@@ -115,6 +120,9 @@ struct ScanArgs {
   int64_t cap_full_p2;
 };
 void launch_scan(const ScanArgs& a, cudaStream_t s);
+// scan_async.cu: top-k scan with cp.async-staged code tiles; false when the
+// configuration is not covered (full mode, M not in {4, 8, 16, 32}, k > 2048)
+bool launch_scan_async(const ScanArgs& a, cudaStream_t s);
 // full mode: sort each query's keys and split into ids/dists rows of width `ld`
 void launch_full_finish(uint64_t* keys, int64_t cap_p2, const int64_t* stats, int nq,
                         int32_t* ids, float* dists, int64_t ld, cudaStream_t s);

@@ -1,0 +1,636 @@
+// K3 + K4 fast path: approximate group scores from the probe's fp32 scores,
+// float64 only where a decision depends on it (reference: search.py:111-139).
+//
+// qs2 = |q - c_s|^2 needs a float64 centroid row per (region, group) item;
+// the probe GEMM already holds s~_c = |c|^2 - 2 q.c for every centroid with
+// an a-priori error bound eps (probe.cu, probe_tc.cu).  With
+// qs2~ = s~ + |q|^2 every approximate score is within E of the exact one
+// (alpha <= 1; the float32 key adds one more rounding, folded into E).
+//
+//   K3a k_plan_scores_approx  one warp per (query, probed region), lanes over
+//       its groups: gather s~ of the neighbor centroid, form the score, write
+//       its float32 order key.
+//   K4  k_plan_approx         one CTA per query:
+//     1. locates the approximate crossing (kept count / candidate budget) by
+//        bucket refinement over the keys, sorts only the boundary bucket and
+//        takes v*, the approximate score of the last begun group;
+//     2. splits items into A (score~ < v*-3E: exact < v*-2E), the window W
+//        (|score~ - v*| <= 3E) and C (score~ > v*+3E: exact > v*+2E);
+//     3. scores W exactly, sorts it and walks it from A's count and weight;
+//     4. certifies: the exact last begun group x_c lies in W with
+//        v*-2E <= score(x_c) <= v*+2E and the walk ends inside W.  Then the
+//        groups preceding x_c in the exact order are exactly A and the W
+//        groups before it, every C group follows it, and the begun set,
+//        lengths and stats are the exact walk's.  Otherwise the query is
+//        flagged and the exact planner (plan.cu) redoes it;
+//     5. emits A and the begun W groups (compacted, one metadata gather per
+//        group) with float64 base/score recomputed exactly from one centroid
+//        row per emitted group.
+#include "common.cuh"
+#include "kernels.h"
+#include "plan_common.cuh"
+
+namespace givf {
+
+constexpr int PA_THREADS = 256;
+constexpr int PA_ITEMS = 4096;    // items staged in shared memory (else read from L2/HBM)
+constexpr int PA_BUCKETS = 1024;
+constexpr int PA_SORT = 1024;     // boundary-bucket sort capacity
+constexpr int PA_SMALL = 128;     // refine further while the bucket is larger
+constexpr int PA_WCAP = 256;      // window capacity
+constexpr int PA_CAND = 2048;     // begun groups (else the exact planner)
+constexpr int PA_PSTAGE = 512;    // probed regions staged in shared memory
+constexpr int PA_U = 4;           // centroid rows in flight per 8-lane group
+// histogram cells and prefixes carry (count << 40 | weight): weights are group
+// sizes summing to at most n < 2^40, counts at most P*G < 2^24
+constexpr int CW = 40;
+constexpr unsigned long long WMASK = (1ull << CW) - 1;
+
+// ---------------------------------------------------------------- K3a
+__global__ void __launch_bounds__(PA_THREADS) k_plan_scores_approx(PlanArgs a) {
+  const IndexView& ix = a.ix;
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (int64_t)blockIdx.x * (PA_THREADS / 32) + (threadIdx.x >> 5);
+  const int P = a.P, G = ix.G, d = ix.d;
+  if (wid >= (int64_t)a.nq * P) return;
+  const int b = (int)(wid / P), p = (int)(wid % P);
+  const int64_t total = (int64_t)P * G;
+  const int r = a.regions[(int64_t)b * P + p];
+  const double qc = a.qc2[(int64_t)b * P + p];
+  uint32_t* akey = a.akey + (int64_t)b * total + (int64_t)p * G;
+  if (!ix.grouping) {
+    const uint32_t k = f32_key((float)qc);
+    for (int j = lane; j < G; j += 32) akey[j] = k;
+    return;
+  }
+  const float* q = a.Q + (int64_t)b * d;
+  double q2 = 0.0;
+  for (int j = lane; j < d; j += 32) q2 += (double)q[j] * (double)q[j];
+  q2 = warp_sum(q2);
+  const float* Drow = a.D + (int64_t)b * a.ldD;
+  const double al = (double)ix.alphas[r];
+  const double oma_qc = dmul(dsub(1.0, al), qc);
+  for (int j = lane; j < G; j += 32) {
+    const int64_t gi = (int64_t)r * G + j;
+    const double qs2 = dadd((double)__ldg(Drow + ix.nbr[gi]), q2);
+    const double score = dadd(dadd(oma_qc, dmul(al, qs2)), (double)ix.norm[gi]);
+    akey[j] = f32_key((float)score);
+  }
+}
+
+// ---------------------------------------------------------------- K4
+struct PaSmem {
+  // byte offsets into the dynamic shared block
+  size_t skey, ssz, pool, wkey, wval, wlen, wrow, wnorm, qd, preg, pqc, pal, bytes;
+  __host__ __device__ PaSmem(int d, int P, int64_t total) {
+    const bool staged = total <= PA_ITEMS;
+    const bool pst = P <= PA_PSTAGE;
+    size_t o = 0;
+    auto take = [&](size_t n) { size_t r = o; o = (o + n + 15) & ~(size_t)15; return r; };
+    pool = take((size_t)3 * PA_CAND * 4 > (size_t)(PA_BUCKETS + PA_SORT) * 8
+                    ? (size_t)3 * PA_CAND * 4 : (size_t)(PA_BUCKETS + PA_SORT) * 8);
+    wkey = take((size_t)PA_WCAP * 8);
+    qd = take((size_t)d * 8);
+    pqc = take(pst ? (size_t)P * 8 : 0);
+    pal = take(pst ? (size_t)P * 8 : 0);
+    preg = take(pst ? (size_t)P * 4 : 0);
+    wval = take((size_t)PA_WCAP * 4);
+    wlen = take((size_t)PA_WCAP * 4);
+    wrow = take((size_t)PA_WCAP * 4);
+    wnorm = take((size_t)PA_WCAP * 4);
+    skey = take(staged ? (size_t)PA_ITEMS * 4 : 0);
+    ssz = take(staged ? (size_t)PA_ITEMS * 4 : 0);
+    bytes = o;
+  }
+};
+
+__global__ void __launch_bounds__(PA_THREADS, 3) k_plan_approx(PlanArgs a) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const IndexView& ix = a.ix;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const int G = ix.G, d = ix.d, P = a.P;
+  const int64_t total = (int64_t)P * G;
+  const bool staged = total <= PA_ITEMS;
+  const bool pst = P <= PA_PSTAGE;
+  const PaSmem L(d, P, total);
+
+  unsigned long long* hw = reinterpret_cast<unsigned long long*>(dsm + L.pool);
+  uint64_t* bkey = reinterpret_cast<uint64_t*>(hw + PA_BUCKETS);
+  uint32_t* cf = reinterpret_cast<uint32_t*>(dsm + L.pool);  // begun groups: flat
+  int32_t* cl = reinterpret_cast<int32_t*>(cf + PA_CAND);     //   length; after emission: row
+  int32_t* cp = cl + PA_CAND;                                 //   after emission: norm bits | p
+  uint64_t* wkey = reinterpret_cast<uint64_t*>(dsm + L.wkey);
+  uint32_t* wval = reinterpret_cast<uint32_t*>(dsm + L.wval);
+  int32_t* wlen = reinterpret_cast<int32_t*>(dsm + L.wlen);
+  int32_t* wrow = reinterpret_cast<int32_t*>(dsm + L.wrow);
+  float* wnorm = reinterpret_cast<float*>(dsm + L.wnorm);
+  double* qd = reinterpret_cast<double*>(dsm + L.qd);
+  uint32_t* skey = reinterpret_cast<uint32_t*>(dsm + L.skey);
+  int32_t* ssz = reinterpret_cast<int32_t*>(dsm + L.ssz);
+  int32_t* preg = reinterpret_cast<int32_t*>(dsm + L.preg);
+  double* pqc = reinterpret_cast<double*>(dsm + L.pqc);
+  double* pal = reinterpret_cast<double*>(dsm + L.pal);
+  __shared__ unsigned long long red64[40];
+  __shared__ uint32_t red32[40];
+  __shared__ double redd[40];
+  __shared__ int s_b, s_lastb;
+  __shared__ uint32_t s_nbk, s_nw;
+  __shared__ unsigned long long s_before;
+
+  const uint32_t* gkey = a.akey + (int64_t)b * total;
+  const int* greg = a.regions + (int64_t)b * P;
+  const double* gqc = a.qc2 + (int64_t)b * P;
+  const uint64_t kept = (uint64_t)a.kept, budget = (uint64_t)a.budget;
+#ifdef GIVF_PHASES
+  long long t_phase_ = clock64();
+#endif
+
+  // ---- 0. stage the query, the probed regions, the items; key range
+  double q2p = 0.0;
+  for (int j = tid; j < d; j += PA_THREADS) {
+    const double x = (double)a.Q[(int64_t)b * d + j];
+    qd[j] = x;
+    q2p += x * x;
+  }
+  if (pst)
+    for (int p = tid; p < P; p += PA_THREADS) {
+      const int r = greg[p];
+      preg[p] = r;
+      pqc[p] = gqc[p];
+      pal[p] = ix.grouping ? (double)ix.alphas[r] : 0.0;
+    }
+  __syncthreads();
+  auto REG = [&](int p) -> int { return pst ? preg[p] : greg[p]; };
+  auto QC = [&](int p) -> double { return pst ? pqc[p] : gqc[p]; };
+  auto AL = [&](int p) -> double {
+    return pst ? pal[p] : (ix.grouping ? (double)ix.alphas[greg[p]] : 0.0);
+  };
+  auto GI = [&](int64_t f) -> int64_t {
+    const int p = (int)(f / G);
+    return (int64_t)REG(p) * G + (f - (int64_t)p * G);
+  };
+  uint32_t kmin = 0xffffffffu, kmax = 0u;
+  if (staged) {
+    // all of a thread's loads in flight at once (total <= PA_ITEMS)
+    constexpr int PT = PA_ITEMS / PA_THREADS;
+    uint32_t kk[PT];
+    int32_t zz[PT];
+#pragma unroll
+    for (int t = 0; t < PT; ++t) {
+      const int f = tid + t * PA_THREADS;
+      kk[t] = f < total ? gkey[f] : 0u;
+      zz[t] = f < total ? __ldg(ix.gsize + GI(f)) : 0;
+    }
+#pragma unroll
+    for (int t = 0; t < PT; ++t) {
+      const int f = tid + t * PA_THREADS;
+      if (f < total) {
+        skey[f] = kk[t];
+        ssz[f] = zz[t];
+        kmin = min(kmin, kk[t]);
+        kmax = max(kmax, kk[t]);
+      }
+    }
+  } else {
+    for (int64_t f = tid; f < total; f += PA_THREADS) {
+      const uint32_t k = gkey[f];
+      kmin = min(kmin, k);
+      kmax = max(kmax, k);
+    }
+  }
+  const double q2 = block_sum(q2p, redd);
+  kmin = block_min(kmin, red32);
+  kmax = block_max(kmax, red32);
+  auto KEY = [&](int64_t f) -> uint32_t { return staged ? skey[f] : gkey[f]; };
+  auto SIZE = [&](int64_t f) -> int64_t { return staged ? ssz[f] : ix.gsize[GI(f)]; };
+  const double qn = sqrt(q2);
+  const double amax = fmax(fabs((double)key_f32(kmin)), fabs((double)key_f32(kmax)));
+  const double cq = (double)a.cmax + qn;
+  const double E = ix.grouping
+      ? 1.0001 * ((double)a.eps_scale * ((double)a.cmax * a.cmax + 2.0 * qn * a.cmax)) +
+            amax * 1.2e-7 + 1e-12 * cq * cq
+      : amax * 1.2e-7;  // float32 key rounding only
+  PLAN_PHASE(0);
+
+  // ---- 1. approximate crossing: bucket refinement on the float32 keys
+  uint64_t taken_c = 0, taken_w = 0;
+  uint32_t lo = kmin, hi = kmax, bucket_lo = 0, bucket_hi = 0;
+  bool no_cut = false, flag = false;
+  for (int level = 0; level < 4; ++level) {
+    const uint32_t range = hi - lo;
+    const int shift = range == 0 ? 0 : max(0, 32 - __clz(range) - 10);  // <= 1024 buckets
+    const uint32_t nb = (range >> shift) + 1;
+    for (uint32_t i = tid; i < nb; i += PA_THREADS) hw[i] = 0;
+    __syncthreads();
+    for (int64_t f = tid; f < total; f += PA_THREADS) {
+      const uint32_t k = KEY(f);
+      if (k < lo || k > hi) continue;
+      atomicAdd(&hw[(k - lo) >> shift], (1ull << CW) | (unsigned long long)SIZE(f));
+    }
+    __syncthreads();
+    constexpr uint32_t PER = PA_BUCKETS / PA_THREADS;
+    const uint32_t b0 = tid * PER, b1 = min(nb, b0 + PER);
+    unsigned long long rs = 0;
+    for (uint32_t x = b0; x < b1; ++x) rs += hw[x];
+    unsigned long long tot;
+    const unsigned long long ps = block_exclusive_scan(rs, red64, &tot);
+    if (tid == 0) s_b = -1;
+    __syncthreads();
+    {
+      const uint64_t c0 = taken_c + (ps >> CW), w0 = taken_w + (ps & WMASK);
+      const uint64_t c1 = c0 + (rs >> CW), w1 = w0 + (rs & WMASK);
+      if (b0 < b1 && c0 < kept && w0 < budget && (c1 >= kept || w1 >= budget)) {
+        unsigned long long acc = ps;
+        for (uint32_t x = b0; x < b1; ++x) {
+          const unsigned long long nx = acc + hw[x];
+          if (taken_c + (nx >> CW) >= kept || taken_w + (nx & WMASK) >= budget) {
+            s_b = (int)x;
+            s_before = acc;
+            break;
+          }
+          acc = nx;
+        }
+      }
+    }
+    __syncthreads();
+    const int bsel = s_b;
+    if (bsel < 0) {  // never crosses: every group is scanned whole
+      no_cut = true;
+      break;
+    }
+    const uint32_t cnt_b = (uint32_t)(hw[bsel] >> CW);
+    const uint32_t bl = lo + ((uint32_t)bsel << shift);
+    const uint64_t bspan = (uint64_t)bl + ((1ull << shift) - 1);
+    const uint32_t bh = (uint32_t)(bspan < hi ? bspan : hi);
+    taken_c += s_before >> CW;
+    taken_w += s_before & WMASK;
+    __syncthreads();
+    if (cnt_b <= (uint32_t)PA_SMALL || (shift == 0 && cnt_b <= (uint32_t)PA_SORT)) {
+      bucket_lo = bl;
+      bucket_hi = bh;
+      break;
+    }
+    if (shift == 0 || level == 3) {  // > PA_SORT equal approximate keys: exact planner
+      flag = true;
+      break;
+    }
+    lo = bl;
+    hi = bh;
+  }
+  PLAN_PHASE(2);
+
+  double vstar = __longlong_as_double(0x7ff0000000000000ll);  // +inf: no cut
+  if (!no_cut && !flag) {
+    if (tid == 0) { s_nbk = 0; s_lastb = -1; }
+    __syncthreads();
+    for (int64_t f = tid; f < total; f += PA_THREADS) {
+      const uint32_t k = KEY(f);
+      if (k >= bucket_lo && k <= bucket_hi) bkey[atomicAdd(&s_nbk, 1u)] = ((uint64_t)k << 32) | (uint32_t)f;
+    }
+    __syncthreads();
+    const uint32_t nbk = s_nbk;
+    const uint32_t np2 = next_pow2(max(nbk, 1u));
+    for (uint32_t i = nbk + tid; i < np2; i += PA_THREADS) bkey[i] = kKeyPad;
+    __syncthreads();
+    bitonic_sort_keys(bkey, np2);
+    unsigned long long carry = taken_w;
+    for (uint32_t t0 = 0; t0 < nbk; t0 += PA_THREADS) {
+      const uint32_t i = t0 + tid;
+      const unsigned long long sz = i < nbk ? (unsigned long long)SIZE((uint32_t)bkey[i]) : 0ull;
+      unsigned long long tile;
+      const unsigned long long excl = block_exclusive_scan(sz, red64, &tile);
+      if (i < nbk && taken_c + i < kept && carry + excl < budget) atomicMax(&s_lastb, (int)i);
+      carry += tile;
+    }
+    __syncthreads();
+    vstar = (double)key_f32((uint32_t)(bkey[max(s_lastb, 0)] >> 32));
+  }
+  PLAN_PHASE(3);
+
+  // ---- 2./3. window around v*: exact scores, sorted, walked from A's prefix
+  const double wlo = vstar - 3.0 * E, whi = vstar + 3.0 * E;
+  if (tid == 0) s_nw = 0;
+  __syncthreads();
+  int my_a = 0;  // A items of this thread (for the compaction below)
+  unsigned long long nA, wA;
+  {
+    unsigned long long cw = 0;
+    for (int64_t f = tid; f < total; f += PA_THREADS) {
+      const double v = (double)key_f32(KEY(f));
+      if (v < wlo) {
+        ++my_a;
+        cw += (1ull << CW) | (unsigned long long)SIZE(f);
+      } else if (v <= whi && !no_cut) {
+        const uint32_t p = atomicAdd(&s_nw, 1u);
+        if (p < PA_WCAP) wval[p] = (uint32_t)f;
+      }
+    }
+    cw = block_sum(cw, red64);
+    nA = cw >> CW;
+    wA = cw & WMASK;
+  }
+  const uint32_t nw = s_nw;
+  if (nw > (uint32_t)PA_WCAP) flag = true;
+  int lastw = -1;
+  unsigned long long wsum = 0;  // lengths of the begun window groups
+  if (!flag && !no_cut) {
+    // one metadata gather per window group, then the centroid rows
+    if (tid < (int)nw) {
+      const int64_t gi = GI(wval[tid]);
+      wrow[tid] = ix.grouping ? ix.nbr[gi] : 0;
+      wnorm[tid] = ix.grouping ? ix.norm[gi] : 0.f;
+    }
+    __syncthreads();
+    const int grp = tid >> 3, gl = tid & 7;
+    constexpr int NG = PA_THREADS >> 3;
+    for (uint32_t i0 = 0; i0 < nw; i0 += NG * PA_U) {
+      const float* rows[PA_U];
+#pragma unroll
+      for (int u = 0; u < PA_U; ++u) {
+        const uint32_t i = i0 + u * NG + grp;
+        rows[u] = ix.centroids + (int64_t)(i < nw ? wrow[i] : 0) * d;
+      }
+      double qs2[PA_U];
+      if (ix.grouping) {
+        if ((d & 3) == 0 && d <= 128) {
+          group8_sqdist64_multi<PA_U>(rows, qd, d >> 2, qs2);
+        } else {
+#pragma unroll
+          for (int u = 0; u < PA_U; ++u) qs2[u] = group8_sqdist64(rows[u], qd, d);
+        }
+      }
+      if (gl == 0) {
+#pragma unroll
+        for (int u = 0; u < PA_U; ++u) {
+          const uint32_t i = i0 + u * NG + grp;
+          if (i >= nw) continue;
+          const int p = (int)(wval[i] / G);
+          double score = QC(p);
+          if (ix.grouping) {
+            const double al = AL(p);
+            score = dadd(dadd(dmul(dsub(1.0, al), QC(p)), dmul(al, qs2[u])), (double)wnorm[i]);
+          }
+          wkey[i] = f64_key(score);
+        }
+      }
+    }
+    const uint32_t np2 = next_pow2(max(nw, 1u));
+    for (uint32_t i = nw + tid; i < np2; i += PA_THREADS) { wkey[i] = kKeyPad; wval[i] = 0xffffffffu; }
+    __syncthreads();
+    bitonic_sort(wkey, wval, np2);  // (score, flat): the reference order
+    if (tid == 0) s_lastb = -1;
+    __syncthreads();
+    unsigned long long carry = wA, mine = 0;
+    for (uint32_t t0 = 0; t0 < nw; t0 += PA_THREADS) {
+      const uint32_t i = t0 + tid;
+      const unsigned long long sz = i < nw ? (unsigned long long)SIZE(wval[i]) : 0ull;
+      unsigned long long tile;
+      const unsigned long long excl = block_exclusive_scan(sz, red64, &tile);
+      if (i < nw) {
+        const unsigned long long w = carry + excl;
+        const bool ok = (nA + i < kept) && (w < budget);
+        wlen[i] = ok ? (int32_t)min(sz, budget - w) : 0;
+        if (ok) {
+          atomicMax(&s_lastb, (int)i);
+          mine += (unsigned long long)wlen[i];
+        }
+      }
+      carry += tile;
+    }
+    wsum = block_sum(mine, red64);
+    const int xc = s_lastb;
+    if (xc < 0) {
+      flag = true;  // the exact crossing precedes the window
+    } else {
+      lastw = xc;
+      const double sx = key_to_f64(wkey[xc]);
+      if (!(sx >= vstar - 2.0 * E && sx <= vstar + 2.0 * E)) flag = true;
+      const bool ended = ((uint32_t)xc + 1 < nw) || (nA + nw >= kept) || (carry >= budget);
+      if (!ended) flag = true;
+    }
+  }
+  const uint64_t nbegun = nA + (uint64_t)(lastw + 1);
+  if (nbegun > (uint64_t)PA_CAND) flag = true;
+  PLAN_PHASE(4);
+  if (flag) {
+    if (tid == 0) {
+      a.only[b] = 1;
+      if (ix.counters) atomicAdd(&ix.counters[1], 1ull);
+    }
+    return;
+  }
+  if (tid == 0) a.only[b] = 0;
+
+  // ---- 5. begun groups: A (compacted in thread order) then W[0..lastw]
+  {
+    uint32_t tot;
+    uint32_t pos = block_exclusive_scan((uint32_t)my_a, red32, &tot);
+    for (int64_t f = tid; f < total; f += PA_THREADS) {
+      if ((double)key_f32(KEY(f)) < wlo) {
+        cf[pos] = (uint32_t)f;
+        cl[pos] = (int32_t)SIZE(f);
+        ++pos;
+      }
+    }
+    for (int i = tid; i <= lastw; i += PA_THREADS) {
+      cf[nA + i] = wval[i];
+      cl[nA + i] = wlen[i];
+    }
+  }
+  __syncthreads();
+  // emission: one metadata gather per begun group; positions by block scan
+  // (groups with no local rows are dropped).  Slot pos <= candidate index, so
+  // the candidate arrays are reused in place for (row, norm, p).
+  WorkItem* Wl = a.work + (int64_t)b * a.cap_w;
+  const int nc = (int)nbegun;
+  int nemit = 0;
+  for (int c0 = 0; c0 < nc; c0 += PA_THREADS) {
+    const int c = c0 + tid;
+    int64_t ll = 0, start = 0;
+    uint32_t f = 0;
+    int32_t row = 0;
+    float nrm = 0.f;
+    if (c < nc) {  // independent loads, issued together
+      f = cf[c];
+      const int64_t gi = GI(f);
+      const int64_t len_g = cl[c];
+      const int64_t lo_ = ix.llo ? ix.llo[gi] : 0;
+      const int64_t cnt_ = ix.lsize ? ix.lsize[gi] : ix.gsize[gi];
+      start = ix.lstart[gi];
+      if (ix.grouping) {
+        row = ix.nbr[gi];
+        nrm = ix.norm[gi];
+      }
+      ll = min(max(len_g - lo_, (int64_t)0), cnt_);
+    }
+    uint32_t tot;
+    const uint32_t pos = nemit + block_exclusive_scan((uint32_t)(ll > 0), red32, &tot);
+    if (ll > 0) {
+      WorkItem w;
+      w.start = start;
+      w.len = (int32_t)ll;
+      w.flat = (int32_t)f;
+      // deferred rescoring (k_plan_rescore): stash (row, p) and (norm, alpha)
+      const int p = (int)(f / G);
+      w.base = __hiloint2double(p, row);
+      w.score = __hiloint2double(__float_as_int((float)AL(p)), __float_as_int(nrm));
+      Wl[pos] = w;
+      cf[pos] = (uint32_t)row;
+      cl[pos] = __float_as_int(nrm);
+      cp[pos] = (int32_t)(f / G);
+    }
+    nemit += (int)tot;
+  }
+  __syncthreads();
+  PLAN_PHASE(5);
+  // exact float64 base / score of the emitted groups (here only when the
+  // scan order needs them in this CTA; else k_plan_rescore)
+  if (!a.defer_rescore) {
+    const int grp = tid >> 3, gl = tid & 7;
+    constexpr int NG = PA_THREADS >> 3;
+    const bool vec = (d & 3) == 0 && d <= 128;
+    for (int i0 = 0; i0 < nemit; i0 += NG * PA_U) {
+      const float* rows[PA_U];
+#pragma unroll
+      for (int u = 0; u < PA_U; ++u) {
+        const int i = i0 + u * NG + grp;
+        rows[u] = ix.centroids + (int64_t)(i < nemit ? (int)cf[i] : 0) * d;
+      }
+      double qs2[PA_U];
+      if (ix.grouping) {
+        if (vec) {
+          group8_sqdist64_multi<PA_U>(rows, qd, d >> 2, qs2);
+        } else {
+#pragma unroll
+          for (int u = 0; u < PA_U; ++u) qs2[u] = group8_sqdist64(rows[u], qd, d);
+        }
+      }
+      if (gl == 0) {
+#pragma unroll
+        for (int u = 0; u < PA_U; ++u) {
+          const int i = i0 + u * NG + grp;
+          if (i >= nemit) continue;
+          const int p = cp[i];
+          double base = QC(p), score = QC(p);
+          if (ix.grouping) {
+            const double al = AL(p);
+            base = dadd(dmul(dsub(1.0, al), QC(p)), dmul(al, qs2[u]));
+            score = dadd(base, (double)__int_as_float(cl[i]));
+          }
+          Wl[i].base = base;
+          Wl[i].score = score;
+        }
+      }
+    }
+  }
+  PLAN_PHASE(6);
+  if (tid == 0) {
+    a.nwork[b] = nemit;
+    int64_t* st = a.stats + (int64_t)b * 4;
+    st[0] = P;
+    st[1] = (int64_t)nbegun;
+    st[2] = total - (int64_t)kept;
+    st[3] = (int64_t)(wA + wsum);
+  }
+  if (a.sort_work) {
+    __syncthreads();
+    const uint32_t wp2 = next_pow2(max(nemit, 1));
+    int64_t cp2 = 1;
+    while (cp2 < a.cap_w) cp2 <<= 1;
+    uint64_t* sk = a.skey + (int64_t)b * cp2;
+    uint32_t* sv = a.sval + (int64_t)b * cp2;
+    for (uint32_t i = tid; i < wp2; i += PA_THREADS) {
+      sk[i] = (int)i < nemit ? f64_key(Wl[i].score) : kKeyPad;
+      sv[i] = (int)i < nemit ? (uint32_t)Wl[i].flat : 0xffffffffu;
+    }
+    __syncthreads();
+    bitonic_sort(sk, sv, wp2);
+    for (int i = tid; i < nemit; i += PA_THREADS) {
+      const uint64_t key = f64_key(Wl[i].score);
+      const uint32_t fl = (uint32_t)Wl[i].flat;
+      int lo_i = 0, hi_i = nemit - 1;
+      while (lo_i < hi_i) {
+        const int mid = (lo_i + hi_i) >> 1;
+        const bool less = sk[mid] < key || (sk[mid] == key && sv[mid] < fl);
+        if (less) lo_i = mid + 1; else hi_i = mid;
+      }
+      a.order[(int64_t)b * a.cap_w + lo_i] = i;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K4b
+// Exact float64 base / score of the work items k_plan_approx emitted, many
+// queries' items in flight per SM (one CTA per (query, slice of its items)).
+constexpr int RS_THREADS = 128;
+constexpr int RS_SPLIT = 4;
+
+__global__ void __launch_bounds__(RS_THREADS, 4) k_plan_rescore(PlanArgs a) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  double* qd = reinterpret_cast<double*>(dsm);
+  const IndexView& ix = a.ix;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  constexpr int NG = RS_THREADS >> 3, PER = NG * PA_U;
+  if (a.only[b] != 0) return;  // the exact planner owns this query
+  const int n = a.nwork[b];
+  if ((int)blockIdx.y * PER >= n) return;
+  const int d = ix.d;
+  for (int j = tid; j < d; j += RS_THREADS) qd[j] = (double)a.Q[(int64_t)b * d + j];
+  __syncthreads();
+  WorkItem* Wl = a.work + (int64_t)b * a.cap_w;
+  const double* qc2 = a.qc2 + (int64_t)b * a.P;
+  const int grp = tid >> 3, gl = tid & 7;
+  const bool vec = (d & 3) == 0 && d <= 128;
+  for (int i0 = blockIdx.y * PER; i0 < n; i0 += RS_SPLIT * PER) {
+    const float* rows[PA_U];
+    double sb[PA_U], ss[PA_U];
+#pragma unroll
+    for (int u = 0; u < PA_U; ++u) {
+      const int i = i0 + u * NG + grp;
+      sb[u] = i < n ? Wl[i].base : 0.0;
+      ss[u] = i < n ? Wl[i].score : 0.0;
+      rows[u] = ix.centroids + (int64_t)__double2loint(sb[u]) * d;
+    }
+    double qs2[PA_U];
+    if (vec) {
+      group8_sqdist64_multi<PA_U>(rows, qd, d >> 2, qs2);
+    } else {
+#pragma unroll
+      for (int u = 0; u < PA_U; ++u) qs2[u] = group8_sqdist64(rows[u], qd, d);
+    }
+    if (gl == 0) {
+#pragma unroll
+      for (int u = 0; u < PA_U; ++u) {
+        const int i = i0 + u * NG + grp;
+        if (i >= n) continue;
+        const int p = __double2hiint(sb[u]);
+        const double al = (double)__int_as_float(__double2hiint(ss[u]));
+        const double nrm = (double)__int_as_float(__double2loint(ss[u]));
+        const double base = dadd(dmul(dsub(1.0, al), qc2[p]), dmul(al, qs2[u]));
+        Wl[i].base = base;
+        Wl[i].score = dadd(base, nrm);
+      }
+    }
+  }
+}
+
+int launch_plan_approx(const PlanArgs& a0, cudaStream_t s) {
+  PlanArgs a = a0;
+  // the scan-order sort (rerank=False) needs the scores inside k_plan_approx
+  a.defer_rescore = (a.ix.grouping && !a.sort_work) ? 1 : 0;
+  const PaSmem L(a.ix.d, a.P, (int64_t)a.P * a.ix.G);
+  static size_t attr = 0;
+  if (L.bytes > attr) {
+    cudaFuncSetAttribute(k_plan_approx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
+    attr = L.bytes;
+  }
+  const int64_t warps = (int64_t)a.nq * a.P;
+  const int per = PA_THREADS / 32;
+  k_plan_scores_approx<<<(unsigned)((warps + per - 1) / per), PA_THREADS, 0, s>>>(a);
+  k_plan_approx<<<a.nq, PA_THREADS, L.bytes, s>>>(a);
+  if (!a.defer_rescore) return 2;
+  k_plan_rescore<<<dim3(a.nq, RS_SPLIT), RS_THREADS, (size_t)a.ix.d * 8, s>>>(a);
+  return 3;
+}
+
+}  // namespace givf

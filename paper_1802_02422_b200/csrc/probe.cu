@@ -100,7 +100,6 @@ k_probe_gemm(const float* __restrict__ Q, const float* __restrict__ C,
 // found by <= 3 levels of 2048-bucket histograms over the order-preserving
 // u32 keys.  theta = smallest excluded score (+inf when nothing excluded).
 constexpr int SEL_THREADS = 512;
-constexpr int SEL_BUCKETS = 2048;
 
 // Generic path: bucketed refinement over the whole row (any K, any ties).
 __device__ void select_bucketed(const float* __restrict__ row, int K, int Tmin, int cap,
@@ -214,7 +213,7 @@ k_probe_select(const float* __restrict__ D, int64_t ldD, int K, int Tmin, int ca
     if (tid == 0) { cand_n[blockIdx.x] = K; theta[blockIdx.x] = __int_as_float(0x7f800000); }
     return;
   }
-  uint32_t* hist = reinterpret_cast<uint32_t*>(dsm);  // SEL_BUCKETS, aliases tk below
+  uint32_t* hist = reinterpret_cast<uint32_t*>(dsm);  // 2048 buckets, aliases tk below
   if (tmin == nullptr || ntiles < Tmin) {
     select_bucketed(row, K, Tmin, cap, out, cand_n + blockIdx.x, theta + blockIdx.x, hist);
     return;

@@ -12,7 +12,7 @@ python - <<'PY'
 import json
 try:
     d = json.load(open("gpurun_out/bench_c2.json"))
-    print("BENCH:", round(d["value"]), "qps  e2e", round(d["e2e"]["value"] or 0), " r@10", d["config"]["recall@10"],
+    print("BENCH:", round(d["value"]), "qps  e2e", round(d["e2e"]["value"] or 0), " r@10", d["config"]["recall@10"], d.get("fallback_queries_per_step"),
           {k: round(v, 3) for k, v in d["stage_ms_per_step"].items()})
 except Exception as e:
     print("BENCH failed:", e)
