@@ -166,7 +166,9 @@ namespace {
 template <typename T>
 cudaError_t upload(givf_index* ix, const T* host, size_t count, const T** out) {
   void* d = nullptr;
-  size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+  // padded: vector loads (the scan's 4-byte constant-byte words) may read up
+  // to 15 bytes past the last element
+  size_t bytes = ((count * sizeof(T) + 15) & ~(size_t)15) + 16;
   cudaError_t e = cudaMalloc(&d, bytes);
   if (e != cudaSuccess) return e;
   ix->allocs.push_back(d);
@@ -229,9 +231,13 @@ size_t l2_budget() {
   return (size_t)(s ? atoll(s) : (1ll << 20)) << 20;
 }
 
-bool use_async_scan() {
+// 0: warp-independent scan (default), 1: block scan (GIVF_SCAN=block),
+// 2: cp.async-staged block scan (GIVF_SCAN=async)
+int scan_mode() {
   const char* s = getenv("GIVF_SCAN");
-  return s && strcmp(s, "async") == 0;  // measured slower on C2 so far: opt-in
+  if (s && strcmp(s, "async") == 0) return 2;
+  if (s && strcmp(s, "block") == 0) return 1;
+  return 0;
 }
 
 int nstreams_default() {
@@ -528,7 +534,10 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
         sa.cap_full_p2 = full_p2;
       }
       staged(ST_SCAN, st, [&] {
-        if (!(use_async_scan() && launch_scan_async(sa, st))) launch_scan(sa, st);
+        const int mode = scan_mode();
+        if (mode == 2 && launch_scan_async(sa, st)) return;
+        if (mode == 0 && launch_scan_warp(sa, st)) return;
+        launch_scan(sa, st);
       });
       KCHECK();
       if (om == OUT_FULL) {

@@ -123,6 +123,9 @@ void launch_scan(const ScanArgs& a, cudaStream_t s);
 // scan_async.cu: top-k scan with cp.async-staged code tiles; false when the
 // configuration is not covered (full mode, M not in {4, 8, 16, 32}, k > 2048)
 bool launch_scan_async(const ScanArgs& a, cudaStream_t s);
+// scan_warp.cu: warp-independent sweeps (the default); false when the
+// configuration is not covered (M > 32, top-k k > 128, n >= 2^32)
+bool launch_scan_warp(const ScanArgs& a, cudaStream_t s);
 // full mode: sort each query's keys and split into ids/dists rows of width `ld`
 void launch_full_finish(uint64_t* keys, int64_t cap_p2, const int64_t* stats, int nq,
                         int32_t* ids, float* dists, int64_t ld, cudaStream_t s);

@@ -72,7 +72,7 @@ GIVF_DEV float code_sum(const CodeVec<M>& code, const float* lut) {
 
 // LUT of one query (pq.py:147-169): optional rotation q' = R q, then
 // entry[m][i] = <q'_m, codeword[m][i]> accumulated in float64, rounded once;
-// plus the dequantized constants as float64 (grouping.py:123-129).
+// plus (ctab != null) the dequantized constants as float64 (grouping.py:123-129).
 __device__ inline void build_lut_into(const IndexView& ix, const float* __restrict__ q, float* lut,
                                       double* ctab, float* qrot) {
   const int d = ix.d, M = ix.M, ds = d / M;
@@ -95,7 +95,8 @@ __device__ inline void build_lut_into(const IndexView& ix, const float* __restri
     for (int t = 0; t < ds; ++t) acc += (double)cw[t] * (double)qq[t];
     lut[e] = (float)acc;
   }
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) ctab[i] = (double)ix.ctab[i];
+  if (ctab)
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) ctab[i] = (double)ix.ctab[i];
   __syncthreads();
 }
 

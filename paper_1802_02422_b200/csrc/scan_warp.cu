@@ -1,0 +1,464 @@
+// K6 (default): ADC scan with warp-independent sweeps.
+//
+// Same results as k_scan (scan.cu): dist = f32(f64(base) - 2 f64(ip) +
+// f64(const)) with ip summed in numpy's order, top-k by (dist, id)
+// (search.py:142-158).  What changes is how the work is spread:
+//
+//  * The query's work list is taken in windows of SW_SEGS segments; the CTA
+//    stages (start row, base, first position) of a window in shared memory
+//    once.  The window's positions are split evenly between the 8 warps, and
+//    each warp then runs without block barriers.
+//  * A warp handles 32 consecutive positions at a time.  Lane l finds its
+//    segment without any per-position table: lane j holds the first position
+//    of the j-th following segment, one redux.or turns those into a bitmask
+//    of segment starts inside the batch, and popc(mask below l) is the
+//    lane's segment offset.  Code rows of consecutive positions are mostly
+//    consecutive, so code / constant-byte loads stay coalesced.
+//  * top-k: each warp keeps its own candidate buffer (dist key, row) and
+//    shrinks it with a warp radix select to exactly k by (dist, id).  The
+//    smallest k-th key over warps is shared (atomicMin in shared memory) and
+//    filters every warp: all keys above it are out of the final top-k.
+//  * The final merge takes the <= 8k entries under the shared bound, selects
+//    exactly k of them with a block radix select and sorts only those.
+//
+// Used for M in {4, 8, 12, 16, 24, 32}, k <= SW_KMAX and local row indices < 2^32;
+// k_scan covers
+// everything else.
+#include "common.cuh"
+#include "kernels.h"
+#include "scan_common.cuh"
+
+#include <cstdlib>
+
+namespace givf {
+
+constexpr int SW_THREADS = 256;
+constexpr int SW_WARPS = SW_THREADS / 32;
+constexpr int SW_SEGS = 256;   // segments per window
+constexpr int SW_WB = 384;     // per-warp candidate buffer (dist key << 32 | row)
+constexpr int SW_KMAX = 128;   // SW_WARPS * SW_KMAX merge entries
+constexpr unsigned FULL = 0xffffffffu;
+
+// Shared memory: fixed-size parts first so every address is a constant
+// offset (M is a template parameter; only qrot depends on the runtime d).
+constexpr size_t SW_WBUF = 0;                                     // u64 [WARPS][WB]
+constexpr size_t SW_MERGE = SW_WBUF + (size_t)SW_WARPS * SW_WB * 8;  // u64 [WARPS*KMAX]
+constexpr size_t SW_SSTART = SW_MERGE + (size_t)SW_WARPS * SW_KMAX * 8;  // u32 [SEGS]
+constexpr size_t SW_SBASE = SW_SSTART + (size_t)SW_SEGS * 4;      // f64 [SEGS]
+constexpr size_t SW_SOFF = SW_SBASE + (size_t)SW_SEGS * 8;        // i32 [SEGS + 32]
+constexpr size_t SW_CTAB = SW_SOFF + (size_t)(SW_SEGS + 32) * 4;  // f32 [256]
+constexpr size_t SW_LUT = SW_CTAB + 256 * 4;                      // f32 [M][256]
+__host__ __device__ constexpr size_t sw_qrot(int M) { return SW_LUT + (size_t)M * 1024; }
+__host__ __device__ constexpr size_t sw_bytes(int M, int d) {
+  return sw_qrot(M) + (((size_t)d * 4 + 15) & ~(size_t)15);
+}
+
+// Warp radix select: the digit-by-digit search for the need-th smallest of
+// the 32-bit keys key_of(i), i < n, that match `prefix` under `mask` (hist:
+// 256 words private to the warp).  Returns the key; *eq = how many of the n
+// keys equal it, *need = its rank among those equal keys (1-based).
+template <typename KeyOf>
+__device__ uint32_t warp_select(int n, KeyOf key_of, uint32_t* hist, uint32_t* need, uint32_t* eq) {
+  const int lane = threadIdx.x & 31;
+  uint32_t prefix = 0, mask = 0;
+  uint32_t last = 0;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) hist[lane * 8 + j] = 0;
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {
+      const uint32_t k = key_of(i);
+      if ((k & mask) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1u);
+    }
+    __syncwarp();
+    uint32_t h[8], run = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { h[j] = hist[lane * 8 + j]; run += h[j]; }
+    uint32_t incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t excl = incl - run;
+    const bool mine = excl < *need && incl >= *need;
+    const int src = __ffs(__ballot_sync(FULL, mine)) - 1;
+    uint32_t digit = 0, before = 0, cnt = 0;
+    if (mine) {
+      uint32_t c = excl;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (c + h[j] >= *need) { digit = lane * 8 + j; before = c; cnt = h[j]; break; }
+        c += h[j];
+      }
+    }
+    digit = __shfl_sync(FULL, digit, src);
+    before = __shfl_sync(FULL, before, src);
+    last = __shfl_sync(FULL, cnt, src);
+    prefix |= digit << shift;
+    mask |= 255u << shift;
+    *need -= before;
+    __syncwarp();
+  }
+  *eq = last;
+  return prefix;
+}
+
+// Block-wide version (hist: 256 shared words; sh: 3 shared words).
+template <typename KeyOf>
+__device__ uint32_t block_select(int n, KeyOf key_of, uint32_t* hist, uint32_t* sh, uint32_t* need,
+                                 uint32_t* eq) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  uint32_t prefix = 0, mask = 0;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (int i = tid; i < n; i += blockDim.x) {
+      const uint32_t k = key_of(i);
+      if ((k & mask) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (tid < 32) {
+      uint32_t h[8], run = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) { h[j] = hist[lane * 8 + j]; run += h[j]; }
+      uint32_t incl = run;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const uint32_t excl = incl - run;
+      if (excl < *need && incl >= *need) {
+        uint32_t c = excl;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (c + h[j] >= *need) { sh[0] = lane * 8 + j; sh[1] = c; sh[2] = h[j]; break; }
+          c += h[j];
+        }
+      }
+    }
+    __syncthreads();
+    prefix |= sh[0] << shift;
+    mask |= 255u << shift;
+    *need -= sh[1];
+    *eq = sh[2];
+    __syncthreads();
+  }
+  return prefix;
+}
+
+// One warp's buffer down to exactly min(cnt, k) entries by (dist key, id);
+// the k-th key becomes the warp's threshold and is published to s_thr64.
+__device__ __forceinline__ void warp_shrink(uint64_t* wb, int* cnt_io, uint32_t* thr, uint64_t* thr64,
+                                         uint32_t* hist, const int32_t* __restrict__ pids, int k,
+                                         unsigned long long* s_thr64) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  const int cnt = *cnt_io;
+  uint32_t need = (uint32_t)k, eq = 0;
+  const uint32_t kd = warp_select(cnt, [&](int i) { return (uint32_t)(wb[i] >> 32); }, hist, &need, &eq);
+  uint32_t kp;  // id of the k-th key among the entries with dist key kd
+  if (eq == need) {  // every tie is kept: the largest id among them
+    uint32_t mx = 0;
+    for (int i = lane; i < cnt; i += 32) {
+      const uint64_t v = wb[i];
+      if ((uint32_t)(v >> 32) == kd) mx = max(mx, (uint32_t)__ldg(pids + (uint32_t)v));
+    }
+    kp = __reduce_max_sync(FULL, mx);
+  } else {
+    uint32_t need2 = need, eq2;
+    kp = warp_select(cnt, [&](int i) {
+      const uint64_t v = wb[i];
+      return (uint32_t)(v >> 32) == kd ? (uint32_t)__ldg(pids + (uint32_t)v) : 0xffffffffu;
+    }, hist, &need2, &eq2);
+  }
+  int out = 0;
+  for (int i0 = 0; i0 < cnt; i0 += 32) {
+    const int i = i0 + lane;
+    const uint64_t v = i < cnt ? wb[i] : kKeyPad;
+    const uint32_t dk = (uint32_t)(v >> 32);
+    bool keep = i < cnt && dk <= kd;
+    if (keep && dk == kd) keep = (uint32_t)__ldg(pids + (uint32_t)v) <= kp;
+    const uint32_t bal = __ballot_sync(FULL, keep);
+    if (keep) wb[out + __popc(bal & lt_mask)] = v;
+    out += __popc(bal);
+  }
+  __syncwarp();
+  *cnt_io = out;
+  *thr = kd;
+  *thr64 = ((uint64_t)kd << 32) | kp;
+  if (lane == 0) atomicMin(s_thr64, (unsigned long long)*thr64);
+}
+
+template <int M, int D>
+__global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const IndexView& ix = a.ix;
+  float* lut = reinterpret_cast<float*>(dsm + SW_LUT);
+  float* ctab = reinterpret_cast<float*>(dsm + SW_CTAB);
+  float* qrot = reinterpret_cast<float*>(dsm + sw_qrot(M));
+  uint32_t* sstart = reinterpret_cast<uint32_t*>(dsm + SW_SSTART);
+  double* sbase = reinterpret_cast<double*>(dsm + SW_SBASE);
+  int32_t* soff = reinterpret_cast<int32_t*>(dsm + SW_SOFF);
+  uint64_t* merge = reinterpret_cast<uint64_t*>(dsm + SW_MERGE);
+  __shared__ int32_t red32[40];
+  __shared__ unsigned long long s_thr64;
+  __shared__ int s_nmerge, s_nout;
+  __shared__ uint32_t s_sel[4];
+
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  const int k = a.k;
+  build_lut_into(ix, a.Q + (int64_t)b * ix.d, lut, nullptr, qrot);
+  for (int i = tid; i < 256; i += SW_THREADS) ctab[i] = ix.ctab[i];
+  if (tid == 0) { s_thr64 = kKeyPad; s_nmerge = 0; }
+
+  uint64_t* wb = reinterpret_cast<uint64_t*>(dsm + SW_WBUF) + warp * SW_WB;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(merge) + warp * 256;
+  int cnt = 0;
+  uint32_t thr = 0xffffffffu;
+  uint64_t thr64 = kKeyPad;
+  const WorkItem* W = a.work + (int64_t)b * a.cap_w;
+  const int nseg = a.nwork[b];
+  uint64_t* fk = a.mode == 1 ? a.full_keys + (int64_t)b * a.cap_full_p2 : nullptr;
+  auto shrink = [&]() { warp_shrink(wb, &cnt, &thr, &thr64, hist, ix.pids, k, &s_thr64); };
+
+  struct Slot {  // one batch position of a lane
+    uint32_t row;
+    double base;
+    CodeVec<M> code;
+    uint32_t cb;
+    bool ok;
+  };
+
+  int64_t pos_base = 0;
+  for (int s0 = 0; s0 < nseg; s0 += SW_SEGS) {
+    const int ns = min(SW_SEGS, nseg - s0);
+    __syncthreads();  // the previous window's readers are done (first: LUT ready)
+    // SW_SEGS / SW_THREADS consecutive segments per thread
+    constexpr int SPT = SW_SEGS / SW_THREADS;
+    static_assert(SPT * SW_THREADS == SW_SEGS, "window = whole segments per thread");
+    int lens[SPT], mine = 0;
+#pragma unroll
+    for (int j = 0; j < SPT; ++j) {
+      const int i = SPT * tid + j;
+      lens[j] = 0;
+      if (i < ns) {
+        const WorkItem w = W[s0 + i];
+        sstart[i] = (uint32_t)w.start;
+        sbase[i] = w.base;
+        lens[j] = w.len;
+      }
+      mine += lens[j];
+    }
+    int tot;
+    int off = block_exclusive_scan(mine, red32, &tot);
+#pragma unroll
+    for (int j = 0; j < SPT; ++j) {
+      const int i = SPT * tid + j;
+      soff[i] = i < ns ? off : INT_MAX;
+      off += lens[j];
+    }
+    if (tid < 32) soff[SW_SEGS + tid] = INT_MAX;
+    __syncthreads();
+    const int pb = (int)((int64_t)tot * warp / SW_WARPS);
+    const int pe = (int)((int64_t)tot * (warp + 1) / SW_WARPS);
+    if (pb < pe) {
+      int s_cur;
+      {
+        int lo = 0, hi = ns - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (soff[mid] <= pb) lo = mid; else hi = mid - 1;
+        }
+        s_cur = lo;
+      }
+      // positions p0 .. p0+31 -> (segment, row); advances s_cur past the batch
+      auto map = [&](int p0, Slot& sl) {
+        const int nxt = soff[s_cur + 1 + lane];
+        const int rel = nxt - p0;
+        const uint32_t bit = (rel >= 1 && rel <= 31) ? (1u << rel) : 0u;
+        const uint32_t starts = __reduce_or_sync(FULL, bit);
+        const int seg = s_cur + __popc(starts & (FULL >> (31 - lane)));
+        const int p = p0 + lane;
+        sl.ok = p < pe;
+        // loads are issued unconditionally (a valid row for lanes past the
+        // end) so no later instruction has to wait for them to merge values
+        const uint32_t r = sstart[seg] + (uint32_t)(p - soff[seg]);
+        sl.row = sl.ok ? r : sstart[s_cur];
+        sl.base = sbase[seg];
+        sl.code = load_code<M>(ix.codes, sl.row);
+        sl.cb = __ldg(ix.cbytes + sl.row);
+        const int nst = __popc(starts);
+        const int at32 = __shfl_sync(FULL, nxt, nst);
+        s_cur += nst + (at32 - p0 == 32 ? 1 : 0);
+      };
+      auto process = [&](const Slot& cur, int p0) {
+        float dist = 0.f;
+        if (cur.ok) {
+          const float ip = code_sum<M>(cur.code, lut);
+          dist = (float)dadd(dsub(cur.base, 2.0 * (double)ip), (double)ctab[cur.cb]);
+        }
+        if (a.mode == 1) {
+          if (cur.ok) fk[pos_base + p0 + lane] = dist_id_key(dist, __ldg(ix.pids + cur.row));
+          return;
+        }
+        const uint32_t dk = f32_key(dist);
+        bool pass = cur.ok && dk <= thr;
+        if (pass && dk == thr && thr64 != kKeyPad)
+          pass = (((uint64_t)dk << 32) | (uint32_t)__ldg(ix.pids + cur.row)) < thr64;
+        const uint32_t bal = __ballot_sync(FULL, pass);
+        if (bal) {
+          if (pass) wb[cnt + __popc(bal & lt_mask)] = ((uint64_t)dk << 32) | cur.row;
+          cnt += __popc(bal);
+        }
+      };
+      // D batches in flight: the loads of the next D-1 overlap the sums of
+      // the current one
+      Slot sl[D];
+#pragma unroll
+      for (int i = 0; i < D - 1; ++i) map(pb + 32 * i, sl[i]);
+      for (int p0 = pb; p0 < pe; p0 += 32 * D) {
+        if (a.mode == 0) {  // adopt a tighter bound from the other warps
+          const uint64_t t = *(volatile unsigned long long*)&s_thr64;
+          if (t < thr64) { thr64 = t; thr = (uint32_t)(t >> 32); }
+        }
+#pragma unroll
+        for (int i = 0; i < D; ++i) {  // batches past pe are all-invalid no-ops
+          map(p0 + 32 * (i + D - 1), sl[(i + D - 1) % D]);
+          process(sl[i], p0 + 32 * i);
+        }
+        // <= D x 32 appends per iteration: room is kept for them
+        if (cnt > SW_WB - 32 * D) {
+          __syncwarp();
+          shrink();
+        }
+      }
+    }
+    pos_base += tot;
+  }
+  if (a.mode == 1) return;
+
+  // ---- final: every warp down to <= k entries with resolved ids
+  __syncwarp();
+  if (cnt > k) shrink();
+  for (int i = lane; i < cnt; i += 32) {
+    const uint64_t v = wb[i];
+    wb[i] = (v & 0xffffffff00000000ull) | (uint32_t)__ldg(ix.pids + (uint32_t)v);
+  }
+  __syncwarp();
+  if (cnt == k) {  // this warp's k-th key bounds the final top-k
+    uint64_t mx = 0;
+    for (int i = lane; i < cnt; i += 32) mx = max(mx, (uint64_t)wb[i]);
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, (uint64_t)__shfl_xor_sync(FULL, mx, o));
+    if (lane == 0) atomicMin(&s_thr64, (unsigned long long)mx);
+  }
+  __syncthreads();
+  const uint64_t T = s_thr64;
+  for (int i0 = 0; i0 < cnt; i0 += 32) {
+    const int i = i0 + lane;
+    const uint64_t v = i < cnt ? wb[i] : kKeyPad;
+    const bool keep = i < cnt && v <= T;
+    const uint32_t bal = __ballot_sync(FULL, keep);
+    int base = 0;
+    if (lane == 0 && bal) base = atomicAdd(&s_nmerge, __popc(bal));
+    base = __shfl_sync(FULL, base, 0);
+    if (keep) merge[base + __popc(bal & lt_mask)] = v;
+  }
+  __syncthreads();
+  // exactly min(nm, k) smallest by (dist, id), then one small sort
+  const int nm = s_nmerge;
+  uint64_t* fin = merge;
+  int nf = nm;
+  if (nm > k) {
+    uint32_t* bh = reinterpret_cast<uint32_t*>(sstart);  // free after the sweeps
+    uint32_t need = (uint32_t)k, eq = 0;
+    const uint32_t kd = block_select(nm, [&](int i) { return (uint32_t)(merge[i] >> 32); }, bh,
+                                     s_sel, &need, &eq);
+    uint32_t kp = 0xffffffffu;
+    if (eq != need) {
+      uint32_t eq2;
+      kp = block_select(nm, [&](int i) {
+        const uint64_t v = merge[i];
+        return (uint32_t)(v >> 32) == kd ? (uint32_t)v : 0xffffffffu;
+      }, bh, s_sel, &need, &eq2);
+    }
+    const uint64_t lim = ((uint64_t)kd << 32) | kp;
+    fin = reinterpret_cast<uint64_t*>(dsm + SW_WBUF);  // free after the warp phase
+    if (tid == 0) s_nout = 0;
+    __syncthreads();
+    for (int i0 = 0; i0 < nm; i0 += SW_THREADS) {
+      const int i = i0 + tid;
+      const bool keep = i < nm && merge[i] <= lim;
+      const uint32_t bal = __ballot_sync(FULL, keep);
+      int base = 0;
+      if (lane == 0 && bal) base = atomicAdd(&s_nout, __popc(bal));
+      base = __shfl_sync(FULL, base, 0);
+      if (keep) fin[base + __popc(bal & lt_mask)] = merge[i];
+    }
+    __syncthreads();
+    nf = s_nout;
+  }
+  const uint32_t np2 = next_pow2((uint32_t)max(nf, 1));
+  for (uint32_t i = nf + tid; i < np2; i += SW_THREADS) fin[i] = kKeyPad;
+  __syncthreads();
+  bitonic_sort_keys(fin, np2);
+  for (int i = tid; i < k; i += SW_THREADS) {
+    int32_t id = -1;
+    float dv = __int_as_float(0x7f800000);
+    if (i < nf) {
+      const uint64_t key = fin[i];
+      id = (int32_t)(uint32_t)key;
+      dv = key_f32((uint32_t)(key >> 32));
+    }
+    a.out_ids[(int64_t)b * k + i] = id;
+    a.out_d[(int64_t)b * k + i] = dv;
+  }
+}
+
+template <int M, int D>
+static void launch_warp_md(const ScanArgs& a, cudaStream_t s) {
+  const size_t bytes = sw_bytes(M, a.ix.d);
+  static size_t attr = 0;
+  if (attr < bytes) {
+    cudaFuncSetAttribute(k_scan_warp<M, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    attr = bytes;
+  }
+  k_scan_warp<M, D><<<a.nq, SW_THREADS, bytes, s>>>(a);
+}
+
+// batches in flight per warp (GIVF_SCAN_DEPTH, default 2)
+static int scan_depth() {
+  static int d = [] {
+    const char* e = getenv("GIVF_SCAN_DEPTH");
+    const int v = e ? atoi(e) : 2;
+    return (v == 3 || v == 4) ? v : 2;
+  }();
+  return d;
+}
+
+template <int M>
+static void launch_warp_m(const ScanArgs& a, cudaStream_t s) {
+  switch (scan_depth()) {
+    case 3: launch_warp_md<M, 3>(a, s); break;
+    case 4: launch_warp_md<M, 4>(a, s); break;
+    default: launch_warp_md<M, 2>(a, s); break;
+  }
+}
+
+bool launch_scan_warp(const ScanArgs& a, cudaStream_t s) {
+  if (a.mode == 0 && (a.k > SW_KMAX || a.k < 1)) return false;
+  if (a.ix.n >= (int64_t)1 << 32) return false;
+  switch (a.ix.M) {  // M a multiple of 4: cp.async-able code rows
+    case 4: launch_warp_m<4>(a, s); return true;
+    case 8: launch_warp_m<8>(a, s); return true;
+    case 12: launch_warp_m<12>(a, s); return true;
+    case 16: launch_warp_m<16>(a, s); return true;
+    case 24: launch_warp_m<24>(a, s); return true;
+    case 32: launch_warp_m<32>(a, s); return true;
+    default: return false;
+  }
+}
+
+}  // namespace givf
