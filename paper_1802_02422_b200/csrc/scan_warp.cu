@@ -13,7 +13,9 @@
 //    of the j-th following segment, one redux.or turns those into a bitmask
 //    of segment starts inside the batch, and popc(mask below l) is the
 //    lane's segment offset.  Code rows of consecutive positions are mostly
-//    consecutive, so code / constant-byte loads stay coalesced.
+//    consecutive, so code / constant-byte loads stay coalesced; they are
+//    staged by cp.async into a per-warp shared-memory ring (no register
+//    copies waiting on loads) while the previous batch is summed.
 //  * top-k: each warp keeps its own candidate buffer (dist key, row) and
 //    shrinks it with a warp radix select to exactly k by (dist, id).  The
 //    smallest k-th key over warps is shared (atomicMin in shared memory) and
@@ -21,14 +23,14 @@
 //  * The final merge takes the <= 8k entries under the shared bound, selects
 //    exactly k of them with a block radix select and sorts only those.
 //
-// Used for M in {4, 8, 12, 16, 24, 32}, k <= SW_KMAX and local row indices < 2^32;
-// k_scan covers
-// everything else.
+// Used for M in {4, 8, 12, 16, 24, 32}, k <= SW_KMAX and local row indices
+// < 2^32; k_scan covers everything else.
 #include "common.cuh"
 #include "kernels.h"
 #include "scan_common.cuh"
 
 #include <cstdlib>
+#include <cstring>
 
 namespace givf {
 
@@ -48,9 +50,53 @@ constexpr size_t SW_SBASE = SW_SSTART + (size_t)SW_SEGS * 4;      // f64 [SEGS]
 constexpr size_t SW_SOFF = SW_SBASE + (size_t)SW_SEGS * 8;        // i32 [SEGS + 32]
 constexpr size_t SW_CTAB = SW_SOFF + (size_t)(SW_SEGS + 32) * 4;  // f32 [256]
 constexpr size_t SW_LUT = SW_CTAB + 256 * 4;                      // f32 [M][256]
-__host__ __device__ constexpr size_t sw_qrot(int M) { return SW_LUT + (size_t)M * 1024; }
-__host__ __device__ constexpr size_t sw_bytes(int M, int d) {
-  return sw_qrot(M) + (((size_t)d * 4 + 15) & ~(size_t)15);
+// cp.async staging (CPA): per warp D slots x 32 lanes x (M code bytes + the
+// 4-byte word holding the constant byte)
+__host__ __device__ constexpr size_t sw_slot(int M) { return (size_t)32 * (M + 4); }
+__host__ __device__ constexpr size_t sw_ring(int M) { return SW_LUT + (size_t)M * 1024; }
+__host__ __device__ constexpr size_t sw_qrot(int M, int D, bool cpa) {
+  return sw_ring(M) + (cpa ? (size_t)SW_WARPS * D * sw_slot(M) : 0);
+}
+__host__ __device__ constexpr size_t sw_bytes(int M, int D, bool cpa, int d) {
+  return sw_qrot(M, D, cpa) + (((size_t)d * 4 + 15) & ~(size_t)15);
+}
+
+GIVF_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+template <int N>
+GIVF_DEV void cp_async(void* dst, const void* src) {
+  if constexpr (N == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(smem_u32(dst)), "l"(src), "n"(N)
+                 : "memory");
+}
+GIVF_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+GIVF_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+template <int M>
+constexpr int cp_chunk() { return M % 16 == 0 ? 16 : (M % 8 == 0 ? 8 : 4); }
+
+// code row of M bytes (M % 4 == 0) from shared memory
+template <int M>
+GIVF_DEV CodeVec<M> smem_code(const uint8_t* p) {
+  CodeVec<M> v;
+  if constexpr (M % 16 == 0) {
+#pragma unroll
+    for (int i = 0; i < M / 16; ++i) {
+      const uint4 x = reinterpret_cast<const uint4*>(p)[i];
+      v.w[4 * i] = x.x; v.w[4 * i + 1] = x.y; v.w[4 * i + 2] = x.z; v.w[4 * i + 3] = x.w;
+    }
+  } else if constexpr (M % 8 == 0) {
+#pragma unroll
+    for (int i = 0; i < M / 8; ++i) {
+      const uint2 x = reinterpret_cast<const uint2*>(p)[i];
+      v.w[2 * i] = x.x; v.w[2 * i + 1] = x.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < M / 4; ++i) v.w[i] = reinterpret_cast<const uint32_t*>(p)[i];
+  }
+  return v;
 }
 
 // Warp radix select: the digit-by-digit search for the need-th smallest of
@@ -191,13 +237,13 @@ __device__ __forceinline__ void warp_shrink(uint64_t* wb, int* cnt_io, uint32_t*
   if (lane == 0) atomicMin(s_thr64, (unsigned long long)*thr64);
 }
 
-template <int M, int D>
+template <int M, int U, bool CPA>
 __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
   extern __shared__ __align__(16) unsigned char dsm[];
   const IndexView& ix = a.ix;
   float* lut = reinterpret_cast<float*>(dsm + SW_LUT);
   float* ctab = reinterpret_cast<float*>(dsm + SW_CTAB);
-  float* qrot = reinterpret_cast<float*>(dsm + sw_qrot(M));
+  float* qrot = reinterpret_cast<float*>(dsm + sw_qrot(M, 2 * U, CPA));
   uint32_t* sstart = reinterpret_cast<uint32_t*>(dsm + SW_SSTART);
   double* sbase = reinterpret_cast<double*>(dsm + SW_SBASE);
   int32_t* soff = reinterpret_cast<int32_t*>(dsm + SW_SOFF);
@@ -224,7 +270,8 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
   uint64_t* fk = a.mode == 1 ? a.full_keys + (int64_t)b * a.cap_full_p2 : nullptr;
   auto shrink = [&]() { warp_shrink(wb, &cnt, &thr, &thr64, hist, ix.pids, k, &s_thr64); };
 
-  struct Slot {  // one batch position of a lane
+  uint8_t* ring = dsm + sw_ring(M) + (size_t)warp * 2 * U * sw_slot(M);
+  struct Slot {  // one batch position of a lane (CPA: code and cb in the ring)
     uint32_t row;
     double base;
     CodeVec<M> code;
@@ -275,7 +322,7 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
         s_cur = lo;
       }
       // positions p0 .. p0+31 -> (segment, row); advances s_cur past the batch
-      auto map = [&](int p0, Slot& sl) {
+      auto map = [&](int p0, Slot& sl, int slot) {
         const int nxt = soff[s_cur + 1 + lane];
         const int rel = nxt - p0;
         const uint32_t bit = (rel >= 1 && rel <= 31) ? (1u << rel) : 0u;
@@ -288,18 +335,38 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
         const uint32_t r = sstart[seg] + (uint32_t)(p - soff[seg]);
         sl.row = sl.ok ? r : sstart[s_cur];
         sl.base = sbase[seg];
-        sl.code = load_code<M>(ix.codes, sl.row);
-        sl.cb = __ldg(ix.cbytes + sl.row);
+        if constexpr (CPA) {
+          uint8_t* dst = ring + slot * sw_slot(M);
+          constexpr int CH = cp_chunk<M>();
+          const uint8_t* src = ix.codes + (size_t)sl.row * M;
+#pragma unroll
+          for (int c = 0; c < M / CH; ++c) cp_async<CH>(dst + lane * M + c * CH, src + c * CH);
+          cp_async<4>(dst + 32 * M + lane * 4, ix.cbytes + (sl.row & ~3u));
+          cp_async_commit();
+        } else {
+          sl.code = load_code<M>(ix.codes, sl.row);
+          sl.cb = __ldg(ix.cbytes + sl.row);
+        }
         const int nst = __popc(starts);
         const int at32 = __shfl_sync(FULL, nxt, nst);
         s_cur += nst + (at32 - p0 == 32 ? 1 : 0);
       };
-      auto process = [&](const Slot& cur, int p0) {
-        float dist = 0.f;
-        if (cur.ok) {
-          const float ip = code_sum<M>(cur.code, lut);
-          dist = (float)dadd(dsub(cur.base, 2.0 * (double)ip), (double)ctab[cur.cb]);
+      auto dist_of = [&](const Slot& cur, int slot) -> float {
+        CodeVec<M> code;
+        uint32_t cb;
+        if constexpr (CPA) {
+          const uint8_t* src = ring + slot * sw_slot(M);
+          code = smem_code<M>(src + lane * M);
+          const uint32_t cw = reinterpret_cast<const uint32_t*>(src + 32 * M)[lane];
+          cb = (cw >> ((cur.row & 3u) * 8)) & 0xffu;
+        } else {
+          code = cur.code;
+          cb = cur.cb;
         }
+        const float ip = code_sum<M>(code, lut);
+        return (float)dadd(dsub(cur.base, 2.0 * (double)ip), (double)ctab[cb]);
+      };
+      auto consider = [&](const Slot& cur, float dist, int p0) {
         if (a.mode == 1) {
           if (cur.ok) fk[pos_base + p0 + lane] = dist_id_key(dist, __ldg(ix.pids + cur.row));
           return;
@@ -314,20 +381,28 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
           cnt += __popc(bal);
         }
       };
-      // D batches in flight: the loads of the next D-1 overlap the sums of
-      // the current one
+      // Two groups of U batches: one group's loads are in flight while the
+      // other's U independent sums are computed (interleaved by the compiler).
+      constexpr int D = 2 * U;
       Slot sl[D];
 #pragma unroll
-      for (int i = 0; i < D - 1; ++i) map(pb + 32 * i, sl[i]);
+      for (int i = 0; i < U; ++i) map(pb + 32 * i, sl[i], i);
       for (int p0 = pb; p0 < pe; p0 += 32 * D) {
         if (a.mode == 0) {  // adopt a tighter bound from the other warps
           const uint64_t t = *(volatile unsigned long long*)&s_thr64;
           if (t < thr64) { thr64 = t; thr = (uint32_t)(t >> 32); }
         }
 #pragma unroll
-        for (int i = 0; i < D; ++i) {  // batches past pe are all-invalid no-ops
-          map(p0 + 32 * (i + D - 1), sl[(i + D - 1) % D]);
-          process(sl[i], p0 + 32 * i);
+        for (int h = 0; h < 2; ++h) {  // batches past pe are all-invalid no-ops
+          const int cur = h * U, nxt = (1 - h) * U;
+#pragma unroll
+          for (int i = 0; i < U; ++i) map(p0 + 32 * (U * (h + 1) + i), sl[nxt + i], nxt + i);
+          if constexpr (CPA) cp_async_wait<U>();  // the current group landed
+          float dv[U];
+#pragma unroll
+          for (int i = 0; i < U; ++i) dv[i] = dist_of(sl[cur + i], cur + i);
+#pragma unroll
+          for (int i = 0; i < U; ++i) consider(sl[cur + i], dv[i], p0 + 32 * (cur + i));
         }
         // <= D x 32 appends per iteration: room is kept for them
         if (cnt > SW_WB - 32 * D) {
@@ -335,6 +410,7 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
           shrink();
         }
       }
+      if constexpr (CPA) cp_async_wait<0>();  // prefetches past pe
     }
     pos_base += tot;
   }
@@ -417,34 +493,50 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
   }
 }
 
-template <int M, int D>
+template <int M, int U, bool CPA>
 static void launch_warp_md(const ScanArgs& a, cudaStream_t s) {
-  const size_t bytes = sw_bytes(M, a.ix.d);
+  const size_t bytes = sw_bytes(M, 2 * U, CPA, a.ix.d);
   static size_t attr = 0;
   if (attr < bytes) {
-    cudaFuncSetAttribute(k_scan_warp<M, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaFuncSetAttribute(k_scan_warp<M, U, CPA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)bytes);
     attr = bytes;
   }
-  k_scan_warp<M, D><<<a.nq, SW_THREADS, bytes, s>>>(a);
+  k_scan_warp<M, U, CPA><<<a.nq, SW_THREADS, bytes, s>>>(a);
 }
 
-// batches in flight per warp (GIVF_SCAN_DEPTH, default 2)
-static int scan_depth() {
-  static int d = [] {
-    const char* e = getenv("GIVF_SCAN_DEPTH");
-    const int v = e ? atoi(e) : 2;
-    return (v == 3 || v == 4) ? v : 2;
+// Batches summed together per warp (GIVF_SCAN_GROUP, default 1; twice that
+// many in flight) and how code rows are staged (default: cp.async into a
+// per-warp shared-memory ring; GIVF_SCAN_STAGE=registers: plain loads).
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+static int scan_group() {  // batches summed together (GIVF_SCAN_GROUP: 1, 2, 4)
+  static int u = [] { const int v = env_int("GIVF_SCAN_GROUP", 1); return (v == 2 || v == 4) ? v : 1; }();
+  return u;
+}
+static bool scan_cpa() {  // measured faster on C2: the default
+  static bool c = [] {
+    const char* e = getenv("GIVF_SCAN_STAGE");
+    return !(e && strcmp(e, "registers") == 0);
   }();
-  return d;
+  return c;
+}
+
+template <int M, bool CPA>
+static void launch_warp_mc(const ScanArgs& a, cudaStream_t s) {
+  switch (scan_group()) {
+    case 2: launch_warp_md<M, 2, CPA>(a, s); break;
+    case 4: launch_warp_md<M, 4, CPA>(a, s); break;
+    default: launch_warp_md<M, 1, CPA>(a, s); break;
+  }
 }
 
 template <int M>
 static void launch_warp_m(const ScanArgs& a, cudaStream_t s) {
-  switch (scan_depth()) {
-    case 3: launch_warp_md<M, 3>(a, s); break;
-    case 4: launch_warp_md<M, 4>(a, s); break;
-    default: launch_warp_md<M, 2>(a, s); break;
-  }
+  if (scan_cpa()) launch_warp_mc<M, true>(a, s);
+  else launch_warp_mc<M, false>(a, s);
 }
 
 bool launch_scan_warp(const ScanArgs& a, cudaStream_t s) {
