@@ -30,6 +30,9 @@ _EXPORTS = {
     "ShardedIndex": ".sharded",
     "GivfError": ".errors",
     "InvariantError": ".errors",
+    "StorageError": ".errors",
+    "load_index": ".storage",
+    "save_index": ".storage",
 }
 
 __all__ = sorted(_EXPORTS) + ["__version__"]

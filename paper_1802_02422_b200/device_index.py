@@ -36,6 +36,7 @@ class IndexArrays:
     const_lo: float
     const_hi: float
     grouping: bool
+    meta: object = None              # storage.FileMeta when read from a .givf file
 
     @property
     def k(self) -> int:

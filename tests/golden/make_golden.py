@@ -166,8 +166,28 @@ def fixture_c1like(m, name, rotation=False, d=96, k=256, l=16, nq=16):
     save(name, ix, queries, grid, f"C1-family d={d} K={k} L={l} M={m} rotation={rotation}")
 
 
+def fixture_givf():
+    """The conftest-world indexes (same seeds as fixture_small) written by the
+    reference's own save_index (storage.py:114-127): byte-level fixtures for
+    the .givf reader/writer.  Their arrays equal those stored in the .npz."""
+    from givf.storage import save_index
+
+    data = synth_clustered(12_000, 16, 60, spread=0.4, seed=11)
+    base, learn = data[:10_000], data[10_000:11_900]
+    coarse = train_kmeans(learn, 48, iters=8, seed=5)
+    graph = build_graph(coarse, max_links=8, ef_construction=48, seed=derive_seed(5, "graph"))
+    for name, grouping in (("small_grouped", True), ("small_flat", False)):
+        ix = build_index(base, coarse, graph, learn, l=6, m=4, grouping=grouping, seed=5)
+        ref = np.load(os.path.join(OUT, f"{name}.npz"))
+        for key, val in index_arrays(ix).items():
+            assert np.array_equal(ref[key], val), (name, key)
+        path = os.path.join(OUT, f"{name}.givf")
+        size = save_index(ix, path)
+        print(f"{name}.givf: {size} bytes", flush=True)
+
+
 def main():
-    which = sys.argv[1:] or ["small", "kat", "m8", "m16", "rot"]
+    which = sys.argv[1:] or ["small", "kat", "m8", "m16", "rot", "givf"]
     if "small" in which:
         fixture_small()
     if "kat" in which:
@@ -178,6 +198,8 @@ def main():
         fixture_c1like(16, "c1like_m16")
     if "rot" in which:
         fixture_c1like(8, "rot_m8", rotation=True, d=32, k=64, l=8, nq=10)
+    if "givf" in which:
+        fixture_givf()
 
 
 if __name__ == "__main__":
