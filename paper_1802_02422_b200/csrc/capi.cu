@@ -242,12 +242,14 @@ int scan_mode() {
 
 int nstreams_default() {
   const char* s = getenv("GIVF_STREAMS");
-  return std::max(1, std::min(8, s ? atoi(s) : 2));
+  // measured on C2 with the current kernels: one stream and the largest
+  // chunks win (every stage fills the GPU on its own)
+  return std::max(1, std::min(8, s ? atoi(s) : 1));
 }
 
 size_t workspace_budget() {
   const char* s = getenv("GIVF_WORKSPACE_MB");
-  size_t mb = s ? (size_t)atoll(s) : 4096;
+  size_t mb = s ? (size_t)atoll(s) : 8192;
   return std::max<size_t>(mb, 64) << 20;
 }
 
@@ -438,6 +440,8 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
   if (const char* e = getenv("GIVF_CHUNK_QUERIES")) chunk = std::max<int64_t>(1, atoll(e));
   chunk = std::max<int64_t>(1, std::min<int64_t>(chunk, nq));
   chunk = std::min<int64_t>(chunk, 65535);
+  // equal chunks (no small tail chunk that leaves the GPU half empty)
+  chunk = (nq + (nq + chunk - 1) / chunk - 1) / ((nq + chunk - 1) / chunk);
   const int64_t nchunks = (nq + chunk - 1) / chunk;
   ns = (int)std::min<int64_t>(ns, nchunks);
   const size_t slice = ((fixed + per_q * (size_t)chunk + (1 << 20)) + 4095) & ~(size_t)4095;

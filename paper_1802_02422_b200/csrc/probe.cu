@@ -422,8 +422,7 @@ k_probe_full(const float* __restrict__ Q, const float* __restrict__ C, int nq, i
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
   const bool f32diff = mode == 0;
 
-  for (int b = blockIdx.x; b < nq; b += gridDim.x) {
-    if (mode == 1 && fail[b] == 0) continue;
+  auto one = [&](int b) {
     const float* q = Q + (int64_t)b * d;
     for (int j = threadIdx.x; j < d; j += blockDim.x) { qf[j] = q[j]; qd[j] = (double)q[j]; }
     __syncthreads();
@@ -435,6 +434,25 @@ k_probe_full(const float* __restrict__ Q, const float* __restrict__ C, int nq, i
     __syncthreads();
     bitonic_sort(key, val, kp2);
     emit_probe(key, val, P, !f32diff, k2, v2, dv, regions + (int64_t)b * P, qc2 + (int64_t)b * P);
+    __syncthreads();
+  };
+  if (mode == 0) {
+    for (int b = blockIdx.x; b < nq; b += gridDim.x) one(b);
+    return;
+  }
+  // fallback mode: the flags of blockDim.x queries are read at once and only
+  // the flagged ones are redone
+  __shared__ int s_list[1024];
+  __shared__ int s_n;
+  for (int64_t b0 = blockIdx.x; b0 < nq; b0 += (int64_t)gridDim.x * blockDim.x) {
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    const int64_t b = b0 + (int64_t)threadIdx.x * gridDim.x;
+    if (b < nq && fail[b] != 0) s_list[atomicAdd(&s_n, 1)] = (int)b;
+    __syncthreads();
+    const int n = s_n;
+    for (int i = 0; i < n; ++i) one(s_list[i]);
+    __syncthreads();
   }
 }
 

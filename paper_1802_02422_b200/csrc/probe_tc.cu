@@ -15,9 +15,11 @@
 //           in smem), then B chunks of 256 x 64 through a 4-stage ring
 //   warp 1  TMEM allocator + single-thread tcgen05.mma issuer; commits free
 //           the B stages and publish finished accumulators
-//   warps 2-5  epilogue: tcgen05.ld 32x32b.x32 of the fp32 accumulator
-//           (double-buffered: 2 x 256 TMEM columns), s~ = c2 - 2 acc, rows
-//           of s~ to global + the minimum of every 128-centroid half tile
+//   warps 2-9  epilogue: two warps per TMEM lane quarter, each owning one
+//           128-column half of the accumulator (double-buffered: 2 x 256
+//           TMEM columns); tcgen05.ld 32x32b.x32 of the next 32 columns is in
+//           flight while the current ones become s~ = c2 - 2 acc, go out by
+//           TMA store, and fold into the minimum of the 128-centroid tile
 // Operands use the SWIZZLE_128B K-major canonical layout written by TMA.
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -34,9 +36,10 @@ namespace tc {
 
 constexpr int BM = 128, BN = 256, BK = 64;  // BK bf16 = 128 B = one swizzle row
 constexpr int STAGES = 3;
-// epilogue smem: TMA-store staging (4 warps x 2 x 4 KB) + per-warp |c|^2 tile
-constexpr uint32_t STAGE_OUT = 4 * 2 * 4096 + 4 * 256 * 4;
-constexpr int THREADS = 192;
+constexpr int EPI_WARPS = 8;  // two per TMEM lane quarter, one 128-column half each
+// epilogue smem: TMA-store staging (one 4 KB tile per warp) + per-warp |c|^2
+constexpr uint32_t STAGE_OUT = EPI_WARPS * 4096 + EPI_WARPS * 128 * 4;
+constexpr int THREADS = 64 + 32 * EPI_WARPS;
 constexpr uint32_t A_CHUNK = BM * BK * 2;   // 16 KB
 constexpr uint32_t B_CHUNK = BN * BK * 2;   // 32 KB
 constexpr int TMEM_COLS = 512;              // two 256-column fp32 accumulators
@@ -123,6 +126,33 @@ GIVF_DEV void tmem_ld32(uint32_t taddr, uint32_t* r) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// Asynchronous variant: the registers are valid only after tmem_wait_ld(r),
+// which names them so no use can be scheduled before the wait.
+GIVF_DEV void tmem_ld32_async(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+}
+GIVF_DEV void tmem_wait_ld(uint32_t* r) {
+  asm volatile(
+      "tcgen05.wait::ld.sync.aligned;"
+      : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]),
+        "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]),
+        "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]),
+        "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]),
+        "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+      :
+      : "memory");
+}
+
 struct Smem {
   uint64_t full[STAGES], empty[STAGES];
   uint64_t a_full, a_empty;
@@ -156,7 +186,10 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
     for (int s = 0; s < STAGES; ++s) { mbar_init(&sm->full[s], 1); mbar_init(&sm->empty[s], 1); }
     mbar_init(&sm->a_full, 1);
     mbar_init(&sm->a_empty, 1);
-    for (int a = 0; a < 2; ++a) { mbar_init(&sm->tm_full[a], 1); mbar_init(&sm->tm_empty[a], 4); }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&sm->tm_full[a], 1);
+      mbar_init(&sm->tm_empty[a], EPI_WARPS);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0 && lane == 0) {
@@ -234,41 +267,48 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
       __syncwarp();
     }
   } else {
-    // ------------------------------------------------ epilogue (warps 2..5)
+    // ------------------------------------------------ epilogue (warps 2..9)
+    const int e = warp - 2;
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int half = e >> 2;       // 128-column half of the 256-column tile
     const int ntiles128 = (K + 127) / 128;
-    // per-warp double-buffered 32x32 fp32 staging tiles for the TMA store
-    // (SWIZZLE_128B: the 16-byte chunk k of row r sits at chunk k ^ (r & 7))
-    unsigned char* stage_base = smB + (size_t)STAGES * B_CHUNK + (size_t)(warp - 2) * 2 * 4096;
-    float* c2s = reinterpret_cast<float*>(smB + (size_t)STAGES * B_CHUNK + 4 * 2 * 4096) +
-                 (warp - 2) * BN;
-    uint32_t sbuf = 0;
+    // per-warp 32x32 fp32 staging tile for the TMA store (SWIZZLE_128B: the
+    // 16-byte chunk k of row r sits at chunk k ^ (r & 7))
+    unsigned char* sb = smB + (size_t)STAGES * B_CHUNK + (size_t)e * 4096;
+    float* c2s = reinterpret_cast<float*>(smB + (size_t)STAGES * B_CHUNK + EPI_WARPS * 4096) +
+                 e * 128;
     uint32_t acc = 0, acc_phase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int mb = u / nsplit, sp = u % nsplit;
       const int t0 = sp * per_split, t1 = min(n_tiles, t0 + per_split);
       const int q = mb * BM + quarter * 32 + lane;
       for (int t = t0; t < t1; ++t) {
-        // this tile's |c|^2 column terms: issued before the accumulator wait
-        // so their latency hides behind it, then kept in a per-warp smem copy
-        float c2r[BN / 32];
+        const int colh = t * BN + half * 128;
+        // this half tile's |c|^2 terms: loaded before the accumulator wait so
+        // their latency hides behind it, then kept in a per-warp smem copy
+        float c2r[4];
 #pragma unroll
-        for (int c = 0; c < BN / 32; ++c) {
-          const int col = t * BN + c * 32 + lane;
+        for (int c = 0; c < 4; ++c) {
+          const int col = colh + c * 32 + lane;
           c2r[c] = col < K ? __ldg(c2 + col) : 0.f;
         }
         mbar_wait(&sm->tm_full[acc], acc_phase);
         fence_after();
 #pragma unroll
-        for (int c = 0; c < BN / 32; ++c) c2s[c * 32 + lane] = c2r[c];
+        for (int c = 0; c < 4; ++c) c2s[c * 32 + lane] = c2r[c];
         __syncwarp();
         float* drow = D + (int64_t)q * ldD;
         float mn = __int_as_float(0x7f800000);
-#pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN + c * 32, r);
-          const int col0 = t * BN + c * 32;
+        const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN + half * 128;
+        uint32_t ra[32], rb[32];
+        tmem_ld32_async(tb, ra);
+        tmem_wait_ld(ra);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t* r = (c & 1) ? rb : ra;
+          uint32_t* rn = (c & 1) ? ra : rb;
+          if (c < 3) tmem_ld32_async(tb + (c + 1) * 32, rn);  // next chunk in flight
+          const int col0 = colh + c * 32;
           float v[32];
           if (col0 + 32 <= K) {
             const float4* c24 = reinterpret_cast<const float4*>(c2s + c * 32);
@@ -291,11 +331,9 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
 #pragma unroll
           for (int i = 0; i < 32; ++i) mn = fminf(mn, v[i]);
           if (use_tma_store) {
-            // wait until the store issued from this buffer two chunks ago has
-            // finished reading shared memory, then stage and issue
-            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            // the previous store from this staging tile has read it
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             __syncwarp();
-            unsigned char* sb = stage_base + sbuf * 4096;
 #pragma unroll
             for (int k = 0; k < 8; ++k)
               *reinterpret_cast<float4*>(sb + lane * 128 + ((k ^ (lane & 7)) * 16)) =
@@ -310,7 +348,6 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
                   : "memory");
               asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
-            sbuf ^= 1;
           } else if (q < nq) {
             if (col0 + 32 <= K) {
               float4* dst = reinterpret_cast<float4*>(drow + col0);
@@ -323,12 +360,10 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
                 if (col0 + i < K) drow[col0 + i] = v[i];
             }
           }
-          if ((c & 3) == 3) {  // finished one 128-centroid half tile
-            const int h = t * 2 + (c >> 2);
-            if (q < nq && tmin && h < ntiles128) tmin[(int64_t)q * ntiles128 + h] = mn;
-            mn = __int_as_float(0x7f800000);
-          }
+          if (c < 3) tmem_wait_ld(rn);
         }
+        const int h = t * 2 + half;  // this warp's 128-centroid tile
+        if (q < nq && tmin && h < ntiles128) tmin[(int64_t)q * ntiles128 + h] = mn;
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm->tm_empty[acc]);
