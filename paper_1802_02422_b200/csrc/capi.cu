@@ -247,6 +247,11 @@ int nstreams_default() {
   return std::max(1, std::min(8, s ? atoi(s) : 1));
 }
 
+int64_t probe_sub_default() {
+  const char* s = getenv("GIVF_PROBE_SUB");
+  return s ? std::max<int64_t>(0, atoll(s)) : 0;
+}
+
 size_t workspace_budget() {
   const char* s = getenv("GIVF_WORKSPACE_MB");
   size_t mb = s ? (size_t)atoll(s) : 8192;
@@ -413,8 +418,9 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
   const bool rerank = p->rerank != 0;
   const int64_t full_p2 = om == OUT_FULL ? (int64_t)next_pow2_host((uint32_t)std::max<int64_t>(width, 1)) : 0;
 
-  // per-query workspace
-  size_t per_q = aligned_bytes<float>(v.d) + probe_bytes_per_query(pl) +
+  // per-query workspace (the probe's part is sized by probe sub-chunk below)
+  const size_t probe_q = probe_bytes_per_query(pl);
+  size_t per_q = aligned_bytes<float>(v.d) +
                  2 * aligned_bytes<double>(pl.total) + aligned_bytes<int32_t>(pl.total) +
                  aligned_bytes<WorkItem>(pl.cap_w) + aligned_bytes<int>(1) +
                  aligned_bytes<int>(1) + aligned_bytes<int64_t>(4);
@@ -424,7 +430,12 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
   }
   if (om == OUT_FULL && rerank) per_q += (size_t)full_p2 * 8;
   if (!out_dev) per_q += (size_t)width * 8 + 512;
-  const size_t fixed = probe_fixed_bytes(pl) + (1 << 16);
+  // Probe sub-chunks (GIVF_PROBE_SUB queries): GEMM -> select -> recheck ->
+  // K3a run per sub-chunk so the fp32 score matrix D they share stays in L2
+  // instead of making three HBM round trips; 0 = one sub-chunk per chunk.
+  const int64_t sub_env = probe_sub_default();
+  const size_t fixed = probe_fixed_bytes(pl) + (1 << 16) + (sub_env ? probe_q * sub_env : 0);
+  if (!sub_env) per_q += probe_q;
   const size_t budget = workspace_budget();
   int64_t chunk = budget > fixed ? (int64_t)((budget - fixed) / per_q) : 1;
   // Keep one chunk's probe scores + plan scratch resident in the 126 MB L2:
@@ -470,10 +481,6 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
     }
     int* regions = ar.take<int>((size_t)bq * pl.P);
     double* qc2 = ar.take<double>((size_t)bq * pl.P);
-    const float* Dmat = nullptr;
-    float eps_scale = 0.f;
-    rc = run_probe(ix, pl, dQ, bq, regions, qc2, ar, st, &Dmat, &eps_scale);
-    if (rc) return rc;
 
     PlanArgs pa{};
     pa.ix = v;
@@ -499,14 +506,45 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
       pa.sval = ar.take<uint32_t>((size_t)bq * cp2);
       pa.order = ar.take<int32_t>((size_t)bq * pl.cap_w);
     }
-    pa.D = Dmat;
     pa.ldD = v.K;
     pa.cmax = v.cmax;
-    pa.eps_scale = eps_scale;
-    pa.only = Dmat ? ar.take<int>(bq) : nullptr;
+    pa.only = ar.take<int>(bq);
     // the approximate planner's keys alias the exact scratch, which the exact
     // kernels only write after the approximate planner has finished
     pa.akey = reinterpret_cast<uint32_t*>(pa.sbase);
+
+    // probe + K3a per sub-chunk; the probe workspace (D included) is reused
+    const size_t mark = ar.off;
+    const int64_t sub = sub_env ? std::min<int64_t>(sub_env, bq) : bq;
+    bool approx = true;
+    for (int64_t s0 = 0; s0 < bq; s0 += sub) {
+      const int ns_q = (int)std::min<int64_t>(sub, bq - s0);
+      ar.off = mark;
+      const float* Dmat = nullptr;
+      float eps_scale = 0.f;
+      rc = run_probe(ix, pl, dQ + s0 * v.d, ns_q, regions + s0 * pl.P, qc2 + s0 * pl.P, ar, st,
+                     &Dmat, &eps_scale);
+      if (rc) return rc;
+      pa.eps_scale = eps_scale;
+      if (!Dmat) {  // exhaustive probe (nprobe == K or too wide): exact planner only
+        approx = false;
+        continue;
+      }
+      PlanArgs sa = pa;
+      sa.Q = dQ + s0 * v.d;
+      sa.regions = regions + s0 * pl.P;
+      sa.qc2 = qc2 + s0 * pl.P;
+      sa.nq = ns_q;
+      sa.akey = pa.akey + s0 * pl.total;
+      sa.D = Dmat;
+      int nk = 0;
+      staged(ST_PLAN, st, [&] { nk = launch_plan_scores(sa, st); }, 0);
+      g_launches += nk;
+      KCHECK();
+    }
+    ar.off = mark;  // the probe workspace is dead once K3a has run (stream order)
+    pa.approx = approx ? 1 : 0;
+    pa.D = nullptr;
     int nk = 0;
     staged(ST_PLAN, st, [&] { nk = launch_plan(pa, st); }, 0);
     g_launches += nk;

@@ -96,12 +96,16 @@ struct PlanArgs {
   int* only;            // (nq) fallback flags: exact kernels run where only[b] != 0
   uint32_t* akey;       // (nq, P*G) scratch: float32 order key of the approximate score
   int defer_rescore;    // set by launch_plan_approx: base/score by k_plan_rescore
+  int approx;           // akey holds K3a's keys: run the approximate-first planner
 };
-// plan_approx.cu: approximate-first planner (sets only[b] for the queries it
-// cannot certify); returns kernels launched.
+// plan_approx.cu: K3a, the approximate group scores (needs D; may run per
+// probe sub-chunk while D is still in L2), then the approximate-first planner
+// (sets only[b] for the queries it cannot certify); both return kernels launched.
+int launch_plan_scores(const PlanArgs& a, cudaStream_t s);
 int launch_plan_approx(const PlanArgs& a, cudaStream_t s);
-// Launches the approximate-first planner (when a.D is set) followed by the
-// exact planner for the queries it could not certify; returns kernels launched.
+// Launches the approximate-first planner (when a.approx is set; K3a must have
+// run) followed by the exact planner for the queries it could not certify;
+// returns kernels launched.
 int launch_plan(const PlanArgs& a, cudaStream_t s);
 
 // scan.cu

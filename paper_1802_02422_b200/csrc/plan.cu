@@ -369,7 +369,7 @@ size_t plan_smem(int d) {
 
 int launch_plan(const PlanArgs& a, cudaStream_t s) {
   int n = 0;
-  if (a.D != nullptr && a.only != nullptr) {
+  if (a.approx && a.only != nullptr) {
     n += launch_plan_approx(a, s);  // flags the queries it cannot certify
     k_plan_score<<<a.nq, PLAN_THREADS, 0, s>>>(a);
     k_plan_select<<<a.nq, PLAN_THREADS, plan_smem(a.ix.d), s>>>(a);

@@ -624,13 +624,17 @@ int launch_plan_approx(const PlanArgs& a0, cudaStream_t s) {
     cudaFuncSetAttribute(k_plan_approx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
     attr = L.bytes;
   }
+  k_plan_approx<<<a.nq, PA_THREADS, L.bytes, s>>>(a);
+  if (!a.defer_rescore) return 1;
+  k_plan_rescore<<<dim3(a.nq, RS_SPLIT), RS_THREADS, (size_t)a.ix.d * 8, s>>>(a);
+  return 2;
+}
+
+int launch_plan_scores(const PlanArgs& a, cudaStream_t s) {
   const int64_t warps = (int64_t)a.nq * a.P;
   const int per = PA_THREADS / 32;
   k_plan_scores_approx<<<(unsigned)((warps + per - 1) / per), PA_THREADS, 0, s>>>(a);
-  k_plan_approx<<<a.nq, PA_THREADS, L.bytes, s>>>(a);
-  if (!a.defer_rescore) return 2;
-  k_plan_rescore<<<dim3(a.nq, RS_SPLIT), RS_THREADS, (size_t)a.ix.d * 8, s>>>(a);
-  return 3;
+  return 1;
 }
 
 }  // namespace givf

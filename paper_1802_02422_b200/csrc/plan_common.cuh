@@ -87,4 +87,55 @@ __device__ inline void group8_sqdist64_multi(const float* const* rows, const dou
   }
 }
 
+// The query's float64 coordinates this lane of an 8-lane group needs (float4
+// columns gl, gl + 8, gl + 16, gl + 24; d % 4 == 0, d <= 128), held in
+// registers across rows.
+struct QLane {
+  double v[4][4];
+};
+__device__ inline QLane load_qlane(const double* qd, int d4) {
+  const int gl = threadIdx.x & 7;
+  QLane q;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int j = gl + 8 * t;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) q.v[t][i] = j < d4 ? qd[4 * j + i] : 0.0;
+  }
+  return q;
+}
+
+// group8_sqdist64_multi with the query in registers (same arithmetic order).
+template <int U>
+__device__ inline void group8_sqdist64_multi_q(const float* const* rows, const QLane& q, int d4,
+                                               double* out) {
+  const int gl = threadIdx.x & 7;
+  float4 v[U][4];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int j = gl + 8 * t;
+      v[u][t] = j < d4 ? __ldg(reinterpret_cast<const float4*>(rows[u]) + j)
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    double s = 0.0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int j = gl + 8 * t;
+      if (j < d4) {
+        double t0 = dsub((double)v[u][t].x, q.v[t][0]), t1 = dsub((double)v[u][t].y, q.v[t][1]);
+        double t2 = dsub((double)v[u][t].z, q.v[t][2]), t3 = dsub((double)v[u][t].w, q.v[t][3]);
+        s = dadd(s, dadd(dadd(dmul(t0, t0), dmul(t1, t1)), dadd(dmul(t2, t2), dmul(t3, t3))));
+      }
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    out[u] = s;
+  }
+}
+
 }  // namespace givf

@@ -1,12 +1,14 @@
 #!/bin/bash
 # Round evidence on one B200: full bench line (with CPU baseline), reference
 # arm, per-launch kernel list, and one ncu --set full capture of the top
-# kernels.  Everything lands in gpurun_out/.
+# kernels (each only after the same command exited 0 without ncu).
+# Everything lands in gpurun_out/; tools/summarize_profiles.py turns it into
+# profiles/.
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err
 echo "bench rc=$?"
-python bench.py --impl reference --steps 2 --warmup 1 --cpu-seconds 20 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 echo "ref rc=$?"
 CMD="python bench.py --steps 1 --warmup 3 --no-cpu-baseline"
 $CMD > gpurun_out/plain.log 2>&1 && \
@@ -15,6 +17,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 echo "launch list rc=$?"
 $CMD > gpurun_out/plain2.log 2>&1 && \
 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_scan|k_probe_gemm_tc|k_plan_approx|k_probe_select" -s 4 -c 4 \
-    -o gpurun_out/prof_full $CMD > gpurun_out/ncu_full.log 2>&1
+    -k regex:"k_scan_warp|k_probe_gemm_tc|k_plan_approx|k_probe_select|k_plan_rescore|k_plan_scores_approx" \
+    -s 6 -c 6 -o gpurun_out/prof_full $CMD > gpurun_out/ncu_full.log 2>&1
 echo "ncu full rc=$?"
