@@ -298,11 +298,12 @@ bool use_tensor_cores(const IndexView& v) {
 }
 
 // Probe for one chunk of queries: regions (nq, P) and qc2 (nq, P).  *D_out
-// receives the fp32 score matrix (nq, K) when the GEMM path ran, else null;
-// *eps_out its error-bound scale.
+// receives the fp16-encoded score matrix (nq, K) when the GEMM path ran, else
+// null, *scale_out its per-query decode scale and *eps_out the GEMM's
+// error-bound scale.
 int run_probe(givf_index* ix, const Plan& pl, const float* dQ, int nq, int* regions,
-              double* qc2, Arena& ar, cudaStream_t st, const float** D_out = nullptr,
-              float* eps_out = nullptr) {
+              double* qc2, Arena& ar, cudaStream_t st, const uint16_t** D_out = nullptr,
+              const float** scale_out = nullptr, float* eps_out = nullptr) {
   const IndexView& v = ix->v;
   const int P = pl.P, K = v.K, d = v.d;
   if (D_out) *D_out = nullptr;
@@ -327,8 +328,17 @@ int run_probe(givf_index* ix, const Plan& pl, const float* dQ, int nq, int* regi
     KCHECK();
     return GIVF_OK;
   }
-  float* D = ar.take<float>((size_t)nq * K);
-  if (D_out) *D_out = D;
+  ScoreOut so;
+  so.D16 = ar.take<uint16_t>((size_t)nq * K);
+  so.ld = K;
+  float* q2f = ar.take<float>(nq);
+  float* qinv = ar.take<float>(nq);
+  float* qscale = ar.take<float>(nq);
+  so.q2 = q2f;
+  so.qinv = qinv;
+  so.qscale = qscale;
+  if (D_out) *D_out = so.D16;
+  if (scale_out) *scale_out = qscale;
   int* cand = ar.take<int>((size_t)nq * pl.ps.cap);
   int* cand_n = ar.take<int>(nq);
   float* theta = ar.take<float>(nq);
@@ -338,20 +348,25 @@ int run_probe(givf_index* ix, const Plan& pl, const float* dQ, int nq, int* regi
   if (tc) {
     void* abf = ar.take<uint16_t>((size_t)nq * tc_kpad(d));
     staged(ST_GEMM, st, [&] {
+      launch_query_scale(dQ, nq, d, v.cmax, q2f, qinv, qscale, st);
       launch_split_bf16(dQ, nq, d, 0, abf, st);
-      launch_probe_gemm_tc(abf, v.csplit, v.c2f, nq, K, d, D, K, tmin, st);
-    }, 2);
+      launch_probe_gemm_tc(abf, v.csplit, v.c2f, nq, K, d, so, tmin, st);
+    }, 3);
   } else {
-    staged(ST_GEMM, st, [&] { launch_probe_gemm(dQ, v.centroids, v.c2f, nq, K, d, D, K, tmin, st); });
+    staged(ST_GEMM, st, [&] {
+      launch_query_scale(dQ, nq, d, v.cmax, q2f, qinv, qscale, st);
+      launch_probe_gemm(dQ, v.centroids, v.c2f, nq, K, d, so, tmin, st);
+    }, 2);
   }
   staged(ST_SELECT, st, [&] {
-    launch_probe_select(D, K, nq, K, pl.ps.Tmin, pl.ps.cap, tmin, ntiles, cand, cand_n, theta, st);
+    launch_probe_select(so.D16, K, q2f, qscale, nq, K, pl.ps.Tmin, pl.ps.cap, tmin, ntiles, cand,
+                        cand_n, theta, st);
   });
   const float eps_scale = tc ? kEpsScaleTC : probe_eps_scale(d);
   if (eps_out) *eps_out = eps_scale;
   staged(ST_RECHECK, st, [&] {
     launch_probe_recheck(dQ, v.centroids, nq, K, d, P, cand, cand_n, pl.ps.cap, theta, v.cmax,
-                         eps_scale, regions, qc2, failf, v.counters, st);
+                         eps_scale, (float)kHalfRel, regions, qc2, failf, v.counters, st);
   });
   staged(ST_FULL, st, [&] {
     launch_probe_full(dQ, v.centroids, nq, K, d, P, 1, failf, slots, sk, sv, sk2, sv2, sdv,
@@ -364,7 +379,8 @@ int run_probe(givf_index* ix, const Plan& pl, const float* dQ, int nq, int* regi
 size_t probe_bytes_per_query(const Plan& pl) {
   size_t b = aligned_bytes<int>(1) * 4 + aligned_bytes<int>(pl.P) + aligned_bytes<double>(pl.P);
   if (!pl.ps.exhaustive)
-    b += (size_t)pl.K * 4 + (size_t)pl.ps.cap * 4 + aligned_bytes<float>(probe_tiles(pl.K)) +
+    b += (size_t)pl.K * 2 + 3 * aligned_bytes<float>(1) + (size_t)pl.ps.cap * 4 +
+         aligned_bytes<float>(probe_tiles(pl.K)) +
          (size_t)tc_kpad(pl.d) * 2 + 256;
   return b;
 }
@@ -520,10 +536,11 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
     for (int64_t s0 = 0; s0 < bq; s0 += sub) {
       const int ns_q = (int)std::min<int64_t>(sub, bq - s0);
       ar.off = mark;
-      const float* Dmat = nullptr;
+      const uint16_t* Dmat = nullptr;
+      const float* dscale = nullptr;
       float eps_scale = 0.f;
       rc = run_probe(ix, pl, dQ + s0 * v.d, ns_q, regions + s0 * pl.P, qc2 + s0 * pl.P, ar, st,
-                     &Dmat, &eps_scale);
+                     &Dmat, &dscale, &eps_scale);
       if (rc) return rc;
       pa.eps_scale = eps_scale;
       if (!Dmat) {  // exhaustive probe (nprobe == K or too wide): exact planner only
@@ -537,6 +554,7 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
       sa.nq = ns_q;
       sa.akey = pa.akey + s0 * pl.total;
       sa.D = Dmat;
+      sa.dscale = dscale;
       int nk = 0;
       staged(ST_PLAN, st, [&] { nk = launch_plan_scores(sa, st); }, 0);
       g_launches += nk;
@@ -840,13 +858,16 @@ int givf_probe_scores(givf_index_t ix, const float* queries, int64_t nq, float* 
   float* D = o_dev ? scores : ar.take<float>((size_t)nq * K);
   float* tmin = ar.take<float>((size_t)nq * probe_tiles(K));
   const bool tc = use_tensor_cores(v);
+  ScoreOut so;  // the GEMM's own fp32 scores (the search path stores fp16)
+  so.D32 = D;
+  so.ld = K;
   if (tc) {
     void* abf = ar.take<uint16_t>((size_t)nq * tc_kpad(d));
     launch_split_bf16(dQ, (int)nq, d, 0, abf, st);
-    launch_probe_gemm_tc(abf, v.csplit, v.c2f, (int)nq, K, d, D, K, tmin, st);
+    launch_probe_gemm_tc(abf, v.csplit, v.c2f, (int)nq, K, d, so, tmin, st);
     g_launches += 2;
   } else {
-    launch_probe_gemm(dQ, v.centroids, v.c2f, (int)nq, K, d, D, K, tmin, st);
+    launch_probe_gemm(dQ, v.centroids, v.c2f, (int)nq, K, d, so, tmin, st);
     g_launches += 1;
   }
   KCHECK();

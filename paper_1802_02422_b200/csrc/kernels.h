@@ -45,26 +45,44 @@ struct IndexView {
   unsigned long long* counters;  // [0] probe fallbacks, [1] plan fallbacks (device)
 };
 
+// Where the probe GEMM puts its scores s~ = |c|^2 - 2 q.c.  The search path
+// stores them as fp16 (half the HBM traffic of the GEMM, the select and
+// K3a): h = f16((s~ + |q|^2) * qinv), decoded s~ = h * qscale - |q|^2, with
+// qscale = 2^e a per-query power of two that keeps (|q| + cmax)^2 / 2^e
+// <= 2^15.  The rounding adds at most kHalfRel * (|q| + cmax)^2 to every
+// score's error bound.  probe_scores (accuracy checks) keeps fp32.
+constexpr double kHalfRel = 1.0 / 2048.0;  // fp16 half ulp, relative
+struct ScoreOut {
+  float* D32 = nullptr;           // fp32 scores, or
+  uint16_t* D16 = nullptr;        // fp16 encoded scores
+  int64_t ld = 0;                 // row pitch (elements)
+  const float* q2 = nullptr;      // (nq) f32 |q|^2        (fp16 only)
+  const float* qinv = nullptr;    // (nq) 2^-e             (fp16 only)
+  const float* qscale = nullptr;  // (nq) 2^e              (fp16 only)
+};
+
 // probe_tc.cu: tcgen05 bf16x3 probe GEMM
 int tc_kpad(int d);
 bool tc_supported(int d);
 size_t tc_smem_bytes(int d);
 void launch_split_bf16(const float* x, int rows, int d, int centroid, void* out, cudaStream_t s);
 bool launch_probe_gemm_tc(const void* Abf, const void* Bbf, const float* c2, int nq, int K, int d,
-                          float* D, int64_t ldD, float* tmin, cudaStream_t s);
+                          const ScoreOut& o, float* tmin, cudaStream_t s);
 
 // probe.cu
 int probe_tiles(int K);  // per-query tile minima the GEMM epilogue emits
+void launch_query_scale(const float* Q, int nq, int d, float cmax, float* q2, float* qinv,
+                        float* qscale, cudaStream_t s);
 void launch_probe_gemm(const float* Q, const float* C, const float* c2, int nq, int K, int d,
-                       float* D, int64_t ldD, float* tmin, cudaStream_t s);
-void launch_probe_select(const float* D, int64_t ldD, int nq, int K, int Tmin, int cap,
-                         const float* tmin, int ntiles, int* cand, int* cand_n, float* theta,
-                         cudaStream_t s);
+                       const ScoreOut& o, float* tmin, cudaStream_t s);
+void launch_probe_select(const uint16_t* D, int64_t ldD, const float* q2, const float* qscale,
+                         int nq, int K, int Tmin, int cap, const float* tmin, int ntiles,
+                         int* cand, int* cand_n, float* theta, cudaStream_t s);
 size_t probe_recheck_smem(int d, int P, int cap);
 void launch_probe_recheck(const float* Q, const float* C, int nq, int K, int d, int P,
                           const int* cand, const int* cand_n, int cap, const float* theta,
-                          float cmax, float eps_scale, int* regions, double* qc2, int* fail,
-                          unsigned long long* fail_count, cudaStream_t s);
+                          float cmax, float eps_scale, float half_rel, int* regions, double* qc2,
+                          int* fail, unsigned long long* fail_count, cudaStream_t s);
 void launch_probe_full(const float* Q, const float* C, int nq, int K, int d, int P, int mode,
                        const int* fail, int nslots, uint64_t* sk, uint32_t* sv, uint64_t* sk2,
                        uint32_t* sv2, double* sdv, int* regions, double* qc2, cudaStream_t s);
@@ -89,8 +107,9 @@ struct PlanArgs {
   uint64_t* skey;       // (nq, pow2(cap_w)) scratch
   uint32_t* sval;       // (nq, pow2(cap_w)) scratch
   int32_t* order;       // (nq, cap_w)
-  // approximate-first path: the probe's fp32 scores s~ = |c|^2 - 2 q.c
-  const float* D;       // (nq, ldD) or null (exact path only)
+  // approximate-first path: the probe's fp16-encoded scores (see ScoreOut)
+  const uint16_t* D;    // (nq, ldD) or null (exact path only)
+  const float* dscale;  // (nq) decode scale 2^e: qs2~ = h * dscale
   int64_t ldD;
   float cmax, eps_scale;
   int* only;            // (nq) fallback flags: exact kernels run where only[b] != 0

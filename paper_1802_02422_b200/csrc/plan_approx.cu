@@ -26,6 +26,8 @@
 //     5. emits A and the begun W groups (compacted, one metadata gather per
 //        group) with float64 base/score recomputed exactly from one centroid
 //        row per emitted group.
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "plan_common.cuh"
@@ -51,7 +53,7 @@ __global__ void __launch_bounds__(PA_THREADS) k_plan_scores_approx(PlanArgs a) {
   const IndexView& ix = a.ix;
   const int lane = threadIdx.x & 31;
   const int64_t wid = (int64_t)blockIdx.x * (PA_THREADS / 32) + (threadIdx.x >> 5);
-  const int P = a.P, G = ix.G, d = ix.d;
+  const int P = a.P, G = ix.G;
   if (wid >= (int64_t)a.nq * P) return;
   const int b = (int)(wid / P), p = (int)(wid % P);
   const int64_t total = (int64_t)P * G;
@@ -63,16 +65,14 @@ __global__ void __launch_bounds__(PA_THREADS) k_plan_scores_approx(PlanArgs a) {
     for (int j = lane; j < G; j += 32) akey[j] = k;
     return;
   }
-  const float* q = a.Q + (int64_t)b * d;
-  double q2 = 0.0;
-  for (int j = lane; j < d; j += 32) q2 += (double)q[j] * (double)q[j];
-  q2 = warp_sum(q2);
-  const float* Drow = a.D + (int64_t)b * a.ldD;
+  const uint16_t* Drow = a.D + (int64_t)b * a.ldD;
+  const double dsc = (double)a.dscale[b];
   const double al = (double)ix.alphas[r];
   const double oma_qc = dmul(dsub(1.0, al), qc);
   for (int j = lane; j < G; j += 32) {
     const int64_t gi = (int64_t)r * G + j;
-    const double qs2 = dadd((double)__ldg(Drow + ix.nbr[gi]), q2);
+    // fp16-encoded |q - c_s|^2 (ScoreOut in kernels.h), decoded exactly
+    const double qs2 = (double)__half2float(__ushort_as_half(__ldg(Drow + ix.nbr[gi]))) * dsc;
     const double score = dadd(dadd(oma_qc, dmul(al, qs2)), (double)ix.norm[gi]);
     akey[j] = f32_key((float)score);
   }
@@ -152,13 +152,17 @@ __global__ void __launch_bounds__(PA_THREADS, 3) k_plan_approx(PlanArgs a) {
     qd[j] = x;
     q2p += x * x;
   }
-  if (pst)
-    for (int p = tid; p < P; p += PA_THREADS) {
-      const int r = greg[p];
+  double alx = 0.0;  // max |alpha| over the probed regions
+  for (int p = tid; p < P; p += PA_THREADS) {
+    const int r = greg[p];
+    const double al = ix.grouping ? (double)ix.alphas[r] : 0.0;
+    alx = fmax(alx, fabs(al));
+    if (pst) {
       preg[p] = r;
       pqc[p] = gqc[p];
-      pal[p] = ix.grouping ? (double)ix.alphas[r] : 0.0;
+      pal[p] = al;
     }
+  }
   __syncthreads();
   auto REG = [&](int p) -> int { return pst ? preg[p] : greg[p]; };
   auto QC = [&](int p) -> double { return pst ? pqc[p] : gqc[p]; };
@@ -199,6 +203,7 @@ __global__ void __launch_bounds__(PA_THREADS, 3) k_plan_approx(PlanArgs a) {
     }
   }
   const double q2 = block_sum(q2p, redd);
+  alx = block_max(alx, redd);
   kmin = block_min(kmin, red32);
   kmax = block_max(kmax, red32);
   auto KEY = [&](int64_t f) -> uint32_t { return staged ? skey[f] : gkey[f]; };
@@ -206,8 +211,12 @@ __global__ void __launch_bounds__(PA_THREADS, 3) k_plan_approx(PlanArgs a) {
   const double qn = sqrt(q2);
   const double amax = fmax(fabs((double)key_f32(kmin)), fabs((double)key_f32(kmax)));
   const double cq = (double)a.cmax + qn;
+  // Only qs2 is approximate and it enters the score times alpha: alpha_max x
+  // (GEMM bound + fp16 storage of the neighbor scores, kHalfRel of at most
+  // (|q| + cmax)^2), + the float32 key rounding + slack
   const double E = ix.grouping
-      ? 1.0001 * ((double)a.eps_scale * ((double)a.cmax * a.cmax + 2.0 * qn * a.cmax)) +
+      ? 1.0001 * alx * ((double)a.eps_scale * ((double)a.cmax * a.cmax + 2.0 * qn * a.cmax) +
+                        1.001 * kHalfRel * cq * cq) +
             amax * 1.2e-7 + 1e-12 * cq * cq
       : amax * 1.2e-7;  // float32 key rounding only
   PLAN_PHASE(0);

@@ -16,20 +16,48 @@
 // nprobe == K branch go through probe_full, which ranks all K regions
 // exactly.  The result is bit-identical to the oracle's probe_exact by
 // construction, whatever the approximation error of K1a.
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
 namespace givf {
+
+// ----------------------------------------------------------------- scale
+// Per query: |q|^2 (f32) and the power-of-two fp16 encoding scale of its
+// scores (ScoreOut in kernels.h): 2^e >= (|q| + cmax)^2 / 2^15.
+__global__ void k_query_scale(const float* __restrict__ Q, int nq, int d, float cmax,
+                              float* __restrict__ q2o, float* __restrict__ qinv,
+                              float* __restrict__ qscale) {
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (b >= nq) return;
+  double s = 0.0;
+  for (int j = lane; j < d; j += 32) s += (double)Q[(int64_t)b * d + j] * Q[(int64_t)b * d + j];
+  s = warp_sum(s);
+  if (lane == 0) {
+    const double m = (sqrt(s) + (double)cmax) * (sqrt(s) + (double)cmax);
+    const int e = (m > 0.0 ? ilogb(m) + 1 : 0) - 15;
+    q2o[b] = (float)s;
+    qinv[b] = ldexpf(1.f, -e);
+    qscale[b] = ldexpf(1.f, e);
+  }
+}
+
+GIVF_DEV float dec_score(uint16_t h, float scale, float q2) {
+  return fmaf(__half2float(__ushort_as_half(h)), scale, -q2);
+}
 
 // ----------------------------------------------------------------- K1a
 // SIMT fp32 tile GEMM: 64 queries x 128 centroids per CTA, 256 threads,
 // 4x8 outputs per thread, d in chunks of 16 through shared memory.
 constexpr int PG_BM = 64, PG_BN = 128, PG_BK = 16;
 
+template <bool HALF>
 __global__ void __launch_bounds__(256)
 k_probe_gemm(const float* __restrict__ Q, const float* __restrict__ C,
-             const float* __restrict__ c2, int nq, int K, int d,
-             float* __restrict__ D, int64_t ldD, float* __restrict__ tmin) {
+             const float* __restrict__ c2, int nq, int K, int d, ScoreOut o,
+             float* __restrict__ tmin) {
   __shared__ float As[PG_BK][PG_BM + 4];
   __shared__ float Bs[PG_BK][PG_BN + 4];
   const int tid = threadIdx.x;
@@ -78,19 +106,28 @@ k_probe_gemm(const float* __restrict__ Q, const float* __restrict__ C,
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     int qr = q0 + ty * 4 + i;
+    float q2r = 0.f, ir = 1.f;
+    if (HALF && qr < nq) { q2r = o.q2[qr]; ir = o.qinv[qr]; }
     float mn = __int_as_float(0x7f800000);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       int cr = c0 + tx * 8 + j;
       if (cr < K) {
         float v = fmaf(-2.f, acc[i][j], c2[cr]);
-        mn = fminf(mn, v);
-        if (qr < nq) D[(int64_t)qr * ldD + cr] = v;
+        if constexpr (HALF) {
+          const __half h = __float2half_rn((v + q2r) * ir);
+          mn = fminf(mn, __half2float(h));
+          if (qr < nq) o.D16[(int64_t)qr * o.ld + cr] = __half_as_ushort(h);
+        } else {
+          mn = fminf(mn, v);
+          if (qr < nq) o.D32[(int64_t)qr * o.ld + cr] = v;
+        }
       }
     }
     // 16 threads (tx) share a row: reduce within each half-warp
 #pragma unroll
-    for (int o = 8; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    for (int w = 8; w > 0; w >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, w));
+    if (HALF && qr < nq) mn = fmaf(mn, o.qscale[qr], -q2r);  // decoded
     if (tx == 0 && qr < nq && tmin) tmin[(int64_t)qr * ntiles + blockIdx.x] = mn;
   }
 }
@@ -101,8 +138,16 @@ k_probe_gemm(const float* __restrict__ Q, const float* __restrict__ C,
 // u32 keys.  theta = smallest excluded score (+inf when nothing excluded).
 constexpr int SEL_THREADS = 512;
 
+// Decoded scores of one fp16 row (ScoreOut in kernels.h).
+struct HalfRow {
+  const uint16_t* __restrict__ r;
+  float scale, q2;
+  GIVF_DEV float operator()(int i) const { return dec_score(__ldg(r + i), scale, q2); }
+};
+
 // Generic path: bucketed refinement over the whole row (any K, any ties).
-__device__ void select_bucketed(const float* __restrict__ row, int K, int Tmin, int cap,
+template <typename Row>
+__device__ void select_bucketed(Row row, int K, int Tmin, int cap,
                                 int* __restrict__ out, int* __restrict__ n_out,
                                 float* __restrict__ theta_out, uint32_t* hist) {
   __shared__ uint32_t red[40];
@@ -111,7 +156,7 @@ __device__ void select_bucketed(const float* __restrict__ row, int K, int Tmin, 
   const int tid = threadIdx.x;
   uint32_t mn = 0xffffffffu, mx = 0u;
   for (int i = tid; i < K; i += blockDim.x) {
-    uint32_t k = f32_key(row[i]);
+    uint32_t k = f32_key(row(i));
     mn = min(mn, k); mx = max(mx, k);
   }
   uint32_t lo = block_min(mn, red), hi = block_max(mx, red);
@@ -127,7 +172,7 @@ __device__ void select_bucketed(const float* __restrict__ row, int K, int Tmin, 
     for (uint32_t i = tid; i < nb; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     for (int i = tid; i < K; i += blockDim.x) {
-      uint32_t k = f32_key(row[i]);
+      uint32_t k = f32_key(row(i));
       if (k >= lo && k <= hi) atomicAdd(&hist[(k - lo) >> shift], 1u);
     }
     __syncthreads();
@@ -171,7 +216,7 @@ __device__ void select_bucketed(const float* __restrict__ row, int K, int Tmin, 
   __syncthreads();
   uint32_t ex = 0xffffffffu;
   for (int i = tid; i < K; i += blockDim.x) {
-    uint32_t k = f32_key(row[i]);
+    uint32_t k = f32_key(row(i));
     if ((uint64_t)k < boundary) {
       out[atomicAdd(&cnt_lt, 1u)] = i;
     } else if (degenerate && k == deg_key) {
@@ -198,13 +243,14 @@ __device__ void select_bucketed(const float* __restrict__ row, int K, int Tmin, 
 constexpr int SEL_COLLECT = 4096;
 
 __global__ void __launch_bounds__(SEL_THREADS)
-k_probe_select(const float* __restrict__ D, int64_t ldD, int K, int Tmin, int cap,
+k_probe_select(const uint16_t* __restrict__ D, int64_t ldD, const float* __restrict__ q2v,
+               const float* __restrict__ qscale, int K, int Tmin, int cap,
                const float* __restrict__ tmin, int ntiles,
                int* __restrict__ cand, int* __restrict__ cand_n, float* __restrict__ theta) {
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ uint32_t red[40];
   __shared__ uint32_t s_cnt;
-  const float* row = D + (int64_t)blockIdx.x * ldD;
+  const HalfRow row{D + (int64_t)blockIdx.x * ldD, qscale[blockIdx.x], q2v[blockIdx.x]};
   int* out = cand + (int64_t)blockIdx.x * cap;
   const int tid = threadIdx.x;
 
@@ -240,17 +286,19 @@ k_probe_select(const float* __restrict__ D, int64_t ldD, int K, int Tmin, int ca
       ex = min(ex, k);
     }
   };
-  if ((K & 3) == 0 && (reinterpret_cast<uintptr_t>(row) & 15) == 0) {
-    const float4* r4 = reinterpret_cast<const float4*>(row);
-    for (int i = tid; i < (K >> 2); i += blockDim.x) {  // 16-byte loads, 4 scores each
-      const float4 v = __ldg(r4 + i);
-      take(v.x, 4 * i);
-      take(v.y, 4 * i + 1);
-      take(v.z, 4 * i + 2);
-      take(v.w, 4 * i + 3);
+  if ((K & 7) == 0 && (reinterpret_cast<uintptr_t>(row.r) & 15) == 0) {
+    const uint4* r8 = reinterpret_cast<const uint4*>(row.r);
+    for (int i = tid; i < (K >> 3); i += blockDim.x) {  // 16-byte loads, 8 scores each
+      const uint4 v = __ldg(r8 + i);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        take(dec_score((uint16_t)(w[k] & 0xffffu), row.scale, row.q2), 8 * i + 2 * k);
+        take(dec_score((uint16_t)(w[k] >> 16), row.scale, row.q2), 8 * i + 2 * k + 1);
+      }
     }
   } else {
-    for (int i = tid; i < K; i += blockDim.x) take(row[i], i);
+    for (int i = tid; i < K; i += blockDim.x) take(row(i), i);
   }
   ex = block_min(ex, red);  // also orders the collection before its use
   const uint32_t n = s_cnt;
@@ -342,8 +390,8 @@ __global__ void __launch_bounds__(256)
 k_probe_recheck(const float* __restrict__ Q, const float* __restrict__ C, int K, int d,
                 int P, const int* __restrict__ cand, const int* __restrict__ cand_n,
                 int cap, const float* __restrict__ theta, float cmax, float eps_scale,
-                int* __restrict__ regions, double* __restrict__ qc2, int* __restrict__ fail,
-                unsigned long long* fail_count) {
+                float half_rel, int* __restrict__ regions, double* __restrict__ qc2,
+                int* __restrict__ fail, unsigned long long* fail_count) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int capp2 = (int)next_pow2((uint32_t)cap);
   const int pp2 = (int)next_pow2((uint32_t)P);
@@ -385,6 +433,9 @@ k_probe_recheck(const float* __restrict__ Q, const float* __restrict__ C, int K,
                  1e-12 * ((double)cmax + qn) * ((double)cmax + qn);
     double dp = key_f64(key[P - 1]);
     double th = (double)theta[b];
+    // fp16 storage of the scores: the smallest excluded one, decoded, is
+    // within half_rel of its encoded distance th + |q|^2 (plus the f32 decode)
+    eps += (double)half_rel * 1.001 * fabs(th + q2) + 1.2e-7 * (fabs(th) + q2);
     bool ok = (n >= P) && (dp - q2 < th - eps);
     if (!ok) {
       if (threadIdx.x == 0) {
@@ -459,23 +510,29 @@ k_probe_full(const float* __restrict__ Q, const float* __restrict__ C, int nq, i
 // ----------------------------------------------------------------- launchers
 int probe_tiles(int K) { return (K + PG_BN - 1) / PG_BN; }
 
-void launch_probe_gemm(const float* Q, const float* C, const float* c2, int nq, int K, int d,
-                       float* D, int64_t ldD, float* tmin, cudaStream_t s) {
-  dim3 grid((K + PG_BN - 1) / PG_BN, (nq + PG_BM - 1) / PG_BM);
-  k_probe_gemm<<<grid, 256, 0, s>>>(Q, C, c2, nq, K, d, D, ldD, tmin);
+void launch_query_scale(const float* Q, int nq, int d, float cmax, float* q2, float* qinv,
+                        float* qscale, cudaStream_t s) {
+  k_query_scale<<<(nq + 7) / 8, 256, 0, s>>>(Q, nq, d, cmax, q2, qinv, qscale);
 }
 
-void launch_probe_select(const float* D, int64_t ldD, int nq, int K, int Tmin, int cap,
-                         const float* tmin, int ntiles, int* cand, int* cand_n, float* theta,
-                         cudaStream_t s) {
+void launch_probe_gemm(const float* Q, const float* C, const float* c2, int nq, int K, int d,
+                       const ScoreOut& o, float* tmin, cudaStream_t s) {
+  dim3 grid((K + PG_BN - 1) / PG_BN, (nq + PG_BM - 1) / PG_BM);
+  if (o.D16) k_probe_gemm<true><<<grid, 256, 0, s>>>(Q, C, c2, nq, K, d, o, tmin);
+  else k_probe_gemm<false><<<grid, 256, 0, s>>>(Q, C, c2, nq, K, d, o, tmin);
+}
+
+void launch_probe_select(const uint16_t* D, int64_t ldD, const float* q2, const float* qscale,
+                         int nq, int K, int Tmin, int cap, const float* tmin, int ntiles,
+                         int* cand, int* cand_n, float* theta, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_probe_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     attr = true;
   }
   if (ntiles > 8192) tmin = nullptr;  // tile keys must fit the 32 KB staging area
-  k_probe_select<<<nq, SEL_THREADS, 8192 * 4 + SEL_COLLECT * 8, s>>>(D, ldD, K, Tmin, cap, tmin,
-                                                                      ntiles, cand, cand_n, theta);
+  k_probe_select<<<nq, SEL_THREADS, 8192 * 4 + SEL_COLLECT * 8, s>>>(
+      D, ldD, q2, qscale, K, Tmin, cap, tmin, ntiles, cand, cand_n, theta);
 }
 
 size_t probe_recheck_smem(int d, int P, int cap) {
@@ -487,8 +544,8 @@ size_t probe_recheck_smem(int d, int P, int cap) {
 
 void launch_probe_recheck(const float* Q, const float* C, int nq, int K, int d, int P,
                           const int* cand, const int* cand_n, int cap, const float* theta,
-                          float cmax, float eps_scale, int* regions, double* qc2, int* fail,
-                          unsigned long long* fail_count, cudaStream_t s) {
+                          float cmax, float eps_scale, float half_rel, int* regions, double* qc2,
+                          int* fail, unsigned long long* fail_count, cudaStream_t s) {
   size_t sm = probe_recheck_smem(d, P, cap);
   static bool attr = false;
   if (!attr) {
@@ -496,7 +553,7 @@ void launch_probe_recheck(const float* Q, const float* C, int nq, int K, int d, 
     attr = true;
   }
   k_probe_recheck<<<nq, 256, sm, s>>>(Q, C, K, d, P, cand, cand_n, cap, theta, cmax, eps_scale,
-                                      regions, qc2, fail, fail_count);
+                                      half_rel, regions, qc2, fail, fail_count);
 }
 
 void launch_probe_full(const float* Q, const float* C, int nq, int K, int d, int P, int mode,

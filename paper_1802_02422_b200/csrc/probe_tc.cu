@@ -24,6 +24,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <algorithm>
 
@@ -163,11 +164,15 @@ struct Smem {
 }  // namespace tc
 
 // smem: [A resident: KC x 16 KB][B ring: STAGES x 32 KB][barriers]
+// HALF: scores leave as fp16 (ScoreOut in kernels.h), else fp32.
+template <bool HALF>
 __global__ void __launch_bounds__(tc::THREADS, 1)
 k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                 const __grid_constant__ CUtensorMap mapD, int use_tma_store,
                 const float* __restrict__ c2, int nq, int K, int KC, int nsplit,
-                float* __restrict__ D, int64_t ldD, float* __restrict__ tmin) {
+                float* __restrict__ D, uint16_t* __restrict__ D16, int64_t ldD,
+                const float* __restrict__ q2v, const float* __restrict__ qinv,
+                const float* __restrict__ qscale, float* __restrict__ tmin) {
   using namespace tc;
   extern __shared__ __align__(1024) unsigned char dsm[];
   unsigned char* base = reinterpret_cast<unsigned char*>(
@@ -282,6 +287,8 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
       const int mb = u / nsplit, sp = u % nsplit;
       const int t0 = sp * per_split, t1 = min(n_tiles, t0 + per_split);
       const int q = mb * BM + quarter * 32 + lane;
+      float q2r = 0.f, ir = 1.f, sr = 1.f;  // fp16 encoding of this row
+      if (HALF && q < nq) { q2r = q2v[q]; ir = qinv[q]; sr = qscale[q]; }
       for (int t = t0; t < t1; ++t) {
         const int colh = t * BN + half * 128;
         // this half tile's |c|^2 terms: loaded before the accumulator wait so
@@ -297,8 +304,9 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
 #pragma unroll
         for (int c = 0; c < 4; ++c) c2s[c * 32 + lane] = c2r[c];
         __syncwarp();
-        float* drow = D + (int64_t)q * ldD;
-        float mn = __int_as_float(0x7f800000);
+        float* drow = HALF ? nullptr : D + (int64_t)q * ldD;
+        uint16_t* hrow = HALF ? D16 + (int64_t)q * ldD : nullptr;
+        float mn = __int_as_float(0x7f800000);  // (HALF: in the encoded domain)
         const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN + half * 128;
         uint32_t ra[32], rb[32];
         tmem_ld32_async(tb, ra);
@@ -328,41 +336,83 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
                              : __int_as_float(0x7f800000);
             }
           }
+          if constexpr (HALF) {
+            uint32_t hp[16];  // 32 encoded scores, packed in pairs
 #pragma unroll
-          for (int i = 0; i < 32; ++i) mn = fminf(mn, v[i]);
-          if (use_tma_store) {
-            // the previous store from this staging tile has read it
-            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            __syncwarp();
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-              *reinterpret_cast<float4*>(sb + lane * 128 + ((k ^ (lane & 7)) * 16)) =
-                  make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) {
-              asm volatile(
-                  "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                      reinterpret_cast<uint64_t>(&mapD)),
-                  "r"(col0), "r"(mb * BM + quarter * 32), "r"(smem_u32(sb))
-                  : "memory");
-              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            for (int i = 0; i < 16; ++i) {
+              const __half h0 = __float2half_rn((v[2 * i] + q2r) * ir);
+              const __half h1 = __float2half_rn((v[2 * i + 1] + q2r) * ir);
+              mn = fminf(mn, fminf(__half2float(h0), __half2float(h1)));
+              hp[i] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
             }
-          } else if (q < nq) {
-            if (col0 + 32 <= K) {
-              float4* dst = reinterpret_cast<float4*>(drow + col0);
+            if (use_tma_store) {
+              if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+              __syncwarp();
+              // 32 rows x 64 B, SWIZZLE_64B: chunk k of row r at k ^ ((r >> 1) & 3)
 #pragma unroll
-              for (int i = 0; i < 8; ++i)
-                dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-            } else {
+              for (int k = 0; k < 4; ++k)
+                *reinterpret_cast<uint4*>(sb + lane * 64 + ((k ^ ((lane >> 1) & 3)) * 16)) =
+                    make_uint4(hp[4 * k], hp[4 * k + 1], hp[4 * k + 2], hp[4 * k + 3]);
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              __syncwarp();
+              if (lane == 0) {
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                        reinterpret_cast<uint64_t>(&mapD)),
+                    "r"(col0), "r"(mb * BM + quarter * 32), "r"(smem_u32(sb))
+                    : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+              }
+            } else if (q < nq) {
+              if (col0 + 32 <= K && (ldD & 7) == 0) {
+                uint4* dst = reinterpret_cast<uint4*>(hrow + col0);
 #pragma unroll
-              for (int i = 0; i < 32; ++i)
-                if (col0 + i < K) drow[col0 + i] = v[i];
+                for (int k = 0; k < 4; ++k)
+                  dst[k] = make_uint4(hp[4 * k], hp[4 * k + 1], hp[4 * k + 2], hp[4 * k + 3]);
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (col0 + i < K) hrow[col0 + i] = (uint16_t)(hp[i >> 1] >> ((i & 1) * 16));
+              }
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) mn = fminf(mn, v[i]);
+            if (use_tma_store) {
+              // the previous store from this staging tile has read it
+              if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+              __syncwarp();
+#pragma unroll
+              for (int k = 0; k < 8; ++k)
+                *reinterpret_cast<float4*>(sb + lane * 128 + ((k ^ (lane & 7)) * 16)) =
+                    make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              __syncwarp();
+              if (lane == 0) {
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                        reinterpret_cast<uint64_t>(&mapD)),
+                    "r"(col0), "r"(mb * BM + quarter * 32), "r"(smem_u32(sb))
+                    : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+              }
+            } else if (q < nq) {
+              if (col0 + 32 <= K) {
+                float4* dst = reinterpret_cast<float4*>(drow + col0);
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                  dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (col0 + i < K) drow[col0 + i] = v[i];
+              }
             }
           }
           if (c < 3) tmem_wait_ld(rn);
         }
         const int h = t * 2 + half;  // this warp's 128-centroid tile
+        if (HALF) mn = fmaf(mn, sr, -q2r);  // decoded like every stored score
         if (q < nq && tmin && h < ntiles128) tmin[(int64_t)q * ntiles128 + h] = mn;
         fence_before();
         __syncwarp();
@@ -432,17 +482,19 @@ bool make_map(CUtensorMap* m, const void* ptr, int64_t rows, int Kp, int box_row
   return r == CUDA_SUCCESS;
 }
 
-// fp32 score matrix (rows x cols, pitch ld floats) written in 32 x 32 boxes
-// from SWIZZLE_128B staging tiles.
-bool make_map_f32_out(CUtensorMap* m, void* ptr, int64_t rows, int cols, int64_t ld) {
+// Score matrix (rows x cols, pitch ld elements) written in 32 x 32 boxes from
+// swizzled staging tiles: fp32 (128 B rows, SWIZZLE_128B) or fp16 (64 B
+// rows, SWIZZLE_64B).
+bool make_map_out(CUtensorMap* m, void* ptr, int64_t rows, int cols, int64_t ld, bool half) {
   auto enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * (half ? 2 : 4)};
   cuuint32_t box[2] = {32, 32};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ptr, dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  CUresult r = enc(m, half ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                   ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   half ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -478,13 +530,15 @@ size_t tc_smem_bytes(int d) {
 }
 
 bool launch_probe_gemm_tc(const void* Abf, const void* Bbf, const float* c2, int nq, int K, int d,
-                          float* D, int64_t ldD, float* tmin, cudaStream_t s) {
+                          const ScoreOut& o, float* tmin, cudaStream_t s) {
   const int Kp = tc_kpad(d);
+  const bool half = o.D16 != nullptr;
   CUtensorMap ma, mb, md;
   if (!make_map(&ma, Abf, nq, Kp, tc::BM) || !make_map(&mb, Bbf, K, Kp, tc::BN)) return false;
-  // s~ rows go out through TMA stores when the row pitch allows it
-  int use_tma_store = (ldD % 4 == 0) ? 1 : 0;
-  if (use_tma_store && !make_map_f32_out(&md, D, nq, K, ldD)) use_tma_store = 0;
+  // scores go out through TMA stores when the row pitch allows it (16 B)
+  void* dptr = half ? (void*)o.D16 : (void*)o.D32;
+  int use_tma_store = ((o.ld * (half ? 2 : 4)) % 16 == 0) ? 1 : 0;
+  if (use_tma_store && !make_map_out(&md, dptr, nq, K, o.ld, half)) use_tma_store = 0;
   if (!use_tma_store) md = ma;  // unused
   const int KC = Kp / tc::BK;
   const int m_blocks = (nq + tc::BM - 1) / tc::BM;
@@ -494,13 +548,14 @@ bool launch_probe_gemm_tc(const void* Abf, const void* Bbf, const float* c2, int
   const int units = m_blocks * nsplit;
   const int grid = std::min(units, sms);
   const size_t smem = tc_smem_bytes(d);
-  static size_t attr = 0;
-  if (attr < smem) {
-    cudaFuncSetAttribute(k_probe_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = smem;
+  auto kern = half ? k_probe_gemm_tc<true> : k_probe_gemm_tc<false>;
+  static size_t attr[2] = {0, 0};
+  if (attr[half] < smem) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr[half] = smem;
   }
-  k_probe_gemm_tc<<<grid, tc::THREADS, smem, s>>>(ma, mb, md, use_tma_store, c2, nq, K, KC, nsplit,
-                                                  D, ldD, tmin);
+  kern<<<grid, tc::THREADS, smem, s>>>(ma, mb, md, use_tma_store, c2, nq, K, KC, nsplit, o.D32,
+                                       o.D16, o.ld, o.q2, o.qinv, o.qscale, tmin);
   return true;
 }
 

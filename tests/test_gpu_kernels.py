@@ -93,8 +93,9 @@ def test_near_duplicate_centroids_take_the_fallback_and_stay_exact():
 
 def _sphere_index(seed=0, k=4096, d=96, g=8, m=16, on_sphere=1024):
     """Regions whose centroids are all (numerically) equidistant from the
-    query origin, with alpha = 0 and zero norm terms: no fp32 score can
-    separate them, so both certified fast paths must hand over."""
+    query origin, alpha = 0.5 (the neighbor distances count) and zero norm
+    terms: no fp32 / fp16 score can separate them, so both certified fast
+    paths must hand over."""
     from paper_1802_02422_b200.device_index import IndexArrays
 
     rng = np.random.default_rng(seed)
@@ -106,7 +107,7 @@ def _sphere_index(seed=0, k=4096, d=96, g=8, m=16, on_sphere=1024):
     np.cumsum(sizes.sum(1), out=offs[1:])
     n = int(offs[-1])
     return IndexArrays(
-        centroids=c, alphas=np.zeros(k, np.float32),
+        centroids=c, alphas=np.full(k, 0.5, np.float32),
         neighbor_ids=rng.integers(0, k, (k, g)).astype(np.int32),
         norm_terms=np.zeros((k, g), np.float32), group_sizes=sizes, region_offsets=offs,
         point_ids=rng.permutation(n).astype(np.int32),
