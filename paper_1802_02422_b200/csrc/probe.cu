@@ -288,13 +288,25 @@ k_probe_select(const uint16_t* __restrict__ D, int64_t ldD, const float* __restr
   };
   if ((K & 7) == 0 && (reinterpret_cast<uintptr_t>(row.r) & 15) == 0) {
     const uint4* r8 = reinterpret_cast<const uint4*>(row.r);
-    for (int i = tid; i < (K >> 3); i += blockDim.x) {  // 16-byte loads, 8 scores each
-      const uint4 v = __ldg(r8 + i);
-      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    const int n8 = K >> 3;
+    constexpr int U = 4;  // 16-byte loads in flight per thread, 8 scores each
+    for (int i0 = tid; i0 < n8; i0 += U * blockDim.x) {
+      uint4 v[U];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        take(dec_score((uint16_t)(w[k] & 0xffffu), row.scale, row.q2), 8 * i + 2 * k);
-        take(dec_score((uint16_t)(w[k] >> 16), row.scale, row.q2), 8 * i + 2 * k + 1);
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * blockDim.x;
+        v[u] = i < n8 ? __ldg(r8 + i) : make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * blockDim.x;
+        if (i >= n8) break;
+        const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          take(dec_score((uint16_t)(w[k] & 0xffffu), row.scale, row.q2), 8 * i + 2 * k);
+          take(dec_score((uint16_t)(w[k] >> 16), row.scale, row.q2), 8 * i + 2 * k + 1);
+        }
       }
     }
   } else {
