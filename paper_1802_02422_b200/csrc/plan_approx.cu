@@ -169,8 +169,14 @@ __global__ void __launch_bounds__(PA_THREADS, 3) k_plan_approx(PlanArgs a) {
   auto AL = [&](int p) -> double {
     return pst ? pal[p] : (ix.grouping ? (double)ix.alphas[greg[p]] : 0.0);
   };
+  // f / G by multiply-high (exact for f < 2^32 / G; staged f < PA_ITEMS)
+  const uint32_t ginv = G > 1 ? (uint32_t)(0xffffffffu / (uint32_t)G) + 1u : 0u;
+  auto DIVG = [&](int64_t f) -> int {
+    if (G == 1) return (int)f;
+    return staged ? (int)__umulhi((uint32_t)f, ginv) : (int)(f / G);
+  };
   auto GI = [&](int64_t f) -> int64_t {
-    const int p = (int)(f / G);
+    const int p = DIVG(f);
     return (int64_t)REG(p) * G + (f - (int64_t)p * G);
   };
   uint32_t kmin = 0xffffffffu, kmax = 0u;
@@ -182,8 +188,9 @@ __global__ void __launch_bounds__(PA_THREADS, 3) k_plan_approx(PlanArgs a) {
 #pragma unroll
     for (int t = 0; t < PT; ++t) {
       const int f = tid + t * PA_THREADS;
+      const int p = f < total ? DIVG(f) : 0;
       kk[t] = f < total ? gkey[f] : 0u;
-      zz[t] = f < total ? __ldg(ix.gsize + GI(f)) : 0;
+      zz[t] = f < total ? __ldg(ix.gsize + (int64_t)REG(p) * G + (f - p * G)) : 0;
     }
 #pragma unroll
     for (int t = 0; t < PT; ++t) {
