@@ -194,6 +194,91 @@ __device__ uint32_t block_select(int n, KeyOf key_of, uint32_t* hist, uint32_t* 
   return prefix;
 }
 
+// One warp's buffer cut to the entries whose distance key is <= T, where T
+// is the upper edge of the (range-adaptive, <= 256-bin) histogram bin holding
+// the k-th smallest key: >= k entries stay, usually few more.  One or two
+// histogram passes and no id loads; T (all ids) becomes the warp's bound and
+// is published to s_thr64.  Returns false (nothing changed) when more than
+// `room` entries would stay (massive distance ties): use warp_shrink then.
+__device__ __forceinline__ bool warp_cut(uint64_t* wb, int* cnt_io, uint32_t* thr, uint64_t* thr64,
+                                         uint32_t* hist, int k, int room,
+                                         unsigned long long* s_thr64) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  const int cnt = *cnt_io;
+  uint32_t mn = 0xffffffffu, mx = 0u;
+  for (int i = lane; i < cnt; i += 32) {
+    const uint32_t dk = (uint32_t)(wb[i] >> 32);
+    mn = min(mn, dk);
+    mx = max(mx, dk);
+  }
+  uint32_t lo = __reduce_min_sync(FULL, mn), hi = __reduce_max_sync(FULL, mx);
+  uint32_t need = (uint32_t)k, taken = 0, T = hi;
+  bool found = false;
+  for (int pass = 0; pass < 4; ++pass) {
+    const uint32_t range = hi - lo;
+    const int shift = range == 0 ? 0 : max(0, 32 - __clz(range) - 8);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) hist[lane * 8 + j] = 0;
+    __syncwarp();
+    for (int i = lane; i < cnt; i += 32) {
+      const uint32_t dk = (uint32_t)(wb[i] >> 32);
+      if (dk >= lo && dk <= hi) atomicAdd(&hist[(dk - lo) >> shift], 1u);
+    }
+    __syncwarp();
+    uint32_t h[8], run = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { h[j] = hist[lane * 8 + j]; run += h[j]; }
+    uint32_t incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t excl = incl - run;
+    const bool mine = excl < need && incl >= need;
+    const int src = __ffs(__ballot_sync(FULL, mine)) - 1;
+    uint32_t bin = 0, before = 0, through = 0;
+    if (mine) {
+      uint32_t c = excl;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (c + h[j] >= need) { bin = lane * 8 + j; before = c; through = c + h[j]; break; }
+        c += h[j];
+      }
+    }
+    bin = __shfl_sync(FULL, bin, src);
+    before = __shfl_sync(FULL, before, src);
+    through = __shfl_sync(FULL, through, src);
+    __syncwarp();
+    const uint32_t blo = lo + (bin << shift);
+    const uint64_t bspan = (uint64_t)blo + ((1ull << shift) - 1);
+    const uint32_t bhi = (uint32_t)(bspan < hi ? bspan : hi);
+    if (taken + through <= (uint32_t)room) { T = bhi; found = true; break; }
+    if (shift == 0) break;  // one distance key holds too many entries
+    taken += before;
+    need -= before;
+    lo = blo;
+    hi = bhi;
+  }
+  if (!found) return false;
+  int out = 0;
+  for (int i0 = 0; i0 < cnt; i0 += 32) {
+    const int i = i0 + lane;
+    const uint64_t v = i < cnt ? wb[i] : kKeyPad;
+    const bool keep = i < cnt && (uint32_t)(v >> 32) <= T;
+    const uint32_t bal = __ballot_sync(FULL, keep);
+    if (keep) wb[out + __popc(bal & lt_mask)] = v;
+    out += __popc(bal);
+  }
+  __syncwarp();
+  *cnt_io = out;
+  *thr = T;
+  *thr64 = ((uint64_t)T << 32) | 0xffffffffu;  // every id at distance key T
+  if (lane == 0) atomicMin(s_thr64, (unsigned long long)*thr64);
+  return true;
+}
+
 // One warp's buffer down to exactly min(cnt, k) entries by (dist key, id);
 // the k-th key becomes the warp's threshold and is published to s_thr64.
 __device__ __forceinline__ void warp_shrink(uint64_t* wb, int* cnt_io, uint32_t* thr, uint64_t* thr64,
@@ -251,6 +336,7 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
   __shared__ int32_t red32[40];
   __shared__ unsigned long long s_thr64;
   __shared__ int s_nmerge, s_nout;
+  __shared__ int s_wcnt[SW_WARPS];
   __shared__ uint32_t s_sel[4];
 
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -268,7 +354,11 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
   const WorkItem* W = a.work + (int64_t)b * a.cap_w;
   const int nseg = a.nwork[b];
   uint64_t* fk = a.mode == 1 ? a.full_keys + (int64_t)b * a.cap_full_p2 : nullptr;
-  auto shrink = [&]() { warp_shrink(wb, &cnt, &thr, &thr64, hist, ix.pids, k, &s_thr64); };
+  // the histogram cut, with the exact id-resolving shrink for heavy ties
+  auto shrink = [&]() {
+    if (!warp_cut(wb, &cnt, &thr, &thr64, hist, k, SW_WB / 2, &s_thr64))
+      warp_shrink(wb, &cnt, &thr, &thr64, hist, ix.pids, k, &s_thr64);
+  };
 
   uint8_t* ring = dsm + sw_ring(M) + (size_t)warp * 2 * U * sw_slot(M);
   struct Slot {  // one batch position of a lane (CPA: code and cb in the ring)
@@ -373,7 +463,8 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
         }
         const uint32_t dk = f32_key(dist);
         bool pass = cur.ok && dk <= thr;
-        if (pass && dk == thr && thr64 != kKeyPad)
+        // at dk == thr the id decides unless the bound admits every id
+        if (pass && dk == thr && (uint32_t)thr64 != 0xffffffffu)
           pass = (((uint64_t)dk << 32) | (uint32_t)__ldg(ix.pids + cur.row)) < thr64;
         const uint32_t bal = __ballot_sync(FULL, pass);
         if (bal) {
@@ -416,62 +507,66 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
   }
   if (a.mode == 1) return;
 
-  // ---- final: every warp down to <= k entries with resolved ids
+  // ---- final: each warp's entries under the shared bound, ids resolved,
+  // then exactly min(total, k) of them by (dist, id) across the warps
   __syncwarp();
   if (cnt > k) shrink();
   for (int i = lane; i < cnt; i += 32) {
     const uint64_t v = wb[i];
     wb[i] = (v & 0xffffffff00000000ull) | (uint32_t)__ldg(ix.pids + (uint32_t)v);
   }
-  __syncwarp();
-  if (cnt == k) {  // this warp's k-th key bounds the final top-k
-    uint64_t mx = 0;
-    for (int i = lane; i < cnt; i += 32) mx = max(mx, (uint64_t)wb[i]);
-    for (int o = 16; o > 0; o >>= 1) mx = max(mx, (uint64_t)__shfl_xor_sync(FULL, mx, o));
-    if (lane == 0) atomicMin(&s_thr64, (unsigned long long)mx);
-  }
   __syncthreads();
-  const uint64_t T = s_thr64;
-  for (int i0 = 0; i0 < cnt; i0 += 32) {
-    const int i = i0 + lane;
-    const uint64_t v = i < cnt ? wb[i] : kKeyPad;
-    const bool keep = i < cnt && v <= T;
-    const uint32_t bal = __ballot_sync(FULL, keep);
-    int base = 0;
-    if (lane == 0 && bal) base = atomicAdd(&s_nmerge, __popc(bal));
-    base = __shfl_sync(FULL, base, 0);
-    if (keep) merge[base + __popc(bal & lt_mask)] = v;
-  }
-  __syncthreads();
-  // exactly min(nm, k) smallest by (dist, id), then one small sort
-  const int nm = s_nmerge;
-  uint64_t* fin = merge;
-  int nf = nm;
-  if (nm > k) {
-    uint32_t* bh = reinterpret_cast<uint32_t*>(sstart);  // free after the sweeps
-    uint32_t need = (uint32_t)k, eq = 0;
-    const uint32_t kd = block_select(nm, [&](int i) { return (uint32_t)(merge[i] >> 32); }, bh,
-                                     s_sel, &need, &eq);
-    uint32_t kp = 0xffffffffu;
-    if (eq != need) {
-      uint32_t eq2;
-      kp = block_select(nm, [&](int i) {
-        const uint64_t v = merge[i];
-        return (uint32_t)(v >> 32) == kd ? (uint32_t)v : 0xffffffffu;
-      }, bh, s_sel, &need, &eq2);
+  const uint64_t T = s_thr64;  // every warp's bound holds >= k entries
+  {
+    int out = 0;
+    for (int i0 = 0; i0 < cnt; i0 += 32) {
+      const int i = i0 + lane;
+      const uint64_t v = i < cnt ? wb[i] : kKeyPad;
+      const bool keep = i < cnt && v <= T;
+      const uint32_t bal = __ballot_sync(FULL, keep);
+      if (keep) wb[out + __popc(bal & lt_mask)] = v;
+      out += __popc(bal);
     }
-    const uint64_t lim = ((uint64_t)kd << 32) | kp;
-    fin = reinterpret_cast<uint64_t*>(dsm + SW_WBUF);  // free after the warp phase
+    if (lane == 0) s_wcnt[warp] = out;
+  }
+  __syncthreads();
+  uint64_t* const all = reinterpret_cast<uint64_t*>(dsm + SW_WBUF);
+  auto slot_key = [&](int i) -> uint64_t {  // slot i of the warps' buffers
+    return (i % SW_WB) < s_wcnt[i / SW_WB] ? all[i] : kKeyPad;
+  };
+  int nm = 0;
+  for (int w = 0; w < SW_WARPS; ++w) nm += s_wcnt[w];
+  uint64_t* fin = merge;
+  int nf = 0;
+  {
+    uint64_t lim = kKeyPad;
+    if (nm > k) {
+      uint32_t* bh = reinterpret_cast<uint32_t*>(sstart);  // free after the sweeps
+      uint32_t need = (uint32_t)k, eq = 0;
+      const int nslots = SW_WARPS * SW_WB;
+      const uint32_t kd = block_select(nslots, [&](int i) { return (uint32_t)(slot_key(i) >> 32); },
+                                       bh, s_sel, &need, &eq);
+      uint32_t kp = 0xffffffffu;
+      if (eq != need) {
+        uint32_t eq2;
+        kp = block_select(nslots, [&](int i) {
+          const uint64_t v = slot_key(i);
+          return (uint32_t)(v >> 32) == kd ? (uint32_t)v : 0xffffffffu;
+        }, bh, s_sel, &need, &eq2);
+      }
+      lim = ((uint64_t)kd << 32) | kp;
+    }
     if (tid == 0) s_nout = 0;
     __syncthreads();
-    for (int i0 = 0; i0 < nm; i0 += SW_THREADS) {
+    for (int i0 = 0; i0 < SW_WARPS * SW_WB; i0 += SW_THREADS) {
       const int i = i0 + tid;
-      const bool keep = i < nm && merge[i] <= lim;
+      const uint64_t v = slot_key(i);
+      const bool keep = v != kKeyPad && v <= lim;
       const uint32_t bal = __ballot_sync(FULL, keep);
       int base = 0;
       if (lane == 0 && bal) base = atomicAdd(&s_nout, __popc(bal));
       base = __shfl_sync(FULL, base, 0);
-      if (keep) fin[base + __popc(bal & lt_mask)] = merge[i];
+      if (keep) fin[base + __popc(bal & lt_mask)] = v;
     }
     __syncthreads();
     nf = s_nout;
