@@ -446,6 +446,7 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
   }
   if (om == OUT_FULL && rerank) per_q += (size_t)full_p2 * 8;
   if (!out_dev) per_q += (size_t)width * 8 + 512;
+  per_q += aligned_bytes<float>((size_t)v.M * 256);  // prebuilt LUTs
   // Probe sub-chunks (GIVF_PROBE_SUB queries): GEMM -> select -> recheck ->
   // K3a run per sub-chunk so the fp32 score matrix D they share stays in L2
   // instead of making three HBM round trips; 0 = one sub-chunk per chunk.
@@ -592,6 +593,11 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
       if (om == OUT_FULL) {
         sa.full_keys = ar.take<uint64_t>((size_t)bq * full_p2);
         sa.cap_full_p2 = full_p2;
+      }
+      if (om == OUT_TOPK && scan_mode() == 0 && scan_warp_ok(sa)) {  // prebuilt LUTs
+        float* luts = ar.take<float>((size_t)bq * v.M * 256);
+        staged(ST_SCAN, st, [&] { launch_build_luts(v, dQ, bq, luts, st); });
+        sa.luts = luts;
       }
       staged(ST_SCAN, st, [&] {
         const int mode = scan_mode();

@@ -141,7 +141,10 @@ struct ScanArgs {
   float* out_d;         // (nq, k)
   uint64_t* full_keys;  // (nq, cap_full_p2)
   int64_t cap_full_p2;
+  const float* luts;    // (nq, M, 256) built by launch_build_luts, or null: in-kernel
 };
+// K5 for a whole chunk: the inner-product LUT of every query (pq.py:147-169)
+void launch_build_luts(const IndexView& ix, const float* Q, int nq, float* luts, cudaStream_t s);
 void launch_scan(const ScanArgs& a, cudaStream_t s);
 // scan_async.cu: top-k scan with cp.async-staged code tiles; false when the
 // configuration is not covered (full mode, M not in {4, 8, 16, 32}, k > 2048)
@@ -149,6 +152,7 @@ bool launch_scan_async(const ScanArgs& a, cudaStream_t s);
 // scan_warp.cu: warp-independent sweeps (the default); false when the
 // configuration is not covered (M > 32, top-k k > 128, n >= 2^32)
 bool launch_scan_warp(const ScanArgs& a, cudaStream_t s);
+bool scan_warp_ok(const ScanArgs& a);
 // full mode: sort each query's keys and split into ids/dists rows of width `ld`
 void launch_full_finish(uint64_t* keys, int64_t cap_p2, const int64_t* stats, int nq,
                         int32_t* ids, float* dists, int64_t ld, cudaStream_t s);

@@ -342,7 +342,14 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t lt_mask = (1u << lane) - 1u;
   const int k = a.k;
-  build_lut_into(ix, a.Q + (int64_t)b * ix.d, lut, nullptr, qrot);
+  if (a.luts) {  // prebuilt for the chunk (k_build_luts): one coalesced copy
+    const uint4* src = reinterpret_cast<const uint4*>(a.luts + (int64_t)b * M * 256);
+    uint4* dst = reinterpret_cast<uint4*>(lut);
+#pragma unroll 4
+    for (int i = tid; i < M * 64; i += SW_THREADS) dst[i] = __ldg(src + i);
+  } else {
+    build_lut_into(ix, a.Q + (int64_t)b * ix.d, lut, nullptr, qrot);
+  }
   for (int i = tid; i < 256; i += SW_THREADS) ctab[i] = ix.ctab[i];
   if (tid == 0) { s_thr64 = kKeyPad; s_nmerge = 0; }
 
@@ -588,6 +595,60 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
   }
 }
 
+// LUTs of QB queries for one sub-quantizer m per CTA (grid (ceil(nq/QB), M)):
+// the m-th codebook and the queries' m-th (rotated) sub-vectors are staged in
+// shared memory; thread e owns codeword e.  Same arithmetic as
+// build_lut_into (float64 accumulation, one rounding).
+constexpr int LUT_QB = 32;
+
+__global__ void __launch_bounds__(256)
+k_build_luts(IndexView ix, const float* __restrict__ Q, int nq, float* __restrict__ luts) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const int d = ix.d, M = ix.M, ds = d / M;
+  const int m = blockIdx.y, q0 = blockIdx.x * LUT_QB;
+  const int nqb = min(LUT_QB, nq - q0);
+  float* cw = reinterpret_cast<float*>(dsm);               // 256 x ds
+  double* qs = reinterpret_cast<double*>(cw + 256 * ds);  // LUT_QB x ds (1024*ds B: aligned)
+  for (int i = threadIdx.x; i < 256 * ds; i += blockDim.x)
+    cw[i] = ix.codewords[(int64_t)m * 256 * ds + i];
+  for (int i = threadIdx.x; i < nqb * ds; i += blockDim.x) {
+    const int qb = i / ds, t = i % ds;
+    const float* q = Q + (int64_t)(q0 + qb) * d;
+    float v;
+    if (ix.rotation) {  // (R q)[m*ds + t], float64 accumulation rounded once
+      const float* r = ix.rotation + (int64_t)(m * ds + t) * d;
+      double acc = 0.0;
+      for (int j = 0; j < d; ++j) acc += (double)r[j] * (double)q[j];
+      v = (float)acc;
+    } else {
+      v = q[m * ds + t];
+    }
+    qs[i] = (double)v;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 256; e += blockDim.x) {
+    const float* c = cw + e * ds;
+    for (int qb = 0; qb < nqb; ++qb) {
+      const double* qq = qs + qb * ds;
+      double acc = 0.0;
+      for (int t = 0; t < ds; ++t) acc += (double)c[t] * qq[t];
+      luts[((int64_t)(q0 + qb) * M + m) * 256 + e] = (float)acc;
+    }
+  }
+}
+
+void launch_build_luts(const IndexView& ix, const float* Q, int nq, float* luts, cudaStream_t s) {
+  const int ds = ix.d / ix.M;
+  const size_t smem = (size_t)256 * ds * 4 + (size_t)LUT_QB * ds * 8 + 16;
+  static size_t attr = 0;
+  if (smem > attr && smem > 48 * 1024) {
+    cudaFuncSetAttribute(k_build_luts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
+  dim3 grid((nq + LUT_QB - 1) / LUT_QB, ix.M);
+  k_build_luts<<<grid, 256, smem, s>>>(ix, Q, nq, luts);
+}
+
 template <int M, int U, bool CPA>
 static void launch_warp_md(const ScanArgs& a, cudaStream_t s) {
   const size_t bytes = sw_bytes(M, 2 * U, CPA, a.ix.d);
@@ -634,9 +695,15 @@ static void launch_warp_m(const ScanArgs& a, cudaStream_t s) {
   else launch_warp_mc<M, false>(a, s);
 }
 
-bool launch_scan_warp(const ScanArgs& a, cudaStream_t s) {
+bool scan_warp_ok(const ScanArgs& a) {
   if (a.mode == 0 && (a.k > SW_KMAX || a.k < 1)) return false;
   if (a.ix.n >= (int64_t)1 << 32) return false;
+  const int M = a.ix.M;
+  return M == 4 || M == 8 || M == 12 || M == 16 || M == 24 || M == 32;
+}
+
+bool launch_scan_warp(const ScanArgs& a, cudaStream_t s) {
+  if (!scan_warp_ok(a)) return false;
   switch (a.ix.M) {  // M a multiple of 4: cp.async-able code rows
     case 4: launch_warp_m<4>(a, s); return true;
     case 8: launch_warp_m<8>(a, s); return true;
