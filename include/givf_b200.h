@@ -141,7 +141,8 @@ int64_t givf_kernel_launches(void);
 /* Per-stage device time: when enabled, every launch is bracketed by CUDA
  * events on its own stream.  Stages: 0 probe_gemm, 1 probe_select,
  * 2 probe_recheck, 3 probe_full, 4 plan, 5 scan, 6 finish (full sort /
- * scan order), 7 merge.  givf_profile_read synchronises on the recorded
+ * scan order), 7 merge, 8 lut (per-chunk LUT build).  givf_profile_read
+ * synchronises on the recorded
  * events, writes the summed milliseconds and launch counts of the first
  * `nstages` stages, and resets the accumulators. */
 int givf_profile_enable(int on);

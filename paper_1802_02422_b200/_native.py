@@ -33,7 +33,7 @@ EXPORTS = (
 )
 
 STAGES = ("probe_gemm", "probe_select", "probe_recheck", "probe_full", "plan", "scan",
-          "finish", "merge")
+          "finish", "merge", "lut")
 
 
 class IndexDesc(ctypes.Structure):

@@ -23,7 +23,7 @@ thread_local std::string g_err;
 std::atomic<int64_t> g_launches{0};
 
 // Per-stage device timing: CUDA events around every launch, on its stream.
-enum Stage { ST_GEMM, ST_SELECT, ST_RECHECK, ST_FULL, ST_PLAN, ST_SCAN, ST_FINISH, ST_MERGE, ST_N };
+enum Stage { ST_GEMM, ST_SELECT, ST_RECHECK, ST_FULL, ST_PLAN, ST_SCAN, ST_FINISH, ST_MERGE, ST_LUT, ST_N };
 struct Profiler {
   std::mutex mu;
   std::atomic<bool> on{false};
@@ -596,7 +596,7 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
       }
       if (om == OUT_TOPK && scan_mode() == 0 && scan_warp_ok(sa)) {  // prebuilt LUTs
         float* luts = ar.take<float>((size_t)bq * v.M * 256);
-        staged(ST_SCAN, st, [&] { launch_build_luts(v, dQ, bq, luts, st); });
+        staged(ST_LUT, st, [&] { launch_build_luts(v, dQ, bq, luts, st); });
         sa.luts = luts;
       }
       staged(ST_SCAN, st, [&] {

@@ -518,18 +518,20 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
   // then exactly min(total, k) of them by (dist, id) across the warps
   __syncwarp();
   if (cnt > k) shrink();
-  for (int i = lane; i < cnt; i += 32) {
-    const uint64_t v = wb[i];
-    wb[i] = (v & 0xffffffff00000000ull) | (uint32_t)__ldg(ix.pids + (uint32_t)v);
-  }
   __syncthreads();
-  const uint64_t T = s_thr64;  // every warp's bound holds >= k entries
+  // every warp's bound holds >= k entries: entries above the smallest bound
+  // are out; ids are loaded only for the survivors
+  const uint64_t T = s_thr64;
   {
     int out = 0;
     for (int i0 = 0; i0 < cnt; i0 += 32) {
       const int i = i0 + lane;
-      const uint64_t v = i < cnt ? wb[i] : kKeyPad;
-      const bool keep = i < cnt && v <= T;
+      uint64_t v = i < cnt ? wb[i] : kKeyPad;
+      bool keep = i < cnt && (v >> 32) <= (T >> 32);
+      if (keep) {
+        v = (v & 0xffffffff00000000ull) | (uint32_t)__ldg(ix.pids + (uint32_t)v);
+        keep = v <= T;
+      }
       const uint32_t bal = __ballot_sync(FULL, keep);
       if (keep) wb[out + __popc(bal & lt_mask)] = v;
       out += __popc(bal);

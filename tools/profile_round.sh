@@ -17,6 +17,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 echo "launch list rc=$?"
 $CMD > gpurun_out/plain2.log 2>&1 && \
 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_scan_warp|k_probe_gemm_tc|k_plan_approx|k_probe_select|k_plan_rescore|k_plan_scores_approx" \
-    -s 6 -c 6 -o gpurun_out/prof_full $CMD > gpurun_out/ncu_full.log 2>&1
+    -k regex:"k_scan_warp|k_probe_gemm_tc|k_plan_approx|k_probe_select|k_plan_rescore|k_plan_scores_approx|k_probe_recheck|k_build_luts" \
+    -s 8 -c 8 -o gpurun_out/prof_full $CMD > gpurun_out/ncu_full.log 2>&1
 echo "ncu full rc=$?"
