@@ -358,10 +358,11 @@ int run_probe(givf_index* ix, const Plan& pl, const float* dQ, int nq, int* regi
       launch_probe_gemm(dQ, v.centroids, v.c2f, nq, K, d, so, tmin, st);
     }, 2);
   }
+  uint32_t* tup = ar.take<uint32_t>(nq);
   staged(ST_SELECT, st, [&] {
-    launch_probe_select(so.D16, K, q2f, qscale, nq, K, pl.ps.Tmin, pl.ps.cap, tmin, ntiles, cand,
-                        cand_n, theta, st);
-  });
+    launch_probe_select(so.D16, K, q2f, qscale, nq, K, pl.ps.Tmin, pl.ps.cap, tmin, ntiles, tup,
+                        cand, cand_n, theta, st);
+  }, 2);
   const float eps_scale = tc ? kEpsScaleTC : probe_eps_scale(d);
   if (eps_out) *eps_out = eps_scale;
   staged(ST_RECHECK, st, [&] {
@@ -379,7 +380,7 @@ int run_probe(givf_index* ix, const Plan& pl, const float* dQ, int nq, int* regi
 size_t probe_bytes_per_query(const Plan& pl) {
   size_t b = aligned_bytes<int>(1) * 4 + aligned_bytes<int>(pl.P) + aligned_bytes<double>(pl.P);
   if (!pl.ps.exhaustive)
-    b += (size_t)pl.K * 2 + 3 * aligned_bytes<float>(1) + (size_t)pl.ps.cap * 4 +
+    b += (size_t)pl.K * 2 + 4 * aligned_bytes<float>(1) + (size_t)pl.ps.cap * 4 +
          aligned_bytes<float>(probe_tiles(pl.K)) +
          (size_t)tc_kpad(pl.d) * 2 + 256;
   return b;

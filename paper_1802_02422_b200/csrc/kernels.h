@@ -77,7 +77,7 @@ void launch_probe_gemm(const float* Q, const float* C, const float* c2, int nq, 
                        const ScoreOut& o, float* tmin, cudaStream_t s);
 void launch_probe_select(const uint16_t* D, int64_t ldD, const float* q2, const float* qscale,
                          int nq, int K, int Tmin, int cap, const float* tmin, int ntiles,
-                         int* cand, int* cand_n, float* theta, cudaStream_t s);
+                         uint32_t* tup, int* cand, int* cand_n, float* theta, cudaStream_t s);
 size_t probe_recheck_smem(int d, int P, int cap);
 void launch_probe_recheck(const float* Q, const float* C, int nq, int K, int d, int P,
                           const int* cand, const int* cand_n, int cap, const float* theta,

@@ -242,10 +242,42 @@ __device__ void select_bucketed(Row row, int K, int Tmin, int cap,
 // the collection overflows its buffer.
 constexpr int SEL_COLLECT = 4096;
 
+// theta_up for every query: the Tmin-th smallest of its tile-minimum keys, by
+// a 32-step binary search on the key value (one warp per query, no sort).
+__global__ void k_tile_theta(const float* __restrict__ tmin, int nq, int ntiles, int Tmin,
+                             uint32_t* __restrict__ up) {
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (b >= nq) return;
+  const float* trow = tmin + (int64_t)b * ntiles;
+  constexpr int R = 16;  // keys per lane in registers (ntiles <= 512)
+  uint32_t kr[R];
+  const bool inreg = ntiles <= 32 * R;
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    const int i = lane + 32 * j;
+    kr[j] = (inreg && i < ntiles) ? f32_key(trow[i]) : 0xffffffffu;
+  }
+  uint32_t lo = 0, hi = 0xffffffffu;
+  while (lo < hi) {
+    const uint32_t mid = lo + ((hi - lo) >> 1);
+    uint32_t c = 0;
+    if (inreg) {
+#pragma unroll
+      for (int j = 0; j < R; ++j) c += kr[j] <= mid ? 1u : 0u;
+    } else {
+      for (int i = lane; i < ntiles; i += 32) c += f32_key(__ldg(trow + i)) <= mid ? 1u : 0u;
+    }
+    c = __reduce_add_sync(0xffffffffu, c);
+    if (c >= (uint32_t)Tmin) hi = mid; else lo = mid + 1;
+  }
+  if (lane == 0) up[b] = lo;
+}
+
 __global__ void __launch_bounds__(SEL_THREADS)
 k_probe_select(const uint16_t* __restrict__ D, int64_t ldD, const float* __restrict__ q2v,
                const float* __restrict__ qscale, int K, int Tmin, int cap,
-               const float* __restrict__ tmin, int ntiles,
+               const float* __restrict__ tmin, int ntiles, const uint32_t* __restrict__ tup,
                int* __restrict__ cand, int* __restrict__ cand_n, float* __restrict__ theta) {
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ uint32_t red[40];
@@ -264,15 +296,9 @@ k_probe_select(const uint16_t* __restrict__ D, int64_t ldD, const float* __restr
     select_bucketed(row, K, Tmin, cap, out, cand_n + blockIdx.x, theta + blockIdx.x, hist);
     return;
   }
-  // 1. theta_up = Tmin-th smallest tile minimum (bitonic over <= 8192 keys)
-  uint32_t* tk = reinterpret_cast<uint32_t*>(dsm);
+  // 1. theta_up = Tmin-th smallest tile minimum (k_tile_theta)
   uint64_t* ck = reinterpret_cast<uint64_t*>(dsm + 8192 * 4);
-  const uint32_t tp2 = next_pow2((uint32_t)ntiles);
-  const float* trow = tmin + (int64_t)blockIdx.x * ntiles;
-  for (uint32_t i = tid; i < tp2; i += blockDim.x) tk[i] = i < (uint32_t)ntiles ? f32_key(trow[i]) : 0xffffffffu;
-  __syncthreads();
-  bitonic_sort_keys(tk, tp2);
-  const uint32_t up = tk[Tmin - 1];
+  const uint32_t up = tup[blockIdx.x];
   if (tid == 0) s_cnt = 0;
   __syncthreads();
   // 2. one pass over the row: collect keys <= up, track the smallest key above
@@ -536,15 +562,16 @@ void launch_probe_gemm(const float* Q, const float* C, const float* c2, int nq, 
 
 void launch_probe_select(const uint16_t* D, int64_t ldD, const float* q2, const float* qscale,
                          int nq, int K, int Tmin, int cap, const float* tmin, int ntiles,
-                         int* cand, int* cand_n, float* theta, cudaStream_t s) {
+                         uint32_t* tup, int* cand, int* cand_n, float* theta, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_probe_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     attr = true;
   }
-  if (ntiles > 8192) tmin = nullptr;  // tile keys must fit the 32 KB staging area
+  if (tmin && ntiles >= Tmin && K > cap)
+    k_tile_theta<<<(nq + 7) / 8, 256, 0, s>>>(tmin, nq, ntiles, Tmin, tup);
   k_probe_select<<<nq, SEL_THREADS, 8192 * 4 + SEL_COLLECT * 8, s>>>(
-      D, ldD, q2, qscale, K, Tmin, cap, tmin, ntiles, cand, cand_n, theta);
+      D, ldD, q2, qscale, K, Tmin, cap, tmin, ntiles, tup, cand, cand_n, theta);
 }
 
 size_t probe_recheck_smem(int d, int P, int cap) {
