@@ -670,8 +670,8 @@ static int env_int(const char* name, int dflt) {
   const char* e = getenv(name);
   return e ? atoi(e) : dflt;
 }
-static int scan_group() {  // batches summed together (GIVF_SCAN_GROUP: 1, 2, 4)
-  static int u = [] { const int v = env_int("GIVF_SCAN_GROUP", 1); return (v == 2 || v == 4) ? v : 1; }();
+static int scan_group() {  // batches summed together (GIVF_SCAN_GROUP: 1, 2)
+  static int u = [] { const int v = env_int("GIVF_SCAN_GROUP", 1); return v == 2 ? v : 1; }();
   return u;
 }
 static bool scan_cpa() {  // measured faster on C2: the default
@@ -686,7 +686,6 @@ template <int M, bool CPA>
 static void launch_warp_mc(const ScanArgs& a, cudaStream_t s) {
   switch (scan_group()) {
     case 2: launch_warp_md<M, 2, CPA>(a, s); break;
-    case 4: launch_warp_md<M, 4, CPA>(a, s); break;
     default: launch_warp_md<M, 1, CPA>(a, s); break;
   }
 }
