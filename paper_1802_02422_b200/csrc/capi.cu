@@ -742,6 +742,12 @@ int givf_index_create(const givf_index_desc* ds, int device, givf_index_t* out) 
   IndexView& v = ix->v;
   v.K = K; v.d = d; v.G = G; v.M = M; v.grouping = ds->grouping ? 1 : 0; v.n = ds->n;
   v.cmax = (float)(cmax * (1.0 + 1e-6));
+  {
+    int32_t mg = 0;
+    for (size_t i = 0; i < (size_t)K * (ds->grouping ? G : 1); ++i)
+      mg = std::max(mg, ds->group_sizes[i]);
+    v.max_gsize = mg;
+  }
   const size_t KG = (size_t)K * G;
   cudaError_t e = cudaSuccess;
 #define UP(host, count, field) \

@@ -32,6 +32,7 @@ struct IndexView {
   const int32_t* nbr;         // (K, G) or null
   const float* norm;          // (K, G) or null
   const int32_t* gsize;       // (K, G) global group sizes (budget walk)
+  int32_t max_gsize;          // largest group size
   const int64_t* lstart;      // (K, G) first local row of each slice
   const int32_t* lsize;       // (K, G) local rows of each slice (null: = gsize)
   const int32_t* llo;         // (K, G) first global slot held here (null: 0)

@@ -40,7 +40,7 @@ constexpr int PA_BUCKETS = 1024;
 constexpr int PA_SORT = 1024;     // boundary-bucket sort capacity
 constexpr int PA_SMALL = 128;     // refine further while the bucket is larger
 constexpr int PA_WCAP = 256;      // window capacity
-constexpr int PA_CAND = 2048;     // begun groups (else the exact planner)
+constexpr int PA_CAND = 1536;     // begun groups (else the exact planner)
 constexpr int PA_PSTAGE = 512;    // probed regions staged in shared memory
 constexpr int PA_U = 4;           // centroid rows in flight per 8-lane group
 // histogram cells and prefixes carry (count << 40 | weight): weights are group
@@ -82,7 +82,8 @@ __global__ void __launch_bounds__(PA_THREADS) k_plan_scores_approx(PlanArgs a) {
 struct PaSmem {
   // byte offsets into the dynamic shared block
   size_t skey, ssz, pool, wkey, wval, wlen, wrow, wnorm, qd, preg, pqc, pal, bytes;
-  __host__ __device__ PaSmem(int d, int P, int64_t total) {
+  // small: every group size < 2^16, so the staged sizes are 16-bit
+  __host__ __device__ PaSmem(int d, int P, int64_t total, bool small) {
     const bool staged = total <= PA_ITEMS;
     const bool pst = P <= PA_PSTAGE;
     size_t o = 0;
@@ -99,12 +100,15 @@ struct PaSmem {
     wrow = take((size_t)PA_WCAP * 4);
     wnorm = take((size_t)PA_WCAP * 4);
     skey = take(staged ? (size_t)PA_ITEMS * 4 : 0);
-    ssz = take(staged ? (size_t)PA_ITEMS * 4 : 0);
+    ssz = take(staged ? (size_t)PA_ITEMS * (small ? 2 : 4) : 0);
     bytes = o;
   }
 };
 
-__global__ void __launch_bounds__(PA_THREADS, 3) k_plan_approx(PlanArgs a) {
+// INLINE: the emitted groups' exact base/score are computed here (the
+// scan-order sort needs them); otherwise k_plan_rescore does it.
+template <bool INLINE>
+__global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(PlanArgs a) {
   extern __shared__ __align__(16) unsigned char dsm[];
   const IndexView& ix = a.ix;
   const int b = blockIdx.x, tid = threadIdx.x;
@@ -112,7 +116,8 @@ __global__ void __launch_bounds__(PA_THREADS, 3) k_plan_approx(PlanArgs a) {
   const int64_t total = (int64_t)P * G;
   const bool staged = total <= PA_ITEMS;
   const bool pst = P <= PA_PSTAGE;
-  const PaSmem L(d, P, total);
+  const bool small = ix.max_gsize < 65536;
+  const PaSmem L(d, P, total, small);
 
   unsigned long long* hw = reinterpret_cast<unsigned long long*>(dsm + L.pool);
   uint64_t* bkey = reinterpret_cast<uint64_t*>(hw + PA_BUCKETS);
@@ -127,6 +132,7 @@ __global__ void __launch_bounds__(PA_THREADS, 3) k_plan_approx(PlanArgs a) {
   double* qd = reinterpret_cast<double*>(dsm + L.qd);
   uint32_t* skey = reinterpret_cast<uint32_t*>(dsm + L.skey);
   int32_t* ssz = reinterpret_cast<int32_t*>(dsm + L.ssz);
+  uint16_t* ssz16 = reinterpret_cast<uint16_t*>(dsm + L.ssz);
   int32_t* preg = reinterpret_cast<int32_t*>(dsm + L.preg);
   double* pqc = reinterpret_cast<double*>(dsm + L.pqc);
   double* pal = reinterpret_cast<double*>(dsm + L.pal);
@@ -197,7 +203,8 @@ __global__ void __launch_bounds__(PA_THREADS, 3) k_plan_approx(PlanArgs a) {
       const int f = tid + t * PA_THREADS;
       if (f < total) {
         skey[f] = kk[t];
-        ssz[f] = zz[t];
+        if (small) ssz16[f] = (uint16_t)zz[t];
+        else ssz[f] = zz[t];
         kmin = min(kmin, kk[t]);
         kmax = max(kmax, kk[t]);
       }
@@ -214,7 +221,9 @@ __global__ void __launch_bounds__(PA_THREADS, 3) k_plan_approx(PlanArgs a) {
   kmin = block_min(kmin, red32);
   kmax = block_max(kmax, red32);
   auto KEY = [&](int64_t f) -> uint32_t { return staged ? skey[f] : gkey[f]; };
-  auto SIZE = [&](int64_t f) -> int64_t { return staged ? ssz[f] : ix.gsize[GI(f)]; };
+  auto SIZE = [&](int64_t f) -> int64_t {
+    return staged ? (small ? (int64_t)ssz16[f] : (int64_t)ssz[f]) : (int64_t)ix.gsize[GI(f)];
+  };
   const double qn = sqrt(q2);
   const double amax = fmax(fabs((double)key_f32(kmin)), fabs((double)key_f32(kmax)));
   const double cq = (double)a.cmax + qn;
@@ -501,7 +510,7 @@ __global__ void __launch_bounds__(PA_THREADS, 3) k_plan_approx(PlanArgs a) {
   PLAN_PHASE(5);
   // exact float64 base / score of the emitted groups (here only when the
   // scan order needs them in this CTA; else k_plan_rescore)
-  if (!a.defer_rescore) {
+  if (INLINE) {
     const int grp = tid >> 3, gl = tid & 7;
     constexpr int NG = PA_THREADS >> 3;
     const bool vec = (d & 3) == 0 && d <= 128;
@@ -548,7 +557,7 @@ __global__ void __launch_bounds__(PA_THREADS, 3) k_plan_approx(PlanArgs a) {
     st[2] = total - (int64_t)kept;
     st[3] = (int64_t)(wA + wsum);
   }
-  if (a.sort_work) {
+  if (INLINE && a.sort_work) {
     __syncthreads();
     const uint32_t wp2 = next_pow2(max(nemit, 1));
     int64_t cp2 = 1;
@@ -634,13 +643,14 @@ int launch_plan_approx(const PlanArgs& a0, cudaStream_t s) {
   PlanArgs a = a0;
   // the scan-order sort (rerank=False) needs the scores inside k_plan_approx
   a.defer_rescore = (a.ix.grouping && !a.sort_work) ? 1 : 0;
-  const PaSmem L(a.ix.d, a.P, (int64_t)a.P * a.ix.G);
-  static size_t attr = 0;
-  if (L.bytes > attr) {
-    cudaFuncSetAttribute(k_plan_approx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
-    attr = L.bytes;
+  const PaSmem L(a.ix.d, a.P, (int64_t)a.P * a.ix.G, a.ix.max_gsize < 65536);
+  auto kern = a.defer_rescore ? k_plan_approx<false> : k_plan_approx<true>;
+  static size_t attr[2] = {0, 0};
+  if (L.bytes > attr[a.defer_rescore]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
+    attr[a.defer_rescore] = L.bytes;
   }
-  k_plan_approx<<<a.nq, PA_THREADS, L.bytes, s>>>(a);
+  kern<<<a.nq, PA_THREADS, L.bytes, s>>>(a);
   if (!a.defer_rescore) return 1;
   k_plan_rescore<<<dim3(a.nq, RS_SPLIT), RS_THREADS, (size_t)a.ix.d * 8, s>>>(a);
   return 2;
