@@ -266,8 +266,10 @@ struct ProbeShape {
 ProbeShape probe_shape(int K, int P) {
   ProbeShape s;
   s.exhaustive = (P == K);
-  s.Tmin = std::min(K, P + std::max(32, P / 4));
-  s.cap = std::min(K, std::max(2 * s.Tmin, 256));
+  static const int extra = getenv("GIVF_TMIN_EXTRA") ? atoi(getenv("GIVF_TMIN_EXTRA")) : 16;
+  static const int capmin = getenv("GIVF_CAP_MIN") ? atoi(getenv("GIVF_CAP_MIN")) : 128;
+  s.Tmin = std::min(K, P + std::max(extra, P / 4));
+  s.cap = std::min(K, std::max(2 * s.Tmin, capmin));
   if (s.cap > 4096) s.exhaustive = true;  // recheck sorts in <= 4096-entry smem
   return s;
 }
