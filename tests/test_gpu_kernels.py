@@ -48,21 +48,49 @@ def test_probe_scores_within_bound(scale):
     assert ratio.max() < 0.25  # the bound holds with a 4x margin
 
 
-def test_simt_and_tensor_core_paths_agree():
-    code = (
-        "import sys, json, numpy as np; sys.path.insert(0, %r); sys.path.insert(0, %r);"
-        "import golden_io; from paper_1802_02422_b200 import SearchParams, search_batch;"
-        "fx = golden_io.load('c1like_m16');"
-        "i, d, s = search_batch(fx.index, fx.queries, SearchParams(nprobe=32, tau=0.5, candidates=3000), k=50);"
-        "print(json.dumps([i.tolist(), d.tolist(), s.tolist()]))" % (ROOT, os.path.join(ROOT, "tests")))
-    outs = []
-    for mode in ("simt", "tc"):
-        env = dict(os.environ, GIVF_PROBE=mode)
-        out = subprocess.check_output([sys.executable, "-c", code], env=env, cwd=ROOT)
-        outs.append(json.loads(out.decode().strip().splitlines()[-1]))
-    assert outs[0][0] == outs[1][0]
-    assert outs[0][2] == outs[1][2]
-    np.testing.assert_array_equal(np.array(outs[0][1]), np.array(outs[1][1]))
+_MODE_CODE = (
+    "import sys, json, numpy as np; sys.path.insert(0, %r); sys.path.insert(0, %r);"
+    "import golden_io; from paper_1802_02422_b200 import SearchParams, search_batch;"
+    "fx = golden_io.load('c1like_m16');"
+    "p = SearchParams(nprobe=32, tau=0.5, candidates=3000);"
+    "i, d, s = search_batch(fx.index, fx.queries, p, k=50);"
+    "full = search_batch(fx.index, fx.queries, p);"
+    "print(json.dumps([i.tolist(), d.tolist(), s.tolist(),"
+    " [r.ids.tolist() for r in full], [r.distances.tolist() for r in full]]))")
+
+
+def _run_mode(env_over):
+    code = _MODE_CODE % (ROOT, os.path.join(ROOT, "tests"))
+    env = dict(os.environ, **env_over)
+    out = subprocess.check_output([sys.executable, "-c", code], env=env, cwd=ROOT)
+    return json.loads(out.decode().strip().splitlines()[-1])
+
+
+@pytest.fixture(scope="module")
+def default_mode_result():
+    return _run_mode({})
+
+
+@pytest.mark.parametrize("env_over", [
+    {"GIVF_PROBE": "simt"},                        # SIMT fp32 probe GEMM
+    {"GIVF_PROBE_SUB": "5"},                       # probe + K3a in sub-chunks
+    {"GIVF_STREAMS": "2", "GIVF_CHUNK_QUERIES": "3"},  # chunks on two streams
+    {"GIVF_SCAN": "block"},                        # block-synchronous scan
+    {"GIVF_SCAN": "async"},                        # cp.async block scan
+    {"GIVF_SCAN_STAGE": "registers"},              # warp scan, register staging
+    {"GIVF_SCAN_GROUP": "2"},                      # warp scan, 2 batches summed together
+], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+def test_execution_modes_agree(env_over, default_mode_result):
+    """Every tuning knob changes how the work is scheduled, never the result:
+    top-k ids / distances / stats and the full reranked lists are identical."""
+    got = _run_mode(env_over)
+    want = default_mode_result
+    assert got[0] == want[0]
+    assert got[2] == want[2]
+    np.testing.assert_array_equal(np.array(got[1]), np.array(want[1]))
+    assert got[3] == want[3]
+    for a, b in zip(got[4], want[4]):
+        np.testing.assert_array_equal(np.array(a), np.array(b))
 
 
 def test_near_duplicate_centroids_take_the_fallback_and_stay_exact():
