@@ -142,6 +142,15 @@ struct givf_index {
   std::vector<cudaEvent_t> ev_done;
   cudaEvent_t ev_start = nullptr;
 
+  cudaStream_t side = nullptr;  // LUT builds overlap the probe / planner
+  cudaEvent_t ev_q = nullptr, ev_lut = nullptr;
+  cudaError_t ensure_side() {
+    if (side) return cudaSuccess;
+    cudaError_t e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_q, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_lut, cudaEventDisableTiming);
+    return e;
+  }
   cudaError_t ensure_streams(int n) {
     if (!ev_start) {
       cudaError_t e = cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
@@ -499,6 +508,24 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
                                cudaMemcpyHostToDevice, st));
       dQ = tmp;
     }
+    // K5 (LUTs) depends only on the queries: it runs on a side stream while
+    // the probe and the planner run here.  The event is recorded after the
+    // previous chunk's scan (stream order), so the buffer is free to rewrite.
+    float* luts = nullptr;
+    {
+      ScanArgs la{};
+      la.ix = v;
+      la.mode = om == OUT_TOPK ? 0 : 1;
+      la.k = (int)(om == OUT_TOPK ? width : 0);
+      if (om == OUT_TOPK && scan_mode() == 0 && scan_warp_ok(la)) {
+        luts = ar.take<float>((size_t)bq * v.M * 256);
+        CUDA_TRY(ix->ensure_side());
+        CUDA_TRY(cudaEventRecord(ix->ev_q, st));
+        CUDA_TRY(cudaStreamWaitEvent(ix->side, ix->ev_q, 0));
+        staged(ST_LUT, ix->side, [&] { launch_build_luts(v, dQ, bq, luts, ix->side); });
+        CUDA_TRY(cudaEventRecord(ix->ev_lut, ix->side));
+      }
+    }
     int* regions = ar.take<int>((size_t)bq * pl.P);
     double* qc2 = ar.take<double>((size_t)bq * pl.P);
 
@@ -597,9 +624,8 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
         sa.full_keys = ar.take<uint64_t>((size_t)bq * full_p2);
         sa.cap_full_p2 = full_p2;
       }
-      if (om == OUT_TOPK && scan_mode() == 0 && scan_warp_ok(sa)) {  // prebuilt LUTs
-        float* luts = ar.take<float>((size_t)bq * v.M * 256);
-        staged(ST_LUT, st, [&] { launch_build_luts(v, dQ, bq, luts, st); });
+      if (luts) {  // prebuilt on the side stream
+        CUDA_TRY(cudaStreamWaitEvent(st, ix->ev_lut, 0));
         sa.luts = luts;
       }
       staged(ST_SCAN, st, [&] {
@@ -818,6 +844,9 @@ int givf_index_destroy(givf_index_t ix) {
     cudaStreamDestroy(s);
   }
   for (auto e : ix->ev_done) cudaEventDestroy(e);
+  if (ix->side) cudaStreamDestroy(ix->side);
+  if (ix->ev_q) cudaEventDestroy(ix->ev_q);
+  if (ix->ev_lut) cudaEventDestroy(ix->ev_lut);
   if (ix->ev_start) cudaEventDestroy(ix->ev_start);
   delete ix;
   return GIVF_OK;
