@@ -51,7 +51,9 @@ struct IndexView {
 // K3a): h = f16((s~ + |q|^2) * qinv), decoded s~ = h * qscale - |q|^2, with
 // qscale = 2^e a per-query power of two that keeps (|q| + cmax)^2 / 2^e
 // <= 2^15.  The rounding adds at most kHalfRel * (|q| + cmax)^2 to every
-// score's error bound.  probe_scores (accuracy checks) keeps fp32.
+// score's error bound.  probe_scores (accuracy checks) keeps fp32.  With fp16
+// output the GEMMs' per-tile minima are fp16 codes too (uint16 in the tmin
+// buffer); the select compares codes and decodes only its outputs.
 constexpr double kHalfRel = 1.0 / 2048.0;  // fp16 half ulp, relative
 struct ScoreOut {
   float* D32 = nullptr;           // fp32 scores, or

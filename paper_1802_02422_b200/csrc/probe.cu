@@ -47,6 +47,15 @@ __global__ void k_query_scale(const float* __restrict__ Q, int nq, int d, float 
 GIVF_DEV float dec_score(uint16_t h, float scale, float q2) {
   return fmaf(__half2float(__ushort_as_half(h)), scale, -q2);
 }
+// Order-preserving 16-bit key of an fp16 code (-0 folded onto +0): the
+// select works on codes directly, decoding only its outputs.
+GIVF_DEV uint32_t key16(uint32_t h) {
+  h = (h == 0x8000u) ? 0u : h;
+  return (h & 0x8000u) ? (~h & 0xffffu) : (h | 0x8000u);
+}
+GIVF_DEV uint16_t key16_inv(uint32_t k) {
+  return (uint16_t)((k & 0x8000u) ? (k & 0x7fffu) : (~k & 0xffffu));
+}
 
 // ----------------------------------------------------------------- K1a
 // SIMT fp32 tile GEMM: 64 queries x 128 centroids per CTA, 256 threads,
@@ -127,8 +136,13 @@ k_probe_gemm(const float* __restrict__ Q, const float* __restrict__ C,
     // 16 threads (tx) share a row: reduce within each half-warp
 #pragma unroll
     for (int w = 8; w > 0; w >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, w));
-    if (HALF && qr < nq) mn = fmaf(mn, o.qscale[qr], -q2r);  // decoded
-    if (tx == 0 && qr < nq && tmin) tmin[(int64_t)qr * ntiles + blockIdx.x] = mn;
+    if (tx == 0 && qr < nq && tmin) {
+      if (HALF)  // the tile minimum's fp16 code (mn is a widened fp16 value)
+        reinterpret_cast<uint16_t*>(tmin)[(int64_t)qr * ntiles + blockIdx.x] =
+            __half_as_ushort(__float2half_rn(mn));
+      else
+        tmin[(int64_t)qr * ntiles + blockIdx.x] = mn;
+    }
   }
 }
 
@@ -242,23 +256,23 @@ __device__ void select_bucketed(Row row, int K, int Tmin, int cap,
 // the collection overflows its buffer.
 constexpr int SEL_COLLECT = 4096;
 
-// theta_up for every query: the Tmin-th smallest of its tile-minimum keys, by
-// a 32-step binary search on the key value (one warp per query, no sort).
-__global__ void k_tile_theta(const float* __restrict__ tmin, int nq, int ntiles, int Tmin,
+// theta_up for every query: the Tmin-th smallest of its tile minima (fp16
+// codes), by a 16-step binary search on the key (one warp per query, no sort).
+__global__ void k_tile_theta(const uint16_t* __restrict__ tmin, int nq, int ntiles, int Tmin,
                              uint32_t* __restrict__ up) {
   const int lane = threadIdx.x & 31;
   const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (b >= nq) return;
-  const float* trow = tmin + (int64_t)b * ntiles;
+  const uint16_t* trow = tmin + (int64_t)b * ntiles;
   constexpr int R = 16;  // keys per lane in registers (ntiles <= 512)
   uint32_t kr[R];
   const bool inreg = ntiles <= 32 * R;
 #pragma unroll
   for (int j = 0; j < R; ++j) {
     const int i = lane + 32 * j;
-    kr[j] = (inreg && i < ntiles) ? f32_key(trow[i]) : 0xffffffffu;
+    kr[j] = (inreg && i < ntiles) ? key16(trow[i]) : 0xffffffffu;
   }
-  uint32_t lo = 0, hi = 0xffffffffu;
+  uint32_t lo = 0, hi = 0xffffu;
   while (lo < hi) {
     const uint32_t mid = lo + ((hi - lo) >> 1);
     uint32_t c = 0;
@@ -266,7 +280,7 @@ __global__ void k_tile_theta(const float* __restrict__ tmin, int nq, int ntiles,
 #pragma unroll
       for (int j = 0; j < R; ++j) c += kr[j] <= mid ? 1u : 0u;
     } else {
-      for (int i = lane; i < ntiles; i += 32) c += f32_key(__ldg(trow + i)) <= mid ? 1u : 0u;
+      for (int i = lane; i < ntiles; i += 32) c += key16(__ldg(trow + i)) <= mid ? 1u : 0u;
     }
     c = __reduce_add_sync(0xffffffffu, c);
     if (c >= (uint32_t)Tmin) hi = mid; else lo = mid + 1;
@@ -277,7 +291,7 @@ __global__ void k_tile_theta(const float* __restrict__ tmin, int nq, int ntiles,
 __global__ void __launch_bounds__(SEL_THREADS)
 k_probe_select(const uint16_t* __restrict__ D, int64_t ldD, const float* __restrict__ q2v,
                const float* __restrict__ qscale, int K, int Tmin, int cap,
-               const float* __restrict__ tmin, int ntiles, const uint32_t* __restrict__ tup,
+               const void* __restrict__ tmin, int ntiles, const uint32_t* __restrict__ tup,
                int* __restrict__ cand, int* __restrict__ cand_n, float* __restrict__ theta) {
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ uint32_t red[40];
@@ -301,10 +315,11 @@ k_probe_select(const uint16_t* __restrict__ D, int64_t ldD, const float* __restr
   const uint32_t up = tup[blockIdx.x];
   if (tid == 0) s_cnt = 0;
   __syncthreads();
-  // 2. one pass over the row: collect keys <= up, track the smallest key above
+  // 2. one pass over the row: collect codes with key <= up (key16 order ==
+  // decoded order), track the smallest key above
   uint32_t ex = 0xffffffffu;
-  auto take = [&](float v, int i) {
-    uint32_t k = f32_key(v);
+  auto take = [&](uint32_t h, int i) {
+    const uint32_t k = key16(h);
     if (k <= up) {
       uint32_t p = atomicAdd(&s_cnt, 1u);
       if (p < SEL_COLLECT) ck[p] = ((uint64_t)k << 32) | (uint32_t)i;
@@ -330,13 +345,13 @@ k_probe_select(const uint16_t* __restrict__ D, int64_t ldD, const float* __restr
         const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          take(dec_score((uint16_t)(w[k] & 0xffffu), row.scale, row.q2), 8 * i + 2 * k);
-          take(dec_score((uint16_t)(w[k] >> 16), row.scale, row.q2), 8 * i + 2 * k + 1);
+          take(w[k] & 0xffffu, 8 * i + 2 * k);
+          take(w[k] >> 16, 8 * i + 2 * k + 1);
         }
       }
     }
   } else {
-    for (int i = tid; i < K; i += blockDim.x) take(row(i), i);
+    for (int i = tid; i < K; i += blockDim.x) take(__ldg(row.r + i), i);
   }
   ex = block_min(ex, red);  // also orders the collection before its use
   const uint32_t n = s_cnt;
@@ -349,7 +364,8 @@ k_probe_select(const uint16_t* __restrict__ D, int64_t ldD, const float* __restr
     for (uint32_t i = tid; i < n; i += blockDim.x) out[i] = (int)(uint32_t)ck[i];
     if (tid == 0) {
       cand_n[blockIdx.x] = (int)n;
-      theta[blockIdx.x] = ex == 0xffffffffu ? __int_as_float(0x7f800000) : key_f32(ex);
+      theta[blockIdx.x] = ex == 0xffffffffu ? __int_as_float(0x7f800000)
+                                            : dec_score(key16_inv(ex), row.scale, row.q2);
     }
     return;
   }
@@ -361,7 +377,7 @@ k_probe_select(const uint16_t* __restrict__ D, int64_t ldD, const float* __restr
   for (int i = tid; i < cap; i += blockDim.x) out[i] = (int)(uint32_t)ck[i];
   if (tid == 0) {
     cand_n[blockIdx.x] = cap;
-    theta[blockIdx.x] = key_f32((uint32_t)(ck[cap] >> 32));
+    theta[blockIdx.x] = dec_score(key16_inv((uint32_t)(ck[cap] >> 32)), row.scale, row.q2);
   }
 }
 
@@ -569,7 +585,8 @@ void launch_probe_select(const uint16_t* D, int64_t ldD, const float* q2, const 
     attr = true;
   }
   if (tmin && ntiles >= Tmin && K > cap)
-    k_tile_theta<<<(nq + 7) / 8, 256, 0, s>>>(tmin, nq, ntiles, Tmin, tup);
+    k_tile_theta<<<(nq + 7) / 8, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(tmin), nq,
+                                               ntiles, Tmin, tup);
   k_probe_select<<<nq, SEL_THREADS, 8192 * 4 + SEL_COLLECT * 8, s>>>(
       D, ldD, q2, qscale, K, Tmin, cap, tmin, ntiles, tup, cand, cand_n, theta);
 }

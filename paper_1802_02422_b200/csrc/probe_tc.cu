@@ -195,8 +195,8 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
       const int mb = u / nsplit, sp = u % nsplit;
       const int t0 = sp * per_split, t1 = min(n_tiles, t0 + per_split);
       const int q = mb * BM + quarter * 32 + lane;
-      float q2r = 0.f, ir = 1.f, sr = 1.f;  // fp16 encoding of this row
-      if (HALF && q < nq) { q2r = q2v[q]; ir = qinv[q]; sr = qscale[q]; }
+      float q2r = 0.f, ir = 1.f;  // fp16 encoding of this row
+      if (HALF && q < nq) { q2r = q2v[q]; ir = qinv[q]; }
       const float q2ir = q2r * ir;
       for (int t = t0; t < t1; ++t) {
         const int colh = t * BN + half * 128;
@@ -323,9 +323,13 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
           if (c < 3) tmem_wait_ld(rn);
         }
         const int h = t * 2 + half;  // this warp's 128-centroid tile
-        if (HALF)  // decoded like every stored score
-          mn = fmaf(fminf(__low2float(mn2), __high2float(mn2)), sr, -q2r);
-        if (q < nq && tmin && h < ntiles128) tmin[(int64_t)q * ntiles128 + h] = mn;
+        if (q < nq && tmin && h < ntiles128) {
+          if (HALF)  // the tile minimum's fp16 code
+            reinterpret_cast<uint16_t*>(tmin)[(int64_t)q * ntiles128 + h] =
+                __half_as_ushort(__hmin(__low2half(mn2), __high2half(mn2)));
+          else
+            tmin[(int64_t)q * ntiles128 + h] = mn;
+        }
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm->tm_empty[acc]);
@@ -483,8 +487,8 @@ k_probe_gemm_tc2(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       const int mb = u / nsplit, sp = u % nsplit;
       const int t0 = sp * per_split, t1 = min(n_tiles, t0 + per_split);
       const int q = (mb * 2 + half) * BM + quarter * 32 + lane;
-      float q2r = 0.f, ir = 1.f, sr = 1.f;  // fp16 encoding of this row
-      if (HALF && q < nq) { q2r = q2v[q]; ir = qinv[q]; sr = qscale[q]; }
+      float q2r = 0.f, ir = 1.f;  // fp16 encoding of this row
+      if (HALF && q < nq) { q2r = q2v[q]; ir = qinv[q]; }
       const float q2ir = q2r * ir;
       for (int t = t0; t < t1; ++t) {
         const int colh = t * BN2;
@@ -612,9 +616,13 @@ k_probe_gemm_tc2(const __grid_constant__ CUtensorMap mapA, const __grid_constant
           if (c < 3) tmem_wait_ld(rn);
         }
         const int h = t;  // the 128-centroid tile
-        if (HALF)  // decoded like every stored score
-          mn = fmaf(fminf(__low2float(mn2), __high2float(mn2)), sr, -q2r);
-        if (q < nq && tmin && h < ntiles128) tmin[(int64_t)q * ntiles128 + h] = mn;
+        if (q < nq && tmin && h < ntiles128) {
+          if (HALF)  // the tile minimum's fp16 code
+            reinterpret_cast<uint16_t*>(tmin)[(int64_t)q * ntiles128 + h] =
+                __half_as_ushort(__hmin(__low2half(mn2), __high2half(mn2)));
+          else
+            tmin[(int64_t)q * ntiles128 + h] = mn;
+        }
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm->tm_empty[acc]);
