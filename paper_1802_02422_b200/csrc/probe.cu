@@ -315,9 +315,23 @@ k_probe_select(const uint16_t* __restrict__ D, int64_t ldD, const float* __restr
   const uint32_t up = tup[blockIdx.x];
   if (tid == 0) s_cnt = 0;
   __syncthreads();
-  // 2. one pass over the row: collect codes with key <= up (key16 order ==
-  // decoded order), track the smallest key above
+  // 2. only tiles whose minimum key is <= up can hold a candidate: list them
+  // (the others' minima bound the excluded codes), then read just those
+  // tiles, collecting codes with key <= up (key16 order == decoded order)
+  // and tracking the smallest key above.
+  __shared__ uint32_t s_nt;
+  uint16_t* tl = reinterpret_cast<uint16_t*>(dsm);  // <= 8192 tile ids (aliases hist)
+  if (tid == 0) s_nt = 0;
+  __syncthreads();
   uint32_t ex = 0xffffffffu;
+  const uint16_t* trow = reinterpret_cast<const uint16_t*>(tmin) + (int64_t)blockIdx.x * ntiles;
+  for (int t = tid; t < ntiles; t += blockDim.x) {
+    const uint32_t k = key16(__ldg(trow + t));
+    if (k <= up) tl[atomicAdd(&s_nt, 1u)] = (uint16_t)t;
+    else ex = min(ex, k);
+  }
+  __syncthreads();
+  const uint32_t nt = s_nt;
   auto take = [&](uint32_t h, int i) {
     const uint32_t k = key16(h);
     if (k <= up) {
@@ -328,30 +342,25 @@ k_probe_select(const uint16_t* __restrict__ D, int64_t ldD, const float* __restr
     }
   };
   if ((K & 7) == 0 && (reinterpret_cast<uintptr_t>(row.r) & 15) == 0) {
+    // 16 threads per 128-code tile, one 16-byte load (8 codes) each
     const uint4* r8 = reinterpret_cast<const uint4*>(row.r);
     const int n8 = K >> 3;
-    constexpr int U = 4;  // 16-byte loads in flight per thread, 8 scores each
-    for (int i0 = tid; i0 < n8; i0 += U * blockDim.x) {
-      uint4 v[U];
+    for (uint32_t e0 = tid; e0 < nt * 16; e0 += blockDim.x) {
+      const int i = (int)tl[e0 >> 4] * 16 + (int)(e0 & 15);
+      if (i >= n8) continue;
+      const uint4 v = __ldg(r8 + i);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = i0 + u * blockDim.x;
-        v[u] = i < n8 ? __ldg(r8 + i) : make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = i0 + u * blockDim.x;
-        if (i >= n8) break;
-        const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          take(w[k] & 0xffffu, 8 * i + 2 * k);
-          take(w[k] >> 16, 8 * i + 2 * k + 1);
-        }
+      for (int k = 0; k < 4; ++k) {
+        take(w[k] & 0xffffu, 8 * i + 2 * k);
+        take(w[k] >> 16, 8 * i + 2 * k + 1);
       }
     }
   } else {
-    for (int i = tid; i < K; i += blockDim.x) take(__ldg(row.r + i), i);
+    for (uint32_t e0 = tid; e0 < nt * 128; e0 += blockDim.x) {
+      const int i = (int)tl[e0 >> 7] * 128 + (int)(e0 & 127);
+      if (i < K) take(__ldg(row.r + i), i);
+    }
   }
   ex = block_min(ex, red);  // also orders the collection before its use
   const uint32_t n = s_cnt;
