@@ -543,23 +543,34 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
   auto slot_key = [&](int i) -> uint64_t {  // slot i of the warps' buffers
     return (i % SW_WB) < s_wcnt[i / SW_WB] ? all[i] : kKeyPad;
   };
-  int nm = 0;
-  for (int w = 0; w < SW_WARPS; ++w) nm += s_wcnt[w];
-  uint64_t* fin = merge;
+  int nm = 0, myoff = 0;
+  for (int w = 0; w < SW_WARPS; ++w) {
+    if (w == warp) myoff = nm;
+    nm += s_wcnt[w];
+  }
+  // usually the survivors fit the merge area: gather them there so the
+  // selection below touches nm entries, not every buffer slot
+  const bool compact = nm <= SW_WARPS * SW_KMAX;
+  if (compact) {
+    for (int i = lane; i < s_wcnt[warp]; i += 32) merge[myoff + i] = wb[i];
+    __syncthreads();
+  }
+  auto key_at = [&](int i) -> uint64_t { return compact ? merge[i] : slot_key(i); };
+  const int n_in = compact ? nm : SW_WARPS * SW_WB;
+  uint64_t* fin = compact ? all : merge;
   int nf = 0;
   {
     uint64_t lim = kKeyPad;
     if (nm > k) {
       uint32_t* bh = reinterpret_cast<uint32_t*>(sstart);  // free after the sweeps
       uint32_t need = (uint32_t)k, eq = 0;
-      const int nslots = SW_WARPS * SW_WB;
-      const uint32_t kd = block_select(nslots, [&](int i) { return (uint32_t)(slot_key(i) >> 32); },
+      const uint32_t kd = block_select(n_in, [&](int i) { return (uint32_t)(key_at(i) >> 32); },
                                        bh, s_sel, &need, &eq);
       uint32_t kp = 0xffffffffu;
       if (eq != need) {
         uint32_t eq2;
-        kp = block_select(nslots, [&](int i) {
-          const uint64_t v = slot_key(i);
+        kp = block_select(n_in, [&](int i) {
+          const uint64_t v = key_at(i);
           return (uint32_t)(v >> 32) == kd ? (uint32_t)v : 0xffffffffu;
         }, bh, s_sel, &need, &eq2);
       }
@@ -567,9 +578,9 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
     }
     if (tid == 0) s_nout = 0;
     __syncthreads();
-    for (int i0 = 0; i0 < SW_WARPS * SW_WB; i0 += SW_THREADS) {
+    for (int i0 = 0; i0 < n_in; i0 += SW_THREADS) {
       const int i = i0 + tid;
-      const uint64_t v = slot_key(i);
+      const uint64_t v = i < n_in ? key_at(i) : kKeyPad;
       const bool keep = v != kKeyPad && v <= lim;
       const uint32_t bal = __ballot_sync(FULL, keep);
       int base = 0;
