@@ -523,17 +523,25 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
   // are out; ids are loaded only for the survivors
   const uint64_t T = s_thr64;
   {
-    int out = 0;
-    for (int i0 = 0; i0 < cnt; i0 += 32) {
-      const int i = i0 + lane;
+    // every id load of the warp in flight at once (cnt <= SW_WB)
+    constexpr int R = SW_WB / 32;
+    uint64_t vr[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int i = j * 32 + lane;
       uint64_t v = i < cnt ? wb[i] : kKeyPad;
-      bool keep = i < cnt && (v >> 32) <= (T >> 32);
-      if (keep) {
+      if (i < cnt && (v >> 32) <= (T >> 32))
         v = (v & 0xffffffff00000000ull) | (uint32_t)__ldg(ix.pids + (uint32_t)v);
-        keep = v <= T;
-      }
+      else
+        v = kKeyPad;
+      vr[j] = v;
+    }
+    int out = 0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const bool keep = vr[j] <= T;
       const uint32_t bal = __ballot_sync(FULL, keep);
-      if (keep) wb[out + __popc(bal & lt_mask)] = v;
+      if (keep) wb[out + __popc(bal & lt_mask)] = vr[j];
       out += __popc(bal);
     }
     if (lane == 0) s_wcnt[warp] = out;
