@@ -362,8 +362,8 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
   const int nseg = a.nwork[b];
   uint64_t* fk = a.mode == 1 ? a.full_keys + (int64_t)b * a.cap_full_p2 : nullptr;
   // the histogram cut, with the exact id-resolving shrink for heavy ties
-  auto shrink = [&]() {
-    if (!warp_cut(wb, &cnt, &thr, &thr64, hist, k, SW_WB / 2, &s_thr64))
+  auto shrink = [&](int room) {
+    if (!warp_cut(wb, &cnt, &thr, &thr64, hist, k, room, &s_thr64))
       warp_shrink(wb, &cnt, &thr, &thr64, hist, ix.pids, k, &s_thr64);
   };
 
@@ -505,7 +505,7 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
         // <= D x 32 appends per iteration: room is kept for them
         if (cnt > SW_WB - 32 * D) {
           __syncwarp();
-          shrink();
+          shrink(SW_WB / 2);
         }
       }
       if constexpr (CPA) cp_async_wait<0>();  // prefetches past pe
@@ -517,7 +517,7 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
   // ---- final: each warp's entries under the shared bound, ids resolved,
   // then exactly min(total, k) of them by (dist, id) across the warps
   __syncwarp();
-  if (cnt > k) shrink();
+  if (cnt > k) shrink(k + 32);  // tight final bound: few survivors to merge
   __syncthreads();
   // every warp's bound holds >= k entries: entries above the smallest bound
   // are out; ids are loaded only for the survivors
