@@ -108,7 +108,8 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan_score(PlanArgs a) {
 // ---- K4: tau-pruning + budget walk + work-list emission, one CTA per query.
 __global__ void __launch_bounds__(PLAN_THREADS) k_plan_select(PlanArgs a) {
   extern __shared__ __align__(16) unsigned char dsm[];
-  unsigned long long* hw = reinterpret_cast<unsigned long long*>(dsm);
+  unsigned long long* hw = reinterpret_cast<unsigned long long*>(dsm);  // (first 4 KB: u32 weights)
+  uint32_t* hw32 = reinterpret_cast<uint32_t*>(dsm);
   uint64_t* bkey = reinterpret_cast<uint64_t*>(hw + PLAN_BUCKETS);
   uint32_t* hc = reinterpret_cast<uint32_t*>(bkey + SORTCAP);
   uint32_t* bval = hc + PLAN_BUCKETS;
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan_select(PlanArgs a) {
     uint64_t range = hi - lo;
     int shift = range == 0 ? 0 : max(0, 64 - __clzll((long long)range) - 10);  // <= 1024 buckets
     uint32_t nb = (uint32_t)(range >> shift) + 1;
-    for (uint32_t i = tid; i < nb; i += blockDim.x) { hc[i] = 0; hw[i] = 0; }
+    for (uint32_t i = tid; i < nb; i += blockDim.x) { hc[i] = 0; hw32[i] = 0; }
     __syncthreads();
     for (int64_t f = tid; f < total; f += blockDim.x) {
       uint64_t sk = f64_key(sscore[f]);
@@ -166,14 +167,14 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan_select(PlanArgs a) {
       }
       uint32_t bk = (uint32_t)((key - lo) >> shift);
       atomicAdd(&hc[bk], 1u);
-      atomicAdd(&hw[bk], (unsigned long long)ssize[f]);
+      atomicAdd(&hw32[bk], (uint32_t)ssize[f]);  // 32-bit: a 64-bit shared atomic is a CAS loop
     }
     __syncthreads();
     const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;
     uint32_t b0 = tid * per, b1 = min(nb, b0 + per);
     uint32_t rc = 0;
     unsigned long long rw = 0;
-    for (uint32_t x = b0; x < b1; ++x) { rc += hc[x]; rw += hw[x]; }
+    for (uint32_t x = b0; x < b1; ++x) { rc += hc[x]; rw += hw32[x]; }
     uint32_t totc;
     unsigned long long totw;
     uint32_t pc = block_exclusive_scan(rc, red32, &totc);
@@ -187,14 +188,14 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan_select(PlanArgs a) {
       if (b0 < b1 && before_ok && after_hit) {
         uint64_t cc = c0, ww = w0;
         for (uint32_t x = b0; x < b1; ++x) {
-          if (cc + hc[x] >= kept || ww + hw[x] >= budget) {
+          if (cc + hc[x] >= kept || ww + hw32[x] >= budget) {
             s_b = (int)x;
             s_bc_before = (uint32_t)(cc - taken_c);
             s_bw_before = ww - taken_w;
             break;
           }
           cc += hc[x];
-          ww += hw[x];
+          ww += hw32[x];
         }
       }
     }

@@ -119,8 +119,14 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
   const bool small = ix.max_gsize < 65536;
   const PaSmem L(d, P, total, small);
 
-  unsigned long long* hw = reinterpret_cast<unsigned long long*>(dsm + L.pool);
-  uint64_t* bkey = reinterpret_cast<uint64_t*>(hw + PA_BUCKETS);
+  // histogram: separate 32-bit counts and weights (a 64-bit shared atomic
+  // is a CAS loop); bucket weights are sums of group sizes < 2^32
+  uint32_t* hcn = reinterpret_cast<uint32_t*>(dsm + L.pool);
+  uint32_t* hwt = hcn + PA_BUCKETS;
+  auto HW = [&](uint32_t x) -> unsigned long long {
+    return ((unsigned long long)hcn[x] << CW) | hwt[x];
+  };
+  uint64_t* bkey = reinterpret_cast<uint64_t*>(dsm + L.pool) + PA_BUCKETS;
   uint32_t* cf = reinterpret_cast<uint32_t*>(dsm + L.pool);  // begun groups: flat
   int32_t* cl = reinterpret_cast<int32_t*>(cf + PA_CAND);     //   length; after emission: row
   int32_t* cp = cl + PA_CAND;                                 //   after emission: norm bits | p
@@ -245,18 +251,20 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
     const uint32_t range = hi - lo;
     const int shift = range == 0 ? 0 : max(0, 32 - __clz(range) - 10);  // <= 1024 buckets
     const uint32_t nb = (range >> shift) + 1;
-    for (uint32_t i = tid; i < nb; i += PA_THREADS) hw[i] = 0;
+    for (uint32_t i = tid; i < nb; i += PA_THREADS) { hcn[i] = 0; hwt[i] = 0; }
     __syncthreads();
     for (int64_t f = tid; f < total; f += PA_THREADS) {
       const uint32_t k = KEY(f);
       if (k < lo || k > hi) continue;
-      atomicAdd(&hw[(k - lo) >> shift], (1ull << CW) | (unsigned long long)SIZE(f));
+      const uint32_t bk = (k - lo) >> shift;
+      atomicAdd(&hcn[bk], 1u);
+      atomicAdd(&hwt[bk], (uint32_t)SIZE(f));
     }
     __syncthreads();
     constexpr uint32_t PER = PA_BUCKETS / PA_THREADS;
     const uint32_t b0 = tid * PER, b1 = min(nb, b0 + PER);
     unsigned long long rs = 0;
-    for (uint32_t x = b0; x < b1; ++x) rs += hw[x];
+    for (uint32_t x = b0; x < b1; ++x) rs += HW(x);
     unsigned long long tot;
     const unsigned long long ps = block_exclusive_scan(rs, red64, &tot);
     if (tid == 0) s_b = -1;
@@ -267,7 +275,7 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
       if (b0 < b1 && c0 < kept && w0 < budget && (c1 >= kept || w1 >= budget)) {
         unsigned long long acc = ps;
         for (uint32_t x = b0; x < b1; ++x) {
-          const unsigned long long nx = acc + hw[x];
+          const unsigned long long nx = acc + HW(x);
           if (taken_c + (nx >> CW) >= kept || taken_w + (nx & WMASK) >= budget) {
             s_b = (int)x;
             s_before = acc;
@@ -283,7 +291,7 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
       no_cut = true;
       break;
     }
-    const uint32_t cnt_b = (uint32_t)(hw[bsel] >> CW);
+    const uint32_t cnt_b = hcn[bsel];
     const uint32_t bl = lo + ((uint32_t)bsel << shift);
     const uint64_t bspan = (uint64_t)bl + ((1ull << shift) - 1);
     const uint32_t bh = (uint32_t)(bspan < hi ? bspan : hi);

@@ -19,7 +19,7 @@ def main(rep, kregex, obj, mangled, n=40):
     rows = list(csv.reader(io.StringIO(sass)))
     hi = [i for i, r in enumerate(rows) if r and r[0] == "Address"][0]
     hdr = rows[hi]
-    data = [r for r in rows[hi + 1:] if len(r) == len(hdr)]
+    data = [r for r in rows[hi + 1:] if len(r) == len(hdr) and r[0].startswith("0x")]
     ix = {h: i for i, h in enumerate(hdr)}
     with tempfile.TemporaryDirectory() as td:
         subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(obj)], cwd=td,
