@@ -76,7 +76,7 @@ def test_topk_matches_oracle(fx):
         if not run.params.rerank:
             continue
         p = _params(run.params)
-        for k in (1, 10, 100):
+        for k in (1, 10, 100, 128, 129, 300):  # 129+: the block scan's top-k path
             ids, d, st = search_batch(fx.index, fx.queries, p, k=k)
             want_i, want_d, want_s = so.search_topk(fx.index, fx.queries, so.Params(**vars(run.params)), k)
             np.testing.assert_array_equal(st, want_s)
