@@ -257,22 +257,30 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
               hp[i] = *reinterpret_cast<const uint32_t*>(&h);
             }
             if (use_tma_store) {
-              if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-              __syncwarp();
-              // 32 rows x 64 B, SWIZZLE_64B: chunk k of row r at k ^ ((r >> 1) & 3)
+              // two 32-column chunks per 32 x 64 staging tile (128 B rows,
+              // SWIZZLE_128B: 16-byte chunk k of row r at k ^ (r & 7)), one
+              // TMA store per pair of chunks
+              if ((c & 1) == 0) {
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                __syncwarp();
+              }
 #pragma unroll
-              for (int k = 0; k < 4; ++k)
-                *reinterpret_cast<uint4*>(sb + lane * 64 + ((k ^ ((lane >> 1) & 3)) * 16)) =
+              for (int k = 0; k < 4; ++k) {
+                const int kk = (c & 1) * 4 + k;
+                *reinterpret_cast<uint4*>(sb + lane * 128 + ((kk ^ (lane & 7)) * 16)) =
                     make_uint4(hp[4 * k], hp[4 * k + 1], hp[4 * k + 2], hp[4 * k + 3]);
-              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-              __syncwarp();
-              if (lane == 0) {
-                asm volatile(
-                    "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                        reinterpret_cast<uint64_t>(&mapD)),
-                    "r"(col0), "r"(mb * BM + quarter * 32), "r"(smem_u32(sb))
-                    : "memory");
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+              }
+              if (c & 1) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
+                  asm volatile(
+                      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                          reinterpret_cast<uint64_t>(&mapD)),
+                      "r"(col0 - 32), "r"(mb * BM + quarter * 32), "r"(smem_u32(sb))
+                      : "memory");
+                  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
               }
             } else if (q < nq) {
               if (col0 + 32 <= K && (ldD & 7) == 0) {
@@ -698,16 +706,17 @@ bool make_map(CUtensorMap* m, const void* ptr, int64_t rows, int cols, int pitch
 // Score matrix (rows x cols, pitch ld elements) written in 32 x 32 boxes from
 // swizzled staging tiles: fp32 (128 B rows, SWIZZLE_128B) or fp16 (64 B
 // rows, SWIZZLE_64B).
-bool make_map_out(CUtensorMap* m, void* ptr, int64_t rows, int cols, int64_t ld, bool half) {
+bool make_map_out(CUtensorMap* m, void* ptr, int64_t rows, int cols, int64_t ld, bool half,
+                  int half_box = 32) {
   auto enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)ld * (half ? 2 : 4)};
-  cuuint32_t box[2] = {32, 32};
+  cuuint32_t box[2] = {(cuuint32_t)(half ? half_box : 32), 32};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(m, half ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                    ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   half ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   (half && half_box == 32) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -772,7 +781,8 @@ bool launch_probe_gemm_tc(const void* Abf, const void* Bbf, const float* c2, int
   // scores go out through TMA stores when the row pitch allows it (16 B)
   void* dptr = half ? (void*)o.D16 : (void*)o.D32;
   int use_tma_store = ((o.ld * (half ? 2 : 4)) % 16 == 0) ? 1 : 0;
-  if (use_tma_store && !make_map_out(&md, dptr, nq, K, o.ld, half)) use_tma_store = 0;
+  if (use_tma_store && !make_map_out(&md, dptr, nq, K, o.ld, half, pair ? 32 : 64))
+    use_tma_store = 0;
   if (!use_tma_store) md = ma;  // unused
   const int KC = kcols / box_k;
   const int m_units = pair ? (nq + 2 * tc::BM - 1) / (2 * tc::BM) : (nq + tc::BM - 1) / tc::BM;
