@@ -40,6 +40,16 @@ WORKLOADS = {
     "c1": dict(n=1_000_000, d=96, n_clusters=4096, k=4096, l=64, m=8, nq=1000,
                nprobe=32, tau=0.5, candidates=10_000, topk=100, kmeans_iters=10, pq_iters=15,
                n_learn=100_000),
+    # BASELINE.json configs[2] on one B200 (1B x 96, K = 2^20, M = 16; the
+    # 8-GPU layout shards these lists).  Built with TF32 assignments, 8M learn
+    # rows and 3 Lloyd iterations so the build fits a session.
+    "c3": dict(n=1_000_000_000, d=96, n_clusters=1 << 20, k=1 << 20, l=64, m=16, nq=10_000,
+               nprobe=64, tau=0.5, candidates=10_000, topk=100, kmeans_iters=3, pq_iters=8,
+               n_learn=8_000_000, fast=True),
+    # a smaller rehearsal of the c3 build path
+    "c3mini": dict(n=50_000_000, d=96, n_clusters=1 << 18, k=1 << 18, l=64, m=16, nq=10_000,
+                   nprobe=64, tau=0.5, candidates=10_000, topk=100, kmeans_iters=3, pq_iters=8,
+                   n_learn=2_000_000, fast=True),
 }
 
 
@@ -82,7 +92,8 @@ def load_or_build(w, noise, seed, device, allow_build=True):
     t0 = time.perf_counter()
     data = SynthSpec(d=w["d"], n_clusters=w["n_clusters"], sigma=0.3, noise=noise, seed=seed)
     spec = BuildSpec(n=w["n"], k=w["k"], l=w["l"], m=w["m"], n_learn=w["n_learn"],
-                     kmeans_iters=w["kmeans_iters"], pq_iters=w["pq_iters"], seed=seed)
+                     kmeans_iters=w["kmeans_iters"], pq_iters=w["pq_iters"], seed=seed,
+                     fast=w.get("fast", False))
     arr, queries, gt = build_synthetic(data, spec, w["nq"], gt_t=10, device=device, log=log)
     build_s = time.perf_counter() - t0
     try:
@@ -260,6 +271,7 @@ def run_ours(args, w):
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     launches0 = _native.kernel_launches()
     fb0 = sx.dev.fallback_counts()
+    rs0 = sx.dev.plan_fallback_reasons()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -275,6 +287,8 @@ def run_ours(args, w):
     launches = _native.kernel_launches() - launches0
     fb1 = sx.dev.fallback_counts()
     fallbacks = {k_: (fb1[k_] - fb0[k_]) / args.steps for k_ in fb0}
+    rs1 = sx.dev.plan_fallback_reasons()
+    plan_reasons = {k_: (rs1[k_] - rs0[k_]) / args.steps for k_ in rs0 if rs1[k_] > rs0[k_]}
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = float(np.sum(step_ms))
     if world > 1:
@@ -372,7 +386,7 @@ def run_ours(args, w):
         "dtype": "f32/f64 (u8 codes)",
         "data": f"synthetic: seeded gaussian mixture, noise={args.noise}, built on GPU",
         "config": {
-            "workload": f"BASELINE configs[{1 if args.workload == 'c2' else 0}] ({args.workload})",
+            "workload": f"BASELINE configs[{ {'c1': 0, 'c2': 1}.get(args.workload, 2)}] ({args.workload})",
             "n": w["n"], "d": w["d"], "K": w["k"], "L": w["l"], "M": w["m"],
             "queries_per_step": nq, "nprobe": w["nprobe"], "tau": w["tau"],
             "candidates": w["candidates"], "k": k, "noise": args.noise,
@@ -403,6 +417,7 @@ def run_ours(args, w):
         "stage_ms_per_step": step_stage_ms,
         "gpu_launches": int(launches),
         "fallback_queries_per_step": fallbacks,
+        "plan_fallback_reasons_per_step": plan_reasons,
         "e2e": {"value": e2e_qps, "unit": "queries/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
         "clocks": clocks.summary(),

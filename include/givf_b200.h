@@ -102,7 +102,11 @@ int64_t givf_index_device_bytes(givf_index_t index);
 /* Cumulative counts of queries that left the fast path: out[0] = probe
  * candidate sets the float64 re-check could not certify (exhaustive ranking
  * ran instead), out[1] = approximate plans that fell back to the exact
- * planner.  Synchronises the device. */
+ * planner; out[2..7] split out[1] by reason: 2 = more than 1024 equal
+ * approximate keys at the cut, 3 = more than 256 groups in the +-3E window,
+ * 4 = exact crossing before the window, 5 = crossing outside +-2E of v*,
+ * 6 = walk not ended inside the window, 7 = too many begun groups for the
+ * in-CTA rescore.  Synchronises the device. */
 int givf_index_counters(givf_index_t index, int64_t* out, int32_t n);
 
 /* queries (nq, dim) f32.  ids (nq, k) int32 padded with -1, dists (nq, k)

@@ -95,12 +95,19 @@ def synth_rows(spec: SynthSpec, tag: str, start: int, count: int, means=None,
 # ---------------------------------------------------------------- primitives
 
 
+# Fast builds (1B-row benchmark indexes) let the nearest-centroid matmuls use
+# TF32 tensor cores; assignments may then differ from exact fp32 ones at
+# near-ties.  The index is still a valid GroupedIndex -- the search path and
+# its parity do not depend on how the index was built.
+FAST_BUILD = False
+
+
 class _NoTF32:
     def __enter__(self):
         self.a = torch.backends.cuda.matmul.allow_tf32
         self.b = torch.backends.cudnn.allow_tf32
-        torch.backends.cuda.matmul.allow_tf32 = False
-        torch.backends.cudnn.allow_tf32 = False
+        torch.backends.cuda.matmul.allow_tf32 = FAST_BUILD
+        torch.backends.cudnn.allow_tf32 = FAST_BUILD
 
     def __exit__(self, *exc):
         torch.backends.cuda.matmul.allow_tf32 = self.a
@@ -142,6 +149,12 @@ def kmeans(x: torch.Tensor, k: int, iters: int, seed: int) -> torch.Tensor:
         sums.index_add_(0, labels, x.double())
         counts = torch.bincount(labels, minlength=k)
         cent = (sums / counts.clamp_min(1)[:, None]).float()
+        if FAST_BUILD:  # re-seed empty clusters at random points, vectorised
+            empty = torch.nonzero(counts == 0).flatten()
+            if empty.numel():
+                cent[empty] = x[torch.randint(0, n, (empty.numel(),), generator=g,
+                                              device=x.device)]
+            continue
         empty = torch.nonzero(counts == 0).flatten().tolist()
         for e in empty:
             donor = int(torch.argmax(counts))
@@ -339,6 +352,7 @@ class BuildSpec:
     kmeans_iters: int = 10
     pq_iters: int = 15
     seed: int = 0
+    fast: bool = False          # TF32 assignment matmuls (1B-scale builds)
 
     def learn_rows(self) -> int:
         return self.n_learn or max(100_000, 32 * self.k)
@@ -352,6 +366,8 @@ def build_synthetic(data: SynthSpec, spec: BuildSpec, n_queries: int, gt_t: int 
     """
     import time
 
+    global FAST_BUILD
+    FAST_BUILD = spec.fast
     t0 = time.perf_counter()
     means = cluster_means(data, device)
     learn = synth_rows(data, "learn", 0, spec.learn_rows(), means, device)

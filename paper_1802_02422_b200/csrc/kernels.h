@@ -31,6 +31,7 @@ struct IndexView {
   const float* alphas;        // (K)
   const int32_t* nbr;         // (K, G) or null
   const float* norm;          // (K, G) or null
+  const float* rneg;          // (K) max(0, max_g -norm[r, g]) or null
   const int32_t* gsize;       // (K, G) global group sizes (budget walk)
   int32_t max_gsize;          // largest group size
   const int64_t* lstart;      // (K, G) first local row of each slice

@@ -165,10 +165,14 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
     q2p += x * x;
   }
   double alx = 0.0;  // max |alpha| over the probed regions
+  double aln = 0.0;  // min alpha
+  double nng = 0.0;  // max -norm term over the probed regions' groups
   for (int p = tid; p < P; p += PA_THREADS) {
     const int r = greg[p];
     const double al = ix.grouping ? (double)ix.alphas[r] : 0.0;
     alx = fmax(alx, fabs(al));
+    aln = fmin(aln, al);
+    if (ix.rneg) nng = fmax(nng, (double)ix.rneg[r]);
     if (pst) {
       preg[p] = r;
       pqc[p] = gqc[p];
@@ -224,6 +228,8 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
   }
   const double q2 = block_sum(q2p, redd);
   alx = block_max(alx, redd);
+  aln = -block_max(-aln, redd);
+  nng = block_max(nng, redd);
   kmin = block_min(kmin, red32);
   kmax = block_max(kmax, red32);
   auto KEY = [&](int64_t f) -> uint32_t { return staged ? skey[f] : gkey[f]; };
@@ -233,13 +239,14 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
   const double qn = sqrt(q2);
   const double amax = fmax(fabs((double)key_f32(kmin)), fabs((double)key_f32(kmax)));
   const double cq = (double)a.cmax + qn;
-  // Only qs2 is approximate and it enters the score times alpha: alpha_max x
-  // (GEMM bound + fp16 storage of the neighbor scores, kHalfRel of at most
-  // (|q| + cmax)^2), + the float32 key rounding + slack
-  const double E = ix.grouping
-      ? 1.0001 * alx * ((double)a.eps_scale * ((double)a.cmax * a.cmax + 2.0 * qn * a.cmax) +
-                        1.001 * kHalfRel * cq * cq) +
-            amax * 1.2e-7 + 1e-12 * cq * cq
+  // Only qs2 is approximate and it enters the score times alpha.  Loose bound
+  // (any alpha): alpha_max x (GEMM bound + fp16 storage of the neighbor
+  // scores, kHalfRel of at most (|q| + cmax)^2), + the float32 key rounding +
+  // slack.  The tight bound (E_tight below, once v* is known) uses that the
+  // fp16 error is relative to the stored distance itself.
+  const double eps_g = (double)a.eps_scale * ((double)a.cmax * a.cmax + 2.0 * qn * a.cmax);
+  const double E_loose = ix.grouping
+      ? 1.0001 * alx * (eps_g + 1.001 * kHalfRel * cq * cq) + amax * 1.2e-7 + 1e-12 * cq * cq
       : amax * 1.2e-7;  // float32 key rounding only
   PLAN_PHASE(0);
 
@@ -247,6 +254,7 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
   uint64_t taken_c = 0, taken_w = 0;
   uint32_t lo = kmin, hi = kmax, bucket_lo = 0, bucket_hi = 0;
   bool no_cut = false, flag = false;
+  int why = 0;  // fallback reason (counters[2 + why])
   for (int level = 0; level < 4; ++level) {
     const uint32_t range = hi - lo;
     const int shift = range == 0 ? 0 : max(0, 32 - __clz(range) - 10);  // <= 1024 buckets
@@ -305,6 +313,7 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
     }
     if (shift == 0 || level == 3) {  // > PA_SORT equal approximate keys: exact planner
       flag = true;
+      why = 0;
       break;
     }
     lo = bl;
@@ -340,6 +349,23 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
   }
   PLAN_PHASE(3);
 
+  // Tight bound for alpha in [0, 1]: item i's error is at most
+  //   alpha_i (eps_g + r |qs2~_i| + 2^-24 dscale (fp16 subnormal step,
+  //   dscale < 2^-14 (|q| + cmax)^2))
+  //   + float32 key rounding,  r = kHalfRel / (1 - kHalfRel),
+  // and alpha_i qs2~_i = s_i - (1 - alpha_i) qc_i - norm_i <= s_i + nng.
+  // e(s) = Eabs + r' max(0, s + nng) is increasing and s - e(s) too, so for
+  // every item with key <= v* + 3E the error is <= e(v* + 3E) = E, and every
+  // item above lies above v* + 2E exactly: the certification below holds.
+  double E = E_loose;
+  if (ix.grouping && ix.rneg && aln >= 0.0 && alx <= 1.0 && !no_cut) {
+    const double rr = 1.001 * kHalfRel;
+    const double Eabs = 1.001 * alx * eps_g + alx * 4e-12 * cq * cq +
+                        amax * 1.2e-7 * (1.0 + rr) + 1e-12 * cq * cq;
+    const double Et = (Eabs + rr * fmax(0.0, vstar + amax * 1.2e-7 + nng)) / (1.0 - 3.0 * rr);
+    E = fmin(E, Et);
+  }
+
   // ---- 2./3. window around v*: exact scores, sorted, walked from A's prefix
   const double wlo = vstar - 3.0 * E, whi = vstar + 3.0 * E;
   if (tid == 0) s_nw = 0;
@@ -363,7 +389,7 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
     wA = cw & WMASK;
   }
   const uint32_t nw = s_nw;
-  if (nw > (uint32_t)PA_WCAP) flag = true;
+  if (nw > (uint32_t)PA_WCAP && !flag) { flag = true; why = 1; }
   int lastw = -1;
   unsigned long long wsum = 0;  // lengths of the begun window groups
   if (!flag && !no_cut) {
@@ -434,59 +460,43 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
     const int xc = s_lastb;
     if (xc < 0) {
       flag = true;  // the exact crossing precedes the window
+      why = 2;
     } else {
       lastw = xc;
       const double sx = key_to_f64(wkey[xc]);
-      if (!(sx >= vstar - 2.0 * E && sx <= vstar + 2.0 * E)) flag = true;
+      if (!(sx >= vstar - 2.0 * E && sx <= vstar + 2.0 * E)) { flag = true; why = 3; }
       const bool ended = ((uint32_t)xc + 1 < nw) || (nA + nw >= kept) || (carry >= budget);
-      if (!ended) flag = true;
+      if (!ended) { flag = true; why = 4; }
     }
   }
   const uint64_t nbegun = nA + (uint64_t)(lastw + 1);
-  if (nbegun > (uint64_t)PA_CAND) flag = true;
+  // more begun groups than the candidate arrays hold: the deferred variant
+  // streams them (below); the inline rescore needs them staged
+  const bool big = nbegun > (uint64_t)PA_CAND;
+  if (big && INLINE && !flag) { flag = true; why = 5; }
   PLAN_PHASE(4);
   if (flag) {
     if (tid == 0) {
       a.only[b] = 1;
-      if (ix.counters) atomicAdd(&ix.counters[1], 1ull);
+      if (ix.counters) {
+        atomicAdd(&ix.counters[1], 1ull);
+        atomicAdd(&ix.counters[2 + why], 1ull);
+      }
     }
     return;
   }
   if (tid == 0) a.only[b] = 0;
 
-  // ---- 5. begun groups: A (compacted in thread order) then W[0..lastw]
-  {
-    uint32_t tot;
-    uint32_t pos = block_exclusive_scan((uint32_t)my_a, red32, &tot);
-    for (int64_t f = tid; f < total; f += PA_THREADS) {
-      if ((double)key_f32(KEY(f)) < wlo) {
-        cf[pos] = (uint32_t)f;
-        cl[pos] = (int32_t)SIZE(f);
-        ++pos;
-      }
-    }
-    for (int i = tid; i <= lastw; i += PA_THREADS) {
-      cf[nA + i] = wval[i];
-      cl[nA + i] = wlen[i];
-    }
-  }
-  __syncthreads();
-  // emission: one metadata gather per begun group; positions by block scan
-  // (groups with no local rows are dropped).  Slot pos <= candidate index, so
-  // the candidate arrays are reused in place for (row, norm, p).
+  // ---- 5. emission: one metadata gather per begun group; positions by block
+  // scan (groups with no local rows are dropped)
   WorkItem* Wl = a.work + (int64_t)b * a.cap_w;
-  const int nc = (int)nbegun;
   int nemit = 0;
-  for (int c0 = 0; c0 < nc; c0 += PA_THREADS) {
-    const int c = c0 + tid;
+  auto emit_round = [&](bool valid, uint32_t f, int64_t len_g) {  // block-uniform call
     int64_t ll = 0, start = 0;
-    uint32_t f = 0;
     int32_t row = 0;
     float nrm = 0.f;
-    if (c < nc) {  // independent loads, issued together
-      f = cf[c];
+    if (valid) {  // independent loads, issued together
       const int64_t gi = GI(f);
-      const int64_t len_g = cl[c];
       const int64_t lo_ = ix.llo ? ix.llo[gi] : 0;
       const int64_t cnt_ = ix.lsize ? ix.lsize[gi] : ix.gsize[gi];
       start = ix.lstart[gi];
@@ -508,11 +518,49 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
       w.base = __hiloint2double(p, row);
       w.score = __hiloint2double(__float_as_int((float)AL(p)), __float_as_int(nrm));
       Wl[pos] = w;
-      cf[pos] = (uint32_t)row;
-      cl[pos] = __float_as_int(nrm);
-      cp[pos] = (int32_t)(f / G);
+      if (!big) {  // in place: slot pos <= candidate index
+        cf[pos] = (uint32_t)row;
+        cl[pos] = __float_as_int(nrm);
+        cp[pos] = p;
+      }
     }
     nemit += (int)tot;
+  };
+  if (!big) {
+    // A (compacted in thread order) then W[0..lastw] into the candidate arrays
+    {
+      uint32_t tot;
+      uint32_t pos = block_exclusive_scan((uint32_t)my_a, red32, &tot);
+      for (int64_t f = tid; f < total; f += PA_THREADS) {
+        if ((double)key_f32(KEY(f)) < wlo) {
+          cf[pos] = (uint32_t)f;
+          cl[pos] = (int32_t)SIZE(f);
+          ++pos;
+        }
+      }
+      for (int i = tid; i <= lastw; i += PA_THREADS) {
+        cf[nA + i] = wval[i];
+        cl[nA + i] = wlen[i];
+      }
+    }
+    __syncthreads();
+    const int nc = (int)nbegun;
+    for (int c0 = 0; c0 < nc; c0 += PA_THREADS) {
+      const int c = c0 + tid;
+      const bool v = c < nc;
+      emit_round(v, v ? cf[c] : 0u, v ? cl[c] : 0);
+    }
+  } else {
+    for (int64_t f0 = 0; f0 < total; f0 += PA_THREADS) {
+      const int64_t f = f0 + tid;
+      const bool isA = f < total && (double)key_f32(KEY(f)) < wlo;
+      emit_round(isA, (uint32_t)f, isA ? SIZE(f) : 0);
+    }
+    for (int i0 = 0; i0 <= lastw; i0 += PA_THREADS) {
+      const int i = i0 + tid;
+      const bool v = i <= lastw;
+      emit_round(v, v ? wval[i] : 0u, v ? wlen[i] : 0);
+    }
   }
   __syncthreads();
   PLAN_PHASE(5);

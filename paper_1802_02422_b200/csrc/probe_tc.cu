@@ -37,7 +37,7 @@ namespace givf {
 namespace tc {
 
 constexpr int BM = 128, BN = 256, BK = 64;  // BK bf16 = 128 B = one swizzle row
-constexpr int STAGES = 3;
+constexpr int STAGES = 3;  // B ring depth (2 when the resident A block is 6 chunks)
 constexpr int EPI_WARPS = 8;  // two per TMEM lane quarter, one 128-column half each
 // epilogue smem: TMA-store staging (one 4 KB tile per warp) + per-warp |c|^2
 constexpr uint32_t STAGE_OUT = EPI_WARPS * 4096 + EPI_WARPS * 128 * 4;
@@ -72,8 +72,9 @@ struct Smem2 {
 }  // namespace tc
 
 // smem: [A resident: KC x 16 KB][B ring: STAGES x 32 KB][barriers]
-// HALF: scores leave as fp16 (ScoreOut in kernels.h), else fp32.
-template <bool HALF>
+// HALF: scores leave as fp16 (ScoreOut in kernels.h), else fp32.  NS: B ring
+// depth (tc_stages).
+template <bool HALF, int NS>
 __global__ void __launch_bounds__(tc::THREADS, 1)
 k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                 const __grid_constant__ CUtensorMap mapD, int use_tma_store,
@@ -87,7 +88,7 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
       (reinterpret_cast<uintptr_t>(dsm) + 1023) & ~(uintptr_t)1023);
   unsigned char* smA = base;
   unsigned char* smB = base + (size_t)KC * A_CHUNK;
-  Smem* sm = reinterpret_cast<Smem*>(smB + (size_t)STAGES * B_CHUNK + STAGE_OUT);
+  Smem* sm = reinterpret_cast<Smem*>(smB + (size_t)NS * B_CHUNK + STAGE_OUT);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m_blocks = (nq + BM - 1) / BM;
@@ -96,7 +97,7 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
   const int per_split = (n_tiles + nsplit - 1) / nsplit;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&sm->full[s], 1); mbar_init(&sm->empty[s], 1); }
+    for (int s = 0; s < NS; ++s) { mbar_init(&sm->full[s], 1); mbar_init(&sm->empty[s], 1); }
     mbar_init(&sm->a_full, 1);
     mbar_init(&sm->a_empty, 1);
     for (int a = 0; a < 2; ++a) {
@@ -138,7 +139,7 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
             mbar_wait(&sm->empty[stage], phase ^ 1);
             mbar_expect_tx(&sm->full[stage], B_CHUNK);
             tma_load_2d(smB + (size_t)stage * B_CHUNK, &mapB, &sm->full[stage], kc * BK, t * BN);
-            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            if (++stage == NS) { stage = 0; phase ^= 1; }
           }
         }
       }
@@ -170,7 +171,7 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
             mma_commit(&sm->empty[stage]);  // frees the B stage once these MMAs retire
           }
           __syncwarp();
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == NS) { stage = 0; phase ^= 1; }
         }
         if (lane == 0) mma_commit(&sm->tm_full[acc]);  // accumulator ready
         __syncwarp();
@@ -187,8 +188,8 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
     const int ntiles128 = (K + 127) / 128;
     // per-warp 32x32 fp32 staging tile for the TMA store (SWIZZLE_128B: the
     // 16-byte chunk k of row r sits at chunk k ^ (r & 7))
-    unsigned char* sb = smB + (size_t)STAGES * B_CHUNK + (size_t)e * 4096;
-    float* c2s = reinterpret_cast<float*>(smB + (size_t)STAGES * B_CHUNK + EPI_WARPS * 4096) +
+    unsigned char* sb = smB + (size_t)NS * B_CHUNK + (size_t)e * 4096;
+    float* c2s = reinterpret_cast<float*>(smB + (size_t)NS * B_CHUNK + EPI_WARPS * 4096) +
                  e * 128;
     uint32_t acc = 0, acc_phase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -735,7 +736,9 @@ int num_sms() {
 
 int tc_kpad(int d) { return ((3 * d + tc::BK - 1) / tc::BK) * tc::BK; }
 
-bool tc_supported(int d) { return tc_kpad(d) <= 6 * tc::BK; }  // A block resident (<= 96 KB)
+size_t tc_smem_bytes(int d);
+// A block resident (<= 96 KB) next to the B ring and the epilogue staging
+bool tc_supported(int d) { return tc_kpad(d) <= 6 * tc::BK && tc_smem_bytes(d) <= 227 * 1024; }
 
 void launch_split_bf16(const float* x, int rows, int d, int centroid, void* out, cudaStream_t s) {
   const int Kp = tc_kpad(d);
@@ -745,9 +748,12 @@ void launch_split_bf16(const float* x, int rows, int d, int centroid, void* out,
                                       reinterpret_cast<__nv_bfloat16*>(out));
 }
 
+// B ring depth: 3, or 2 when a 6-chunk resident A block (d > 106) leaves no
+// room for the third stage
+int tc_stages(int d) { return tc_kpad(d) / tc::BK >= 6 ? 2 : tc::STAGES; }
 size_t tc_smem_bytes(int d) {
   const int KC = tc_kpad(d) / tc::BK;
-  return 1024 + (size_t)KC * tc::A_CHUNK + (size_t)tc::STAGES * tc::B_CHUNK + tc::STAGE_OUT +
+  return 1024 + (size_t)KC * tc::A_CHUNK + (size_t)tc_stages(d) * tc::B_CHUNK + tc::STAGE_OUT +
          sizeof(tc::Smem) + 64;
 }
 
@@ -792,10 +798,12 @@ bool launch_probe_gemm_tc(const void* Abf, const void* Bbf, const float* c2, int
   const int units = m_units * nsplit;
   const int grid = std::min(units, sms);
   const size_t smem = pair ? tc2_smem_bytes(d, half) : tc_smem_bytes(d);
+  const bool ns2 = tc_stages(d) == 2;
   auto kern = pair ? (half ? k_probe_gemm_tc2<true> : k_probe_gemm_tc2<false>)
-                   : (half ? k_probe_gemm_tc<true> : k_probe_gemm_tc<false>);
-  static size_t attr[4] = {0, 0, 0, 0};
-  const int slot = (pair ? 2 : 0) + (half ? 1 : 0);
+                   : (half ? (ns2 ? k_probe_gemm_tc<true, 2> : k_probe_gemm_tc<true, 3>)
+                           : (ns2 ? k_probe_gemm_tc<false, 2> : k_probe_gemm_tc<false, 3>));
+  static size_t attr[6] = {0, 0, 0, 0, 0, 0};
+  const int slot = (pair ? 2 : ns2 ? 4 : 0) + (half ? 1 : 0);
   if (attr[slot] < smem) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr[slot] = smem;

@@ -179,9 +179,17 @@ class DeviceIndex:
 
     def fallback_counts(self) -> dict:
         """Queries that left the fast path so far (probe re-check / planner)."""
-        out = np.zeros(2, np.int64)
-        _native.check(_native.load().givf_index_counters(self._h, out.ctypes.data, 2))
+        out = np.zeros(8, np.int64)
+        _native.check(_native.load().givf_index_counters(self._h, out.ctypes.data, 8))
         return {"probe": int(out[0]), "plan": int(out[1])}
+
+    def plan_fallback_reasons(self) -> dict:
+        """Approximate-planner fallbacks split by the check that failed."""
+        out = np.zeros(8, np.int64)
+        _native.check(_native.load().givf_index_counters(self._h, out.ctypes.data, 8))
+        names = ("ties", "window_overflow", "crossing_before_window", "crossing_off_center",
+                 "walk_not_ended", "too_many_groups")
+        return {n: int(v) for n, v in zip(names, out[2:8])}
 
     def close(self):
         if getattr(self, "_h", None):

@@ -31,13 +31,13 @@ def _arrays(centroids, seed=0, m=8):
         const_lo=0.0, const_hi=1.0, grouping=False)
 
 
-@pytest.mark.parametrize("scale", [1.0, 37.0])
-def test_probe_scores_within_bound(scale):
+@pytest.mark.parametrize("scale,d", [(1.0, 96), (37.0, 96), (1.0, 128), (1.0, 64), (1.0, 24)])
+def test_probe_scores_within_bound(scale, d):
     from paper_1802_02422_b200.query import probe_scores
 
     rng = np.random.default_rng(1)
-    c = (rng.standard_normal((5000, 96)) * scale).astype(np.float32)
-    q = (rng.standard_normal((300, 96)) * scale).astype(np.float32)
+    c = (rng.standard_normal((5000, d)) * scale).astype(np.float32)
+    q = (rng.standard_normal((300, d)) * scale).astype(np.float32)
     s, eps_scale = probe_scores(_arrays(c), q)
     c64, q64 = c.astype(np.float64), q.astype(np.float64)
     exact = (c64 * c64).sum(1)[None, :] - 2.0 * q64 @ c64.T
@@ -46,6 +46,34 @@ def test_probe_scores_within_bound(scale):
     ratio = np.abs(s - exact) / bound[:, None]
     print(f"max |err| / bound = {ratio.max():.3e}")
     assert ratio.max() < 0.25  # the bound holds with a 4x margin
+
+
+@pytest.mark.parametrize("family", ["aligned", "boundary", "wide"])
+@pytest.mark.parametrize("d", [32, 96, 128])
+def test_probe_bound_adversarial(family, d):
+    """Inputs that maximise the bf16-split residual and the accumulation error
+    (all products one sign, mantissas just below a bf16 rounding boundary,
+    a 2^+-6 exponent spread across columns) stay 4x inside the a-priori
+    bound the certified fast paths rely on (tools/eps_probe.py)."""
+    from paper_1802_02422_b200.query import probe_scores
+
+    rng = np.random.default_rng(7)
+    if family == "aligned":
+        c = rng.uniform(0.5, 1.0, (4096, d))
+    elif family == "boundary":
+        c = 1.0 + (2.0**-8 - 2.0**-17) * rng.integers(1, 127, (4096, d))
+    else:
+        c = rng.uniform(0.5, 1.0, (4096, d)) * 2.0 ** rng.integers(-6, 6, (1, d))
+    c = c.astype(np.float32)
+    q = c[:256].copy()
+    s, eps_scale = probe_scores(_arrays(c), q)
+    c64, q64 = c.astype(np.float64), q.astype(np.float64)
+    exact = (c64 * c64).sum(1)[None, :] - 2.0 * q64 @ c64.T
+    cmax = np.sqrt((c64 * c64).sum(1).max())
+    unit = cmax**2 + 2.0 * np.linalg.norm(q64, axis=1)[:, None] * cmax
+    ratio = np.abs(s - exact) / (eps_scale * unit)
+    print(f"{family} d={d}: max |err| / bound = {ratio.max():.3e}")
+    assert ratio.max() < 0.25
 
 
 _MODE_CODE = (
@@ -193,3 +221,23 @@ def test_parity_on_gpu_built_index(built_index, nprobe, tau, cand):
         assert_topk_equal(ids[i], d[i], wi[i], wd[i])
     r10 = so.recall_at_r(list(ids), gt, 10)
     assert r10 == so.recall_at_r(list(wi), gt, 10)
+
+
+def test_many_begun_groups_stream_without_fallback(built_index):
+    """A budget walk that begins more groups than the planner's staging arrays
+    hold (≈4.6 rows per group here, 60k-candidate budget ⇒ >10k groups) is
+    emitted by streaming, not by the exact fallback; results equal the oracle."""
+    from oracle import search_oracle as so
+    from paper_1802_02422_b200 import SearchParams, search_batch
+    from paper_1802_02422_b200.device_index import DeviceIndex
+
+    arr, q, _ = built_index
+    dev = DeviceIndex(arr)
+    p = SearchParams(nprobe=512, tau=1.0, candidates=60_000)
+    ids, d, st = search_batch(dev, q[:24], p, k=100)
+    wi, wd, ws = so.search_topk(arr, q[:24], so.Params(**vars(p)), 100)
+    np.testing.assert_array_equal(st, ws)
+    assert (st[:, 1] > 1536).all()
+    for i in range(24):
+        assert_topk_equal(ids[i], d[i], wi[i], wd[i])
+    assert dev.fallback_counts()["plan"] == 0
