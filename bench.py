@@ -7,7 +7,7 @@ BASELINE.json configs[1] (N=100M, d=96, K=2^16, L=64, M=16, 10^4 queries,
 k=100) on seeded synthetic data built on the GPU (paper_1802_02422_b200.builder).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c2|c1] [--nprobe P] [--tau T] [--candidates C]
+                    [--workload c2|c1|c3|c4|c3mini|c4mini] [--nprobe P] [--tau T] [--candidates C]
 
 N>1 runs under torchrun: every rank holds a slice of every inverted list and
 the per-rank top-k lists are all-gathered over NCCL and merged.
@@ -46,6 +46,14 @@ WORKLOADS = {
     "c3": dict(n=1_000_000_000, d=96, n_clusters=1 << 20, k=1 << 20, l=64, m=16, nq=10_000,
                nprobe=64, tau=0.5, candidates=10_000, topk=100, kmeans_iters=3, pq_iters=8,
                n_learn=8_000_000, fast=True),
+    # BASELINE.json configs[3] on one B200: 1B x 128 SIFT-like uint8 rows
+    # (builder.SynthSpec kind='sift_u8'), K = 2^20, M = 16
+    "c4": dict(n=1_000_000_000, d=128, n_clusters=1 << 20, k=1 << 20, l=64, m=16, nq=10_000,
+               nprobe=64, tau=0.5, candidates=10_000, topk=100, kmeans_iters=3, pq_iters=8,
+               n_learn=8_000_000, fast=True, kind="sift_u8"),
+    "c4mini": dict(n=50_000_000, d=128, n_clusters=1 << 18, k=1 << 18, l=64, m=16, nq=10_000,
+                   nprobe=64, tau=0.5, candidates=10_000, topk=100, kmeans_iters=3, pq_iters=8,
+                   n_learn=2_000_000, fast=True, kind="sift_u8"),
     # a smaller rehearsal of the c3 build path
     "c3mini": dict(n=50_000_000, d=96, n_clusters=1 << 18, k=1 << 18, l=64, m=16, nq=10_000,
                    nprobe=64, tau=0.5, candidates=10_000, topk=100, kmeans_iters=3, pq_iters=8,
@@ -60,9 +68,92 @@ def log(msg):
 # ---------------------------------------------------------------- workload
 
 
+BUILD_KEYS = ("n", "d", "n_clusters", "k", "l", "m", "nq", "kmeans_iters", "pq_iters", "n_learn",
+              "fast", "kind")
+
+
 def workload_key(w, noise, seed):
-    s = json.dumps({**w, "noise": noise, "seed": seed, "v": 3}, sort_keys=True)
+    """Cache key over the fields that shape the index (not the search params)."""
+    b = {k_: w[k_] for k_ in BUILD_KEYS if k_ in w}
+    s = json.dumps({**b, "noise": noise, "seed": seed, "v": 4}, sort_keys=True)
     return hashlib.blake2b(s.encode(), digest_size=8).hexdigest()
+
+
+def param_sweep(sx, q_dev, gt, w, k, settings, flush, steps=3):
+    """BASELINE configs[1]/[2] nprobe x tau sweeps on the resident index:
+    device-timed queries/sec (CUDA events, L2 flushed) and recall@10 per
+    (nprobe, tau) at the workload's candidate budget."""
+    import torch
+
+    from paper_1802_02422_b200 import SearchParams
+    from paper_1802_02422_b200.query import recall_at_r
+
+    out = []
+    nq = q_dev.shape[0]
+    for nprobe, tau in settings:
+        params = SearchParams(nprobe=nprobe, tau=tau, candidates=w["candidates"], ef_search=w["k"])
+        ids, _, stats = sx.search_topk(q_dev, params, k)  # warm-up (workspace sizing)
+        torch.cuda.synchronize()
+        ms = 0.0
+        for _ in range(steps):
+            l2_flush(flush)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            ids, _, stats = sx.search_topk(q_dev, params, k)
+            b.record()
+            torch.cuda.synchronize()
+            ms += a.elapsed_time(b)
+        ids_h = ids.cpu().numpy() if hasattr(ids, "cpu") else np.asarray(ids)
+        st_h = stats.cpu().numpy() if hasattr(stats, "cpu") else np.asarray(stats)
+        out.append({"nprobe": nprobe, "tau": tau, "candidates": w["candidates"],
+                    "qps": nq * steps / (ms / 1e3),
+                    "recall@10": recall_at_r(list(ids_h), gt, 10),
+                    "codes_scanned_mean": float(st_h[:, 3].mean())})
+        log(f"[sweep] nprobe={nprobe} tau={tau}: {out[-1]['qps']:.0f} q/s  "
+            f"r@10 {out[-1]['recall@10']:.4f}")
+    return out
+
+
+def latency_sweep(dev, queries, w, k, batches=(1, 16, 256, 4096, 10000),
+                  budgets=(10_000, 30_000, 100_000), min_queries=20_000, max_calls=400):
+    """BASELINE.json configs[4]: per-call latency of search_batch through the
+    public API (host queries in pinned memory, host results) at each query
+    batch size and candidate budget; p50/p99 over repeated calls, each on a
+    different slice of the query set, and queries/sec = batch / mean."""
+    import torch
+
+    from paper_1802_02422_b200 import SearchParams
+    from paper_1802_02422_b200.query import search_batch
+
+    out = []
+    qh = torch.from_numpy(queries).pin_memory().numpy()
+    nq = qh.shape[0]
+    for cand in budgets:
+        params = SearchParams(nprobe=w["nprobe"], tau=w["tau"], candidates=cand, ef_search=w["k"])
+        for b in batches:
+            b = min(b, nq)
+            calls = int(max(5, min(max_calls, min_queries // b)))
+            oi = torch.empty((b, k), dtype=torch.int32).pin_memory().numpy()
+            od = torch.empty((b, k), dtype=torch.float32).pin_memory().numpy()
+            os_ = torch.empty((b, 4), dtype=torch.int64).pin_memory().numpy()
+            for i in range(3):  # warm-up (workspace sizing)
+                search_batch(dev, qh[:b], params, k=k, out=(oi, od, os_))
+            lat = []
+            for i in range(calls):
+                s0 = (i * b) % max(1, nq - b + 1)
+                q = qh[s0:s0 + b]
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                search_batch(dev, q, params, k=k, out=(oi, od, os_))
+                lat.append((time.perf_counter() - t0) * 1e3)
+            lat = np.array(lat)
+            out.append({"batch": b, "candidates": cand, "calls": calls,
+                        "p50_ms": float(np.percentile(lat, 50)),
+                        "p99_ms": float(np.percentile(lat, 99)),
+                        "qps": float(b / (lat.mean() / 1e3))})
+            log(f"[sweep] cand={cand} batch={b}: p50 {out[-1]['p50_ms']:.3f} ms "
+                f"p99 {out[-1]['p99_ms']:.3f} ms  {out[-1]['qps']:.0f} q/s")
+    return out
 
 
 def load_or_build(w, noise, seed, device, allow_build=True):
@@ -90,12 +181,19 @@ def load_or_build(w, noise, seed, device, allow_build=True):
     if not allow_build:
         raise RuntimeError("workload cache missing")
     t0 = time.perf_counter()
-    data = SynthSpec(d=w["d"], n_clusters=w["n_clusters"], sigma=0.3, noise=noise, seed=seed)
+    data = SynthSpec(d=w["d"], n_clusters=w["n_clusters"], sigma=0.3, noise=noise, seed=seed,
+                     kind=w.get("kind", "gauss"))
     spec = BuildSpec(n=w["n"], k=w["k"], l=w["l"], m=w["m"], n_learn=w["n_learn"],
                      kmeans_iters=w["kmeans_iters"], pq_iters=w["pq_iters"], seed=seed,
                      fast=w.get("fast", False))
     arr, queries, gt = build_synthetic(data, spec, w["nq"], gt_t=10, device=device, log=log)
     build_s = time.perf_counter() - t0
+    import torch
+
+    torch.cuda.empty_cache()  # the build's temporaries; the index allocates its own
+    if (w["n"] > 200_000_000 and not os.environ.get("GIVF_BENCH_CACHE")
+            and int(os.environ.get("WORLD_SIZE", "1")) == 1):
+        return arr, queries, gt, build_s  # tens of GB: cache only on request
     try:
         os.makedirs(cache_dir, exist_ok=True)
         tmp = path + f".tmp{os.getpid()}.npz"
@@ -343,6 +441,12 @@ def run_ours(args, w):
         e2e_qps = nq * args.steps / e2e_t
         assert np.array_equal(oi, ids_h), "e2e results differ from the device-resident run"
 
+    sweep = latency_sweep(sx.dev, queries, w, k) if (args.latency_sweep and world == 1) else None
+    psweep = None
+    if args.sweep and world == 1:
+        settings = [(int(a), float(b)) for a, b in (x.split(":") for x in args.sweep.split(","))]
+        psweep = param_sweep(sx, q_dev, gt, w, k, settings, flush)
+
     if rank != 0:
         return None
     m = w["m"]
@@ -384,9 +488,11 @@ def run_ours(args, w):
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f32/f64 (u8 codes)",
-        "data": f"synthetic: seeded gaussian mixture, noise={args.noise}, built on GPU",
+        "data": ("synthetic: seeded SIFT-like uint8 gamma mixture, built on GPU"
+                 if w.get("kind") == "sift_u8"
+                 else f"synthetic: seeded gaussian mixture, noise={args.noise}, built on GPU"),
         "config": {
-            "workload": f"BASELINE configs[{ {'c1': 0, 'c2': 1}.get(args.workload, 2)}] ({args.workload})",
+            "workload": f"BASELINE configs[{ {'c1': 0, 'c2': 1, 'c4': 3, 'c4mini': 3}.get(args.workload, 2)}] ({args.workload})",
             "n": w["n"], "d": w["d"], "K": w["k"], "L": w["l"], "M": w["m"],
             "queries_per_step": nq, "nprobe": w["nprobe"], "tau": w["tau"],
             "candidates": w["candidates"], "k": k, "noise": args.noise,
@@ -417,6 +523,8 @@ def run_ours(args, w):
         "stage_ms_per_step": step_stage_ms,
         "gpu_launches": int(launches),
         "fallback_queries_per_step": fallbacks,
+        **({"latency_sweep": sweep} if sweep else {}),
+        **({"param_sweep": psweep} if psweep else {}),
         "plan_fallback_reasons_per_step": plan_reasons,
         "e2e": {"value": e2e_qps, "unit": "queries/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
@@ -471,6 +579,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--latency-sweep", action="store_true",
+                    help="add BASELINE configs[4]'s batch x budget latency sweep (N=1)")
+    ap.add_argument("--sweep", default="",
+                    help="extra nprobe:tau settings on the same index, e.g. 32:0.5,128:0.25 (N=1)")
     ap.add_argument("--noise", default="per_coord", choices=["per_coord", "total"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--nprobe", type=int)

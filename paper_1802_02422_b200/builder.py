@@ -44,18 +44,28 @@ def derive_seed(seed: int, tag: str) -> int:
 
 @dataclass(frozen=True)
 class SynthSpec:
-    """Isotropic Gaussian mixture around unit-norm means, rows L2-normalised
-    (BASELINE.json configs 0-2).  noise='per_coord': sigma per coordinate
-    (the literal reading); 'total': sigma/sqrt(d) per coordinate."""
+    """kind='gauss' (BASELINE.json configs 0-2): isotropic Gaussian mixture
+    around unit-norm means, rows L2-normalised; noise='per_coord': sigma per
+    coordinate (the literal reading), 'total': sigma/sqrt(d) per coordinate.
+
+    kind='sift_u8' (config 3, SIFT-like uint8): cluster profiles
+    mu_c = U8_SCALE * Gamma(0.5) per coordinate (nonnegative, heavy-tailed,
+    many near-zero coordinates); a row is clip(round(mu_c * Gamma(4)/4),
+    0, 255) -- multiplicative noise of mean 1, zeros stay zero -- stored as
+    uint8 values and widened to float32 as vecio does (vecio.py:70-71)."""
 
     d: int
     n_clusters: int
     sigma: float = 0.3
     noise: str = "per_coord"
     seed: int = 0
+    kind: str = "gauss"
 
     def coord_sigma(self) -> float:
         return self.sigma if self.noise == "per_coord" else self.sigma / math.sqrt(self.d)
+
+
+U8_SCALE = 32.0  # sift_u8 profile scale (mean coordinate 16, tail clipped at 255)
 
 
 def _gen(seed: int, device) -> torch.Generator:
@@ -66,6 +76,9 @@ def _gen(seed: int, device) -> torch.Generator:
 
 def cluster_means(spec: SynthSpec, device="cuda") -> torch.Tensor:
     g = _gen(derive_seed(spec.seed, "means"), device)
+    if spec.kind == "sift_u8":
+        a = torch.full((spec.n_clusters, spec.d), 0.5, device=device, dtype=torch.float32)
+        return U8_SCALE * torch._standard_gamma(a, generator=g)
     m = torch.randn(spec.n_clusters, spec.d, generator=g, device=device, dtype=torch.float32)
     return m / m.norm(dim=1, keepdim=True)
 
@@ -83,9 +96,13 @@ def synth_rows(spec: SynthSpec, tag: str, start: int, count: int, means=None,
     for c in range(c0, c1 + 1):
         g = _gen(derive_seed(spec.seed, f"{tag}:{c}"), device)
         lab = torch.randint(0, spec.n_clusters, (CHUNK_ROWS,), generator=g, device=device)
-        noise = torch.randn(CHUNK_ROWS, spec.d, generator=g, device=device, dtype=torch.float32)
-        x = means[lab] + s * noise
-        x = x / x.norm(dim=1, keepdim=True).clamp_min(1e-30)
+        if spec.kind == "sift_u8":
+            a = torch.full((CHUNK_ROWS, spec.d), 4.0, device=device, dtype=torch.float32)
+            x = (means[lab] * (torch._standard_gamma(a, generator=g) * 0.25)).round_().clamp_(0, 255)
+        else:
+            noise = torch.randn(CHUNK_ROWS, spec.d, generator=g, device=device, dtype=torch.float32)
+            x = means[lab] + s * noise
+            x = x / x.norm(dim=1, keepdim=True).clamp_min(1e-30)
         lo = max(start, c * CHUNK_ROWS)
         hi = min(start + count, (c + 1) * CHUNK_ROWS)
         out[lo - start: hi - start] = x[lo - c * CHUNK_ROWS: hi - c * CHUNK_ROWS]
@@ -418,6 +435,8 @@ def build_synthetic(data: SynthSpec, spec: BuildSpec, n_queries: int, gt_t: int 
         region[s:e], pick[s:e], codes[s:e], cbytes[s:e] = r.int(), p.short(), cd, b
         gt.update(x, s)
         del x, t
+        if n >= 100 * CHUNK_ROWS and (s // CHUNK_ROWS) % 100 == 99:
+            log(f"[build]   {e} rows encoded: {time.perf_counter()-t0:.1f}s")
     log(f"[build] {n} base rows assigned/encoded + ground truth: {time.perf_counter()-t0:.1f}s")
 
     groups = l if spec.grouping else 1

@@ -241,3 +241,28 @@ def test_many_begun_groups_stream_without_fallback(built_index):
     for i in range(24):
         assert_topk_equal(ids[i], d[i], wi[i], wd[i])
     assert dev.fallback_counts()["plan"] == 0
+
+
+def test_parity_sift_u8_d128():
+    """BASELINE config 3's data family at small scale: d = 128 uint8-valued
+    rows (unnormalised, distances ~1e5), M = 16; the 2-stage tensor-core
+    probe (d > 106) and the full pipeline against the oracle."""
+    import torch
+
+    from oracle import search_oracle as so
+    from paper_1802_02422_b200 import SearchParams, search_batch
+    from paper_1802_02422_b200.builder import BuildSpec, SynthSpec, build_synthetic
+
+    torch.manual_seed(0)
+    data = SynthSpec(d=128, n_clusters=700, kind="sift_u8", seed=5)
+    spec = BuildSpec(n=200_000, k=1024, l=32, m=16, n_learn=50_000, kmeans_iters=5, pq_iters=5,
+                     seed=5)
+    arr, q, gt = build_synthetic(data, spec, 64, device="cuda", log=lambda *_: None)
+    assert float(q.min()) >= 0.0 and float(q.max()) <= 255.0 and np.all(q == np.round(q))
+    for nprobe, tau, cand in [(32, 0.5, 10_000), (96, 0.25, 3_000)]:
+        p = SearchParams(nprobe=nprobe, tau=tau, candidates=cand)
+        ids, d, st = search_batch(arr, q, p, k=100)
+        wi, wd, ws = so.search_topk(arr, q, so.Params(**vars(p)), 100)
+        np.testing.assert_array_equal(st, ws)
+        for i in range(q.shape[0]):
+            assert_topk_equal(ids[i], d[i], wi[i], wd[i])
