@@ -43,11 +43,11 @@ GIVF_DEV CodeVec<M> load_code(const uint8_t* __restrict__ codes, int64_t row) {
 // ip = sum of the M LUT entries in numpy's float32 reduction order: M < 8 a
 // left-to-right sum; otherwise 8 running lanes r_j += e_{j+8i}, then
 // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the tail in order.
+// ip = sum of the M LUT entries in numpy's float32 reduction order: M < 8 a
+// left-to-right sum; otherwise 8 running lanes r_j += e_{j+8i}, then
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the tail in order.
 template <int M>
-GIVF_DEV float code_sum(const CodeVec<M>& code, const float* lut) {
-  float e[M];
-#pragma unroll
-  for (int j = 0; j < M; ++j) e[j] = lut[j * 256 + code.byte(j)];
+GIVF_DEV float numpy_sum(const float (&e)[M]) {
   if constexpr (M < 8) {
     float r = e[0];
 #pragma unroll
@@ -68,6 +68,67 @@ GIVF_DEV float code_sum(const CodeVec<M>& code, const float* lut) {
     for (int j = body; j < M; ++j) s = __fadd_rn(s, e[j]);
     return s;
   }
+}
+
+template <int M>
+GIVF_DEV float code_sum(const CodeVec<M>& code, const float* lut) {
+  float e[M];
+#pragma unroll
+  for (int j = 0; j < M; ++j) e[j] = lut[j * 256 + code.byte(j)];
+  return numpy_sum<M>(e);
+}
+
+// Bank-conflict-free LUT reads (M in {8, 16}).  The LUT is stored
+// "interleaved": xl[code * 32 + c * M + m] = LUT[m][code] for each of the
+// 32 / M copies c, so entry (m, code) of copy c sits in bank c * M + m.
+// Lane l reads copy c = l / M and, at step s, sub-quantizer m = s ^ x with
+// x = l % M: the 32 lanes of a warp hit 32 distinct banks, one wavefront per
+// step instead of ~3.1 for random codes in a [m][256] table.
+//
+// Slot s holds e_{s^x}.  XOR by a constant maps the pairs {t, t^8}, then
+// {2t, 2t+1}, {4t..4t+3}, ... onto themselves, so numpy's tree over the
+// slots adds exactly the same pairs as over e (in swapped order at most, and
+// float addition is commutative): the sum is bit-identical to code_sum.
+//
+// The row is pre-permuted so slot s reads byte s of registers: words by
+// k ^ (x >> 2), bytes inside a word by i ^ (x & 3).
+template <int M>
+GIVF_DEV CodeVec<M> xl_permute(const CodeVec<M>& c, int x) {
+  static_assert(M == 8 || M == 16, "interleaved LUT: M in {8, 16}");
+  CodeVec<M> p;
+  const int xh = x >> 2;
+  if constexpr (M == 16) {
+    uint32_t t[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) t[k] = (xh & 1) ? c.w[k ^ 1] : c.w[k];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) p.w[k] = (xh & 2) ? t[k ^ 2] : t[k];
+  } else {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) p.w[k] = (xh & 1) ? c.w[k ^ 1] : c.w[k];
+  }
+  const int xb = x & 3;
+  const uint32_t sel = (uint32_t)(xb | ((1 ^ xb) << 4) | ((2 ^ xb) << 8) | ((3 ^ xb) << 12));
+#pragma unroll
+  for (int k = 0; k < CodeVec<M>::W; ++k) p.w[k] = __byte_perm(p.w[k], 0, sel);
+  return p;
+}
+
+// lane_base = shared-window address of the interleaved LUT + the lane's copy
+// and column offset (c * M + x) * 4 (LUT base 128-byte aligned).
+template <int M>
+GIVF_DEV float code_sum_xl(const CodeVec<M>& code, uint32_t lane_base, int x) {
+  const CodeVec<M> p = xl_permute<M>(code, x);
+  float e[M];
+#pragma unroll
+  for (int s = 0; s < M; ++s) {
+    // base + (c*M + (s^x))*4 + byte*128 == (lane_base + byte*128) ^ (s*4):
+    // bits 2..5 of lane_base hold x*4 and nothing else touches them
+    const uint32_t byte = __byte_perm(p.w[s >> 2], 0, 0x4440 | (s & 3));
+    const uint32_t addr = (lane_base + (byte << 7)) ^ ((uint32_t)s << 2);
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(e[s]) : "r"(addr));
+  }
+  return numpy_sum<M>(e);
 }
 
 // LUT of one query (pq.py:147-169): optional rotation q' = R q, then

@@ -37,7 +37,7 @@ namespace givf {
 constexpr int SW_THREADS = 256;
 constexpr int SW_WARPS = SW_THREADS / 32;
 constexpr int SW_SEGS = 256;   // segments per window
-constexpr int SW_WB = 384;     // per-warp candidate buffer (dist key << 32 | row)
+constexpr int SW_WB = 256;     // per-warp candidate buffer (dist key << 32 | row)
 constexpr int SW_KMAX = 128;   // SW_WARPS * SW_KMAX merge entries
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -53,12 +53,18 @@ constexpr size_t SW_LUT = SW_CTAB + 256 * 4;                      // f32 [M][256
 // cp.async staging (CPA): per warp D slots x 32 lanes x (M code bytes + the
 // 4-byte word holding the constant byte)
 __host__ __device__ constexpr size_t sw_slot(int M) { return (size_t)32 * (M + 4); }
-__host__ __device__ constexpr size_t sw_ring(int M) { return SW_LUT + (size_t)M * 1024; }
-__host__ __device__ constexpr size_t sw_qrot(int M, int D, bool cpa) {
-  return sw_ring(M) + (cpa ? (size_t)SW_WARPS * D * sw_slot(M) : 0);
+// LUT: [M][256] f32, or (XL) the interleaved copies of code_sum_xl, 32 KB
+// (+128: the interleaved LUT's address is rounded up to 128 bytes, as the
+// XOR addressing of code_sum_xl needs; dynamic shared memory is only
+// guaranteed 16-byte alignment)
+__host__ __device__ constexpr size_t sw_lut_bytes(int M, bool xl) { return xl ? 32768 + 128 : (size_t)M * 1024; }
+__host__ __device__ constexpr size_t sw_ring(int M, bool xl) { return SW_LUT + sw_lut_bytes(M, xl); }
+__host__ __device__ constexpr size_t sw_qrot(int M, int D, bool cpa, bool xl) {
+  return sw_ring(M, xl) + (cpa ? (size_t)SW_WARPS * D * sw_slot(M) : 0);
 }
-__host__ __device__ constexpr size_t sw_bytes(int M, int D, bool cpa, int d) {
-  return sw_qrot(M, D, cpa) + (((size_t)d * 4 + 15) & ~(size_t)15);
+// qrot (in-kernel LUT build) is only needed without prebuilt LUTs (never XL)
+__host__ __device__ constexpr size_t sw_bytes(int M, int D, bool cpa, bool xl, int d) {
+  return sw_qrot(M, D, cpa, xl) + (xl ? 0 : (((size_t)d * 4 + 15) & ~(size_t)15));
 }
 
 GIVF_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -322,13 +328,15 @@ __device__ __forceinline__ void warp_shrink(uint64_t* wb, int* cnt_io, uint32_t*
   if (lane == 0) atomicMin(s_thr64, (unsigned long long)*thr64);
 }
 
-template <int M, int U, bool CPA>
+template <int M, int U, bool CPA, bool XL>
 __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
   extern __shared__ __align__(16) unsigned char dsm[];
   const IndexView& ix = a.ix;
   float* lut = reinterpret_cast<float*>(dsm + SW_LUT);
+  if constexpr (XL)  // 128-byte aligned shared-window address
+    lut += ((128u - (smem_u32(lut) & 127u)) & 127u) / 4u;
   float* ctab = reinterpret_cast<float*>(dsm + SW_CTAB);
-  float* qrot = reinterpret_cast<float*>(dsm + sw_qrot(M, 2 * U, CPA));
+  float* qrot = reinterpret_cast<float*>(dsm + sw_qrot(M, 2 * U, CPA, XL));
   uint32_t* sstart = reinterpret_cast<uint32_t*>(dsm + SW_SSTART);
   double* sbase = reinterpret_cast<double*>(dsm + SW_SBASE);
   int32_t* soff = reinterpret_cast<int32_t*>(dsm + SW_SOFF);
@@ -342,7 +350,24 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t lt_mask = (1u << lane) - 1u;
   const int k = a.k;
-  if (a.luts) {  // prebuilt for the chunk (k_build_luts): one coalesced copy
+  if constexpr (XL) {
+    // prebuilt [m][256] -> interleaved copies.  Lane (sub, m) = (l / M, l % M)
+    // reads 4 codes of row m and writes copy c = cc ^ sub: a warp's stores
+    // cover 32 distinct banks
+    constexpr int NC = 32 / M;
+    const float4* src = reinterpret_cast<const float4*>(a.luts + (int64_t)b * M * 256);
+    const int m = lane % M, sub = lane / M;
+#pragma unroll 2
+    for (int i = warp; i < M * 64 / 32; i += SW_WARPS) {
+      const int chunk = NC * i + sub;  // codes 4*chunk .. 4*chunk+3
+      const float4 v = __ldg(src + m * 64 + chunk);
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) {
+        float* dst = lut + (4 * chunk) * 32 + (cc ^ sub) * M + m;
+        dst[0] = v.x; dst[32] = v.y; dst[64] = v.z; dst[96] = v.w;
+      }
+    }
+  } else if (a.luts) {  // prebuilt for the chunk (k_build_luts): one coalesced copy
     const uint4* src = reinterpret_cast<const uint4*>(a.luts + (int64_t)b * M * 256);
     uint4* dst = reinterpret_cast<uint4*>(lut);
 #pragma unroll 4
@@ -367,7 +392,10 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
       warp_shrink(wb, &cnt, &thr, &thr64, hist, ix.pids, k, &s_thr64);
   };
 
-  uint8_t* ring = dsm + sw_ring(M) + (size_t)warp * 2 * U * sw_slot(M);
+  uint8_t* ring = dsm + sw_ring(M, XL) + (size_t)warp * 2 * U * sw_slot(M);
+  const int xl_x = lane % M;                                  // XL: column rotation
+  // XL: the lane's copy and column inside the interleaved LUT
+  const uint32_t xl_base = smem_u32(lut) + (uint32_t)((lane / M) * M + xl_x) * 4u;
   struct Slot {  // one batch position of a lane (CPA: code and cb in the ring)
     uint32_t row;
     double base;
@@ -460,7 +488,9 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
           code = cur.code;
           cb = cur.cb;
         }
-        const float ip = code_sum<M>(code, lut);
+        float ip;
+        if constexpr (XL) ip = code_sum_xl<M>(code, xl_base, xl_x);
+        else ip = code_sum<M>(code, lut);
         return (float)dadd(dsub(cur.base, 2.0 * (double)ip), (double)ctab[cb]);
       };
       auto consider = [&](const Slot& cur, float dist, int p0) {
@@ -670,16 +700,34 @@ void launch_build_luts(const IndexView& ix, const float* Q, int nq, float* luts,
   k_build_luts<<<grid, 256, smem, s>>>(ix, Q, nq, luts);
 }
 
-template <int M, int U, bool CPA>
-static void launch_warp_md(const ScanArgs& a, cudaStream_t s) {
-  const size_t bytes = sw_bytes(M, 2 * U, CPA, a.ix.d);
+template <int M, int U, bool CPA, bool XL>
+static void launch_warp_mdx(const ScanArgs& a, cudaStream_t s) {
+  const size_t bytes = sw_bytes(M, 2 * U, CPA, XL, a.ix.d);
   static size_t attr = 0;
   if (attr < bytes) {
-    cudaFuncSetAttribute(k_scan_warp<M, U, CPA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_scan_warp<M, U, CPA, XL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)bytes);
     attr = bytes;
   }
-  k_scan_warp<M, U, CPA><<<a.nq, SW_THREADS, bytes, s>>>(a);
+  k_scan_warp<M, U, CPA, XL><<<a.nq, SW_THREADS, bytes, s>>>(a);
+}
+
+// Interleaved (bank-conflict-free) LUT for M in {8, 16} with prebuilt LUTs
+// (GIVF_SCAN_LUT=plain keeps the [m][256] table)
+static bool scan_xl() {
+  static bool x = [] {
+    const char* e = getenv("GIVF_SCAN_LUT");
+    return !(e && strcmp(e, "plain") == 0);
+  }();
+  return x;
+}
+
+template <int M, int U, bool CPA>
+static void launch_warp_md(const ScanArgs& a, cudaStream_t s) {
+  if constexpr (M == 8 || M == 16) {
+    if (a.luts && scan_xl()) { launch_warp_mdx<M, U, CPA, true>(a, s); return; }
+  }
+  launch_warp_mdx<M, U, CPA, false>(a, s);
 }
 
 // Batches summed together per warp (GIVF_SCAN_GROUP, default 1; twice that

@@ -108,6 +108,7 @@ def default_mode_result():
     {"GIVF_SCAN": "async"},                        # cp.async block scan
     {"GIVF_SCAN_STAGE": "registers"},              # warp scan, register staging
     {"GIVF_SCAN_GROUP": "2"},                      # warp scan, 2 batches summed together
+    {"GIVF_SCAN_LUT": "plain"},                    # warp scan, [m][256] LUT (bank conflicts)
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_execution_modes_agree(env_over, default_mode_result):
     """Every tuning knob changes how the work is scheduled, never the result:
