@@ -328,7 +328,8 @@ __device__ __forceinline__ void warp_shrink(uint64_t* wb, int* cnt_io, uint32_t*
   if (lane == 0) atomicMin(s_thr64, (unsigned long long)*thr64);
 }
 
-template <int M, int U, bool CPA, bool XL>
+// FULLK: every scanned key to full_keys (mode 1), else top-k (mode 0)
+template <int M, int U, bool CPA, bool XL, bool FULLK>
 __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
   extern __shared__ __align__(16) unsigned char dsm[];
   const IndexView& ix = a.ix;
@@ -383,9 +384,15 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
   int cnt = 0;
   uint32_t thr = 0xffffffffu;
   uint64_t thr64 = kKeyPad;
+  // the bound as a float (+inf while it admits everything)
+  auto f_of = [](uint32_t t) -> float {
+    const float f = key_f32(t);
+    return isnan(f) ? __int_as_float(0x7f800000) : f;
+  };
+  float thr_f = f_of(thr);
   const WorkItem* W = a.work + (int64_t)b * a.cap_w;
   const int nseg = a.nwork[b];
-  uint64_t* fk = a.mode == 1 ? a.full_keys + (int64_t)b * a.cap_full_p2 : nullptr;
+  uint64_t* fk = FULLK ? a.full_keys + (int64_t)b * a.cap_full_p2 : nullptr;
   // the histogram cut, with the exact id-resolving shrink for heavy ties
   auto shrink = [&](int room) {
     if (!warp_cut(wb, &cnt, &thr, &thr64, hist, k, room, &s_thr64))
@@ -430,6 +437,7 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
     for (int j = 0; j < SPT; ++j) {
       const int i = SPT * tid + j;
       soff[i] = i < ns ? off : INT_MAX;
+      if (i < ns) sstart[i] -= (uint32_t)off;  // row of position p = sstart[seg] + p
       off += lens[j];
     }
     if (tid < 32) soff[SW_SEGS + tid] = INT_MAX;
@@ -446,6 +454,15 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
         }
         s_cur = lo;
       }
+      int s_last;  // segment of the warp's last position pe - 1
+      {
+        int lo = s_cur, hi = ns - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (soff[mid] <= pe - 1) lo = mid; else hi = mid - 1;
+        }
+        s_last = lo;
+      }
       // positions p0 .. p0+31 -> (segment, row); advances s_cur past the batch
       auto map = [&](int p0, Slot& sl, int slot) {
         const int nxt = soff[s_cur + 1 + lane];
@@ -455,11 +472,12 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
         const int seg = s_cur + __popc(starts & (FULL >> (31 - lane)));
         const int p = p0 + lane;
         sl.ok = p < pe;
-        // loads are issued unconditionally (a valid row for lanes past the
-        // end) so no later instruction has to wait for them to merge values
-        const uint32_t r = sstart[seg] + (uint32_t)(p - soff[seg]);
-        sl.row = sl.ok ? r : sstart[s_cur];
-        sl.base = sbase[seg];
+        // lanes past the end load the warp's last row (their segment is
+        // capped the same way), so every load is issued unconditionally
+        const int pc = min(p, pe - 1);
+        const int sg = pc == p ? seg : s_last;
+        sl.row = sstart[sg] + (uint32_t)pc;
+        sl.base = sbase[sg];
         if constexpr (CPA) {
           uint8_t* dst = ring + slot * sw_slot(M);
           constexpr int CH = cp_chunk<M>();
@@ -483,7 +501,7 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
           const uint8_t* src = ring + slot * sw_slot(M);
           code = smem_code<M>(src + lane * M);
           const uint32_t cw = reinterpret_cast<const uint32_t*>(src + 32 * M)[lane];
-          cb = (cw >> ((cur.row & 3u) * 8)) & 0xffu;
+          cb = __byte_perm(cw, 0, 0x4440u | (cur.row & 3u));
         } else {
           code = cur.code;
           cb = cur.cb;
@@ -494,18 +512,18 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
         return (float)dadd(dsub(cur.base, 2.0 * (double)ip), (double)ctab[cb]);
       };
       auto consider = [&](const Slot& cur, float dist, int p0) {
-        if (a.mode == 1) {
+        if constexpr (FULLK) {
           if (cur.ok) fk[pos_base + p0 + lane] = dist_id_key(dist, __ldg(ix.pids + cur.row));
           return;
         }
-        const uint32_t dk = f32_key(dist);
-        bool pass = cur.ok && dk <= thr;
+        // dist <= thr_f  <=>  f32_key(dist) <= thr (finite distances)
+        bool pass = cur.ok && dist <= thr_f;
         // at dk == thr the id decides unless the bound admits every id
-        if (pass && dk == thr && (uint32_t)thr64 != 0xffffffffu)
-          pass = (((uint64_t)dk << 32) | (uint32_t)__ldg(ix.pids + cur.row)) < thr64;
+        if (pass && dist == thr_f && (uint32_t)thr64 != 0xffffffffu)
+          pass = (((uint64_t)f32_key(dist) << 32) | (uint32_t)__ldg(ix.pids + cur.row)) < thr64;
         const uint32_t bal = __ballot_sync(FULL, pass);
         if (bal) {
-          if (pass) wb[cnt + __popc(bal & lt_mask)] = ((uint64_t)dk << 32) | cur.row;
+          if (pass) wb[cnt + __popc(bal & lt_mask)] = ((uint64_t)f32_key(dist) << 32) | cur.row;
           cnt += __popc(bal);
         }
       };
@@ -516,9 +534,9 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
 #pragma unroll
       for (int i = 0; i < U; ++i) map(pb + 32 * i, sl[i], i);
       for (int p0 = pb; p0 < pe; p0 += 32 * D) {
-        if (a.mode == 0) {  // adopt a tighter bound from the other warps
+        if constexpr (!FULLK) {  // adopt a tighter bound from the other warps
           const uint64_t t = *(volatile unsigned long long*)&s_thr64;
-          if (t < thr64) { thr64 = t; thr = (uint32_t)(t >> 32); }
+          if (t < thr64) { thr64 = t; thr = (uint32_t)(t >> 32); thr_f = f_of(thr); }
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {  // batches past pe are all-invalid no-ops
@@ -536,13 +554,14 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
         if (cnt > SW_WB - 32 * D) {
           __syncwarp();
           shrink(SW_WB / 2);
+          thr_f = f_of(thr);
         }
       }
       if constexpr (CPA) cp_async_wait<0>();  // prefetches past pe
     }
     pos_base += tot;
   }
-  if (a.mode == 1) return;
+  if constexpr (FULLK) return;
 
   // ---- final: each warp's entries under the shared bound, ids resolved,
   // then exactly min(total, k) of them by (dist, id) across the warps
@@ -700,16 +719,23 @@ void launch_build_luts(const IndexView& ix, const float* Q, int nq, float* luts,
   k_build_luts<<<grid, 256, smem, s>>>(ix, Q, nq, luts);
 }
 
-template <int M, int U, bool CPA, bool XL>
-static void launch_warp_mdx(const ScanArgs& a, cudaStream_t s) {
+template <int M, int U, bool CPA, bool XL, bool FULLK>
+static void launch_warp_mdxf(const ScanArgs& a, cudaStream_t s) {
   const size_t bytes = sw_bytes(M, 2 * U, CPA, XL, a.ix.d);
   static size_t attr = 0;
   if (attr < bytes) {
-    cudaFuncSetAttribute(k_scan_warp<M, U, CPA, XL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_scan_warp<M, U, CPA, XL, FULLK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)bytes);
     attr = bytes;
   }
-  k_scan_warp<M, U, CPA, XL><<<a.nq, SW_THREADS, bytes, s>>>(a);
+  k_scan_warp<M, U, CPA, XL, FULLK><<<a.nq, SW_THREADS, bytes, s>>>(a);
+}
+
+template <int M, int U, bool CPA, bool XL>
+static void launch_warp_mdx(const ScanArgs& a, cudaStream_t s) {
+  if constexpr (XL) launch_warp_mdxf<M, U, CPA, true, false>(a, s);  // XL: top-k only
+  else if (a.mode == 1) launch_warp_mdxf<M, U, CPA, false, true>(a, s);
+  else launch_warp_mdxf<M, U, CPA, false, false>(a, s);
 }
 
 // Interleaved (bank-conflict-free) LUT for M in {8, 16} with prebuilt LUTs
@@ -725,7 +751,7 @@ static bool scan_xl() {
 template <int M, int U, bool CPA>
 static void launch_warp_md(const ScanArgs& a, cudaStream_t s) {
   if constexpr (M == 8 || M == 16) {
-    if (a.luts && scan_xl()) { launch_warp_mdx<M, U, CPA, true>(a, s); return; }
+    if (a.luts && a.mode == 0 && scan_xl()) { launch_warp_mdx<M, U, CPA, true>(a, s); return; }
   }
   launch_warp_mdx<M, U, CPA, false>(a, s);
 }
