@@ -100,3 +100,44 @@ def test_fast_probe_equals_exact_probe():
         q = rng.standard_normal(24).astype(np.float32)
         a, b = so.probe_exact(c, q, 40), so.probe_exact_fast(c, q, 40)
         np.testing.assert_array_equal(a[0], b[0])
+
+
+def _xl_sum(lut, code, x):
+    """Host model of scan_common.cuh:code_sum_xl for one lane with column
+    rotation x: slot s holds entry m = s ^ x, and numpy's tree is applied to
+    the slots (float32, one rounding per add)."""
+    m = lut.shape[0]
+    v = [lut[s ^ x, code[s ^ x]] for s in range(m)]
+    f = np.float32
+    if m == 16:
+        r = [f(v[t] + v[t + 8]) for t in range(8)]
+    else:
+        r = v
+    return f(f(f(r[0] + r[1]) + f(r[2] + r[3])) + f(f(r[4] + r[5]) + f(r[6] + r[7])))
+
+
+def test_interleaved_lut_order_is_bit_identical():
+    """The bank-conflict-free scan reads sub-quantizer s ^ x at step s; the
+    XOR only permutes the leaves of numpy's pairwise tree inside pairs,
+    quads and octets, so every lane's sum equals lookup_code_sums bit for
+    bit (pq.py:172-177)."""
+    rng = np.random.default_rng(7)
+    for m in (8, 16):
+        lut = (rng.standard_normal((m, 256)) * rng.choice([1e-3, 1.0, 1e3], (m, 1))).astype(np.float32)
+        codes = rng.integers(0, 256, (400, m)).astype(np.uint8)
+        want = so.code_sums(lut, codes)
+        for x in range(m):
+            got = np.array([_xl_sum(lut, c, x) for c in codes], np.float32)
+            np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def test_interleaved_lut_banks_are_distinct():
+    """Entry (m, code) of copy c sits at word code * 32 + c * M + m; lane l
+    reads copy l // M, column m = s ^ (l % M): 32 distinct banks per step
+    for any codes."""
+    rng = np.random.default_rng(3)
+    for m in (8, 16):
+        for s in range(m):
+            codes = rng.integers(0, 256, 32)
+            banks = {((int(codes[l]) * 32 + (l // m) * m + (s ^ (l % m))) % 32) for l in range(32)}
+            assert len(banks) == 32
