@@ -206,9 +206,17 @@ __device__ uint32_t block_select(int n, KeyOf key_of, uint32_t* hist, uint32_t* 
 // histogram passes and no id loads; T (all ids) becomes the warp's bound and
 // is published to s_thr64.  Returns false (nothing changed) when more than
 // `room` entries would stay (massive distance ties): use warp_shrink then.
+//
+// Quota bound (tw, k8 > 0): the first pass's histogram also gives the upper
+// edge of the bin holding the k8-th smallest key: this warp holds >= k8
+// entries at or below it, and keeps them (every later cut keeps its k-th
+// smallest and everything below).  With k8 = ceil(k / WARPS) the largest of
+// the warps' edges is a CTA-wide bound (>= k entries at or below it) as
+// tight as the k-th of all rows scanned so far, long before any one warp's
+// own k-th gets there.
 __device__ __forceinline__ bool warp_cut(uint64_t* wb, int* cnt_io, uint32_t* thr, uint64_t* thr64,
                                          uint32_t* hist, int k, int room,
-                                         unsigned long long* s_thr64) {
+                                         unsigned long long* s_thr64, uint32_t* tw, int k8) {
   const int lane = threadIdx.x & 31;
   const uint32_t lt_mask = (1u << lane) - 1u;
   const int cnt = *cnt_io;
@@ -242,6 +250,26 @@ __device__ __forceinline__ bool warp_cut(uint64_t* wb, int* cnt_io, uint32_t* th
       if (lane >= o) incl += y;
     }
     const uint32_t excl = incl - run;
+    if (pass == 0 && k8 > 0) {  // the quota bound (see above)
+      const uint32_t n8 = (uint32_t)k8;
+      const bool m8 = excl < n8 && incl >= n8;
+      const uint32_t bal8 = __ballot_sync(FULL, m8);
+      if (bal8) {
+        uint32_t b8 = 0;
+        if (m8) {
+          uint32_t c = excl;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (c + h[j] >= n8) { b8 = lane * 8 + j; break; }
+            c += h[j];
+          }
+        }
+        b8 = __shfl_sync(FULL, b8, __ffs(bal8) - 1);
+        const uint64_t e8 = (uint64_t)lo + ((uint64_t)(b8 + 1) << shift) - 1;
+        const uint32_t t8 = (uint32_t)(e8 < hi ? e8 : hi);
+        if (lane == 0 && t8 < *tw) *(volatile uint32_t*)tw = t8;
+      }
+    }
     const bool mine = excl < need && incl >= need;
     const int src = __ffs(__ballot_sync(FULL, mine)) - 1;
     uint32_t bin = 0, before = 0, through = 0;
@@ -347,6 +375,8 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
   __shared__ int s_nmerge, s_nout;
   __shared__ int s_wcnt[SW_WARPS];
   __shared__ uint32_t s_sel[4];
+  __shared__ __align__(16) uint32_t s_tw[SW_WARPS];  // per-warp quota bounds (warp_cut)
+  static_assert(SW_WARPS == 8, "quota bound read as two uint4");
 
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t lt_mask = (1u << lane) - 1u;
@@ -378,6 +408,8 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
   }
   for (int i = tid; i < 256; i += SW_THREADS) ctab[i] = ix.ctab[i];
   if (tid == 0) { s_thr64 = kKeyPad; s_nmerge = 0; }
+  if (tid < SW_WARPS) s_tw[tid] = 0xffffffffu;
+  const int k8 = (k + SW_WARPS - 1) / SW_WARPS;
 
   uint64_t* wb = reinterpret_cast<uint64_t*>(dsm + SW_WBUF) + warp * SW_WB;
   uint32_t* hist = reinterpret_cast<uint32_t*>(merge) + warp * 256;
@@ -395,7 +427,7 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
   uint64_t* fk = FULLK ? a.full_keys + (int64_t)b * a.cap_full_p2 : nullptr;
   // the histogram cut, with the exact id-resolving shrink for heavy ties
   auto shrink = [&](int room) {
-    if (!warp_cut(wb, &cnt, &thr, &thr64, hist, k, room, &s_thr64))
+    if (!warp_cut(wb, &cnt, &thr, &thr64, hist, k, room, &s_thr64, &s_tw[warp], FULLK ? 0 : k8))
       warp_shrink(wb, &cnt, &thr, &thr64, hist, ix.pids, k, &s_thr64);
   };
 
@@ -535,7 +567,16 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
       for (int i = 0; i < U; ++i) map(pb + 32 * i, sl[i], i);
       for (int p0 = pb; p0 < pe; p0 += 32 * D) {
         if constexpr (!FULLK) {  // adopt a tighter bound from the other warps
-          const uint64_t t = *(volatile unsigned long long*)&s_thr64;
+          // the quota bound: the largest of the warps' k8-th edges
+          uint32_t q[8];
+          asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]) : "r"(smem_u32(&s_tw[0])));
+          asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(q[4]), "=r"(q[5]), "=r"(q[6]), "=r"(q[7]) : "r"(smem_u32(&s_tw[4])));
+          const uint32_t qb = max(max(max(q[0], q[1]), max(q[2], q[3])), max(max(q[4], q[5]), max(q[6], q[7])));
+          const uint64_t tq = ((uint64_t)qb << 32) | 0xffffffffull;
+          const uint64_t ts = *(volatile unsigned long long*)&s_thr64;
+          const uint64_t t = ts < tq ? ts : tq;
           if (t < thr64) { thr64 = t; thr = (uint32_t)(t >> 32); thr_f = f_of(thr); }
         }
 #pragma unroll
