@@ -226,6 +226,7 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
       kmax = max(kmax, k);
     }
   }
+  PLAN_PHASE(8);
   const double q2 = block_sum(q2p, redd);
   alx = block_max(alx, redd);
   aln = -block_max(-aln, redd);
@@ -394,12 +395,14 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
   unsigned long long wsum = 0;  // lengths of the begun window groups
   if (!flag && !no_cut) {
     // one metadata gather per window group, then the centroid rows
+    PLAN_PHASE(1);
     if (tid < (int)nw) {
       const int64_t gi = GI(wval[tid]);
       wrow[tid] = ix.grouping ? ix.nbr[gi] : 0;
       wnorm[tid] = ix.grouping ? ix.norm[gi] : 0.f;
     }
     __syncthreads();
+    PLAN_PHASE(10);
     const int grp = tid >> 3, gl = tid & 7;
     constexpr int NG = PA_THREADS >> 3;
     for (uint32_t i0 = 0; i0 < nw; i0 += NG * PA_U) {
@@ -436,7 +439,9 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
     const uint32_t np2 = next_pow2(max(nw, 1u));
     for (uint32_t i = nw + tid; i < np2; i += PA_THREADS) { wkey[i] = kKeyPad; wval[i] = 0xffffffffu; }
     __syncthreads();
+    PLAN_PHASE(7);
     bitonic_sort(wkey, wval, np2);  // (score, flat): the reference order
+    PLAN_PHASE(11);
     if (tid == 0) s_lastb = -1;
     __syncthreads();
     unsigned long long carry = wA, mine = 0;
@@ -475,6 +480,12 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
   const bool big = nbegun > (uint64_t)PA_CAND;
   if (big && INLINE && !flag) { flag = true; why = 5; }
   PLAN_PHASE(4);
+#ifdef GIVF_PHASES
+  if (tid == 0 && ix.counters) {  // sizes: window items, begun groups
+    atomicAdd(&ix.counters[24], (unsigned long long)nw);
+    atomicAdd(&ix.counters[25], (unsigned long long)nbegun);
+  }
+#endif
   if (flag) {
     if (tid == 0) {
       a.only[b] = 1;
@@ -544,6 +555,7 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
       }
     }
     __syncthreads();
+    PLAN_PHASE(12);
     const int nc = (int)nbegun;
     for (int c0 = 0; c0 < nc; c0 += PA_THREADS) {
       const int c = c0 + tid;

@@ -21,11 +21,12 @@ _native.check(_native.load().givf_index_counters(dev.handle, out.ctypes.data, 32
 before = out.copy()
 search_batch(dev, qt, p, k=100); torch.cuda.synchronize()
 _native.check(_native.load().givf_index_counters(dev.handle, out.ctypes.data, 32))
-ph = (out - before)[8:16]
-names = ['stage', '-', 'levels', 'bucket+walk', 'window', 'emit', 'rescore', '-']
+ph = (out - before)[8:24]
+names = ['stage(q,regions)', 'w:classify', 'levels', 'bucket+walk', 'w:walk+cert', 'emit', 'rescore', 'w:f64 score',
+         'stage:items', '-', 'w:gather', 'w:sort', 'emit:A compact', '-', '-', '-']
 tot = ph.sum()
 for n, v in zip(names, ph):
     print(f"PHASE {n:14s} {100*v/max(tot,1):5.1f}%  {v/q.shape[0]:10.0f} cycles/query")
-print("fallbacks", (out-before)[:2])
+print("fallbacks", (out-before)[:2], "window items/query", (out-before)[24] / q.shape[0], "begun/query", (out-before)[25] / q.shape[0])
 PY
 make clean > /dev/null && make -j16 > /dev/null 2>&1
