@@ -113,7 +113,9 @@ int givf_index_counters(givf_index_t index, int64_t* out, int32_t n);
  * f32 padded with +inf, stats (nq) -- host or device; stream = cudaStream_t
  * to launch on (NULL = the default stream).  Returns after the results are
  * visible to the caller (host outputs: synchronised; device outputs:
- * enqueued on `stream`). */
+ * enqueued on `stream`).  Page-locked (pinned, mapped) host outputs are
+ * written by the kernels in place, so their transfer overlaps the scan;
+ * pageable host outputs go through a device buffer and one copy. */
 int givf_search_topk(givf_index_t index, const float* queries, int64_t nq,
                      const givf_search_params* params, int32_t k, int32_t* ids,
                      float* dists, givf_search_stats* stats, void* stream);

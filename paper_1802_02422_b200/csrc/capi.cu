@@ -95,6 +95,23 @@ bool is_device_ptr(const void* p) {
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
+// Output pointers kernels may write directly: device / managed memory, or
+// page-locked host memory mapped into the device's address space (written
+// over the bus by the kernels themselves, so the device-to-host transfer of
+// the results overlaps the scan instead of following it).  Null otherwise.
+template <typename T>
+T* kernel_writable(T* p) {
+  if (!p) return nullptr;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) return p;
+  if (at.type == cudaMemoryTypeHost && at.devicePointer) return static_cast<T*>(at.devicePointer);
+  return nullptr;
+}
+
 // Grow-only scratch arena carved per call.
 struct Arena {
   void* base = nullptr;
@@ -446,8 +463,14 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
   cudaStream_t st = (cudaStream_t)stream;  // NULL = the default stream
   const IndexView& v = ix->v;
   const bool q_dev = is_device_ptr(queries);
-  const bool out_dev = is_device_ptr(ids) && is_device_ptr(dists);
-  const bool st_dev = is_device_ptr(stats);
+  // outputs the kernels write in place (device or pinned host memory)
+  int32_t* const ids_w = kernel_writable(ids);
+  float* const dists_w = kernel_writable(dists);
+  int64_t* const stats_w = reinterpret_cast<int64_t*>(kernel_writable(stats));
+  const bool out_dev = ids_w && dists_w;
+  const bool st_dev = stats_w != nullptr;
+  // results in host memory: the call returns once they have landed
+  const bool host_out = !(is_device_ptr(ids) && is_device_ptr(dists) && is_device_ptr(stats));
   const bool rerank = p->rerank != 0;
   const int64_t full_p2 = om == OUT_FULL ? (int64_t)next_pow2_host((uint32_t)std::max<int64_t>(width, 1)) : 0;
 
@@ -549,7 +572,7 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
     pa.cap_w = pl.cap_w;
     pa.work = ar.take<WorkItem>((size_t)bq * pl.cap_w);
     pa.nwork = ar.take<int>(bq);
-    int64_t* dstats = st_dev ? reinterpret_cast<int64_t*>(stats + q0) : ar.take<int64_t>((size_t)bq * 4);
+    int64_t* dstats = st_dev ? stats_w + q0 * 4 : ar.take<int64_t>((size_t)bq * 4);
     pa.stats = dstats;
     pa.sort_work = (om == OUT_FULL && !rerank) ? 1 : 0;
     if (pa.sort_work) {
@@ -607,8 +630,8 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
     int32_t* oid;
     float* od;
     if (out_dev) {
-      oid = ids + q0 * width;
-      od = dists + q0 * width;
+      oid = ids_w + q0 * width;
+      od = dists_w + q0 * width;
     } else {
       oid = ar.take<int32_t>((size_t)bq * width);
       od = ar.take<float>((size_t)bq * width);
@@ -669,7 +692,7 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
     CUDA_TRY(cudaEventRecord(ix->ev_done[i], ix->pstreams[i]));
     CUDA_TRY(cudaStreamWaitEvent(caller, ix->ev_done[i], 0));
   }
-  if (!out_dev || !st_dev || !q_dev) CUDA_TRY(cudaStreamSynchronize(caller));
+  if (host_out || !q_dev) CUDA_TRY(cudaStreamSynchronize(caller));
   return GIVF_OK;
 }
 
