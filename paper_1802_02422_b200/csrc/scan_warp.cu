@@ -611,7 +611,14 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
   __syncthreads();
   // every warp's bound holds >= k entries: entries above the smallest bound
   // are out; ids are loaded only for the survivors
-  const uint64_t T = s_thr64;
+  uint64_t T = s_thr64;
+  {  // the quota bound (warp_cut) holds as well
+    uint32_t qb = 0;
+#pragma unroll
+    for (int w = 0; w < SW_WARPS; ++w) qb = max(qb, s_tw[w]);
+    const uint64_t tq = ((uint64_t)qb << 32) | 0xffffffffull;
+    T = T < tq ? T : tq;
+  }
   {
     // every id load of the warp in flight at once (cnt <= SW_WB)
     constexpr int R = SW_WB / 32;
