@@ -105,6 +105,51 @@ GIVF_DEV CodeVec<M> smem_code(const uint8_t* p) {
   return v;
 }
 
+// Ascending sort of n <= 128 keys by one warp: element e = 4 * lane + r in
+// registers, bitonic network (partners inside a lane: register swaps; across
+// lanes: xor shuffles), padded with kKeyPad; written back in place.
+__device__ __forceinline__ void warp_sort128(uint64_t* keys, int n) {
+  const int lane = threadIdx.x & 31;
+  uint64_t v[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) v[r] = 4 * lane + r < n ? keys[4 * lane + r] : kKeyPad;
+#pragma unroll
+  for (int size = 2; size <= 128; size <<= 1) {
+#pragma unroll
+    for (int j = size >> 1; j > 0; j >>= 1) {
+      if (j >= 4) {
+        const int lj = j >> 2;
+        const bool lower = (lane & lj) == 0;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int e = 4 * lane + r;
+          const bool asc = (e & size) == 0;
+          const uint64_t o = __shfl_xor_sync(0xffffffffu, v[r], lj);
+          // the lower element of the pair keeps the min when ascending
+          const bool take_min = lower == asc;
+          v[r] = take_min ? (o < v[r] ? o : v[r]) : (o > v[r] ? o : v[r]);
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int p = r ^ j;
+          if (p > r) {
+            const int e = 4 * lane + r;
+            const bool asc = (e & size) == 0;
+            const uint64_t a = v[r], b = v[p];
+            const bool sw = asc ? (a > b) : (a < b);
+            v[r] = sw ? b : a;
+            v[p] = sw ? a : b;
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+    if (4 * lane + r < n) keys[4 * lane + r] = v[r];
+}
+
 // Warp radix select: the digit-by-digit search for the need-th smallest of
 // the 32-bit keys key_of(i), i < n, that match `prefix` under `mask` (hist:
 // 256 words private to the warp).  Returns the key; *eq = how many of the n
@@ -696,10 +741,15 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
     __syncthreads();
     nf = s_nout;
   }
-  const uint32_t np2 = next_pow2((uint32_t)max(nf, 1));
-  for (uint32_t i = nf + tid; i < np2; i += SW_THREADS) fin[i] = kKeyPad;
-  __syncthreads();
-  bitonic_sort_keys(fin, np2);
+  if (nf <= 128) {  // k <= SW_KMAX: one warp sorts in registers, no block barriers
+    if (warp == 0) warp_sort128(fin, nf);
+    __syncthreads();
+  } else {
+    const uint32_t np2 = next_pow2((uint32_t)max(nf, 1));
+    for (uint32_t i = nf + tid; i < np2; i += SW_THREADS) fin[i] = kKeyPad;
+    __syncthreads();
+    bitonic_sort_keys(fin, np2);
+  }
   for (int i = tid; i < k; i += SW_THREADS) {
     int32_t id = -1;
     float dv = __int_as_float(0x7f800000);
