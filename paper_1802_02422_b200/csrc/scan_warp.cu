@@ -709,7 +709,12 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
   const int n_in = compact ? nm : SW_WARPS * SW_WB;
   uint64_t* fin = compact ? all : merge;
   int nf = 0;
-  {
+  if (compact && nm <= 128) {  // few survivors: sort them all, keep the first k
+    if (warp == 0) warp_sort128(merge, nm);
+    __syncthreads();
+    fin = merge;
+    nf = min(nm, k);
+  } else {
     uint64_t lim = kKeyPad;
     if (nm > k) {
       uint32_t* bh = reinterpret_cast<uint32_t*>(sstart);  // free after the sweeps
@@ -740,15 +745,15 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
     }
     __syncthreads();
     nf = s_nout;
-  }
-  if (nf <= 128) {  // k <= SW_KMAX: one warp sorts in registers, no block barriers
-    if (warp == 0) warp_sort128(fin, nf);
-    __syncthreads();
-  } else {
-    const uint32_t np2 = next_pow2((uint32_t)max(nf, 1));
-    for (uint32_t i = nf + tid; i < np2; i += SW_THREADS) fin[i] = kKeyPad;
-    __syncthreads();
-    bitonic_sort_keys(fin, np2);
+    if (nf <= 128) {  // k <= SW_KMAX: one warp sorts in registers, no block barriers
+      if (warp == 0) warp_sort128(fin, nf);
+      __syncthreads();
+    } else {
+      const uint32_t np2 = next_pow2((uint32_t)max(nf, 1));
+      for (uint32_t i = nf + tid; i < np2; i += SW_THREADS) fin[i] = kKeyPad;
+      __syncthreads();
+      bitonic_sort_keys(fin, np2);
+    }
   }
   for (int i = tid; i < k; i += SW_THREADS) {
     int32_t id = -1;
