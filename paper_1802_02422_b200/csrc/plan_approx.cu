@@ -28,6 +28,9 @@
 //        row per emitted group.
 #include <cuda_fp16.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "plan_common.cuh"
@@ -656,14 +659,15 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
 // Exact float64 base / score of the work items k_plan_approx emitted, many
 // queries' items in flight per SM (one CTA per (query, slice of its items)).
 constexpr int RS_THREADS = 128;
-constexpr int RS_SPLIT = 4;
+constexpr int RS_SPLIT = 2;
+constexpr int RS_U = 2;  // centroid rows in flight per 8-lane group (64 registers: 8 CTAs/SM)
 
-__global__ void __launch_bounds__(RS_THREADS, 4) k_plan_rescore(PlanArgs a) {
+__global__ void __launch_bounds__(RS_THREADS, 6) k_plan_rescore(PlanArgs a) {
   extern __shared__ __align__(16) unsigned char dsm[];
   double* qd = reinterpret_cast<double*>(dsm);
   const IndexView& ix = a.ix;
   const int b = blockIdx.x, tid = threadIdx.x;
-  constexpr int NG = RS_THREADS >> 3, PER = NG * PA_U;
+  constexpr int NG = RS_THREADS >> 3, PER = NG * RS_U;
   if (a.only[b] != 0) return;  // the exact planner owns this query
   const int n = a.nwork[b];
   if ((int)blockIdx.y * PER >= n) return;
@@ -674,26 +678,26 @@ __global__ void __launch_bounds__(RS_THREADS, 4) k_plan_rescore(PlanArgs a) {
   const double* qc2 = a.qc2 + (int64_t)b * a.P;
   const int grp = tid >> 3, gl = tid & 7;
   const bool vec = (d & 3) == 0 && d <= 128;
-  for (int i0 = blockIdx.y * PER; i0 < n; i0 += RS_SPLIT * PER) {
-    const float* rows[PA_U];
-    double sb[PA_U], ss[PA_U];
+  for (int i0 = blockIdx.y * PER; i0 < n; i0 += gridDim.y * PER) {
+    const float* rows[RS_U];
+    double sb[RS_U], ss[RS_U];
 #pragma unroll
-    for (int u = 0; u < PA_U; ++u) {
+    for (int u = 0; u < RS_U; ++u) {
       const int i = i0 + u * NG + grp;
       sb[u] = i < n ? Wl[i].base : 0.0;
       ss[u] = i < n ? Wl[i].score : 0.0;
       rows[u] = ix.centroids + (int64_t)__double2loint(sb[u]) * d;
     }
-    double qs2[PA_U];
+    double qs2[RS_U];
     if (vec) {
-      group8_sqdist64_multi<PA_U>(rows, qd, d >> 2, qs2);
+      group8_sqdist64_multi<RS_U>(rows, qd, d >> 2, qs2);
     } else {
 #pragma unroll
-      for (int u = 0; u < PA_U; ++u) qs2[u] = group8_sqdist64(rows[u], qd, d);
+      for (int u = 0; u < RS_U; ++u) qs2[u] = group8_sqdist64(rows[u], qd, d);
     }
     if (gl == 0) {
 #pragma unroll
-      for (int u = 0; u < PA_U; ++u) {
+      for (int u = 0; u < RS_U; ++u) {
         const int i = i0 + u * NG + grp;
         if (i >= n) continue;
         const int p = __double2hiint(sb[u]);
@@ -720,7 +724,11 @@ int launch_plan_approx(const PlanArgs& a0, cudaStream_t s) {
   }
   kern<<<a.nq, PA_THREADS, L.bytes, s>>>(a);
   if (!a.defer_rescore) return 1;
-  k_plan_rescore<<<dim3(a.nq, RS_SPLIT), RS_THREADS, (size_t)a.ix.d * 8, s>>>(a);
+  static const int split = [] {  // CTAs per query (GIVF_RS_SPLIT)
+    const char* e = getenv("GIVF_RS_SPLIT");
+    return e ? std::max(1, std::min(64, atoi(e))) : RS_SPLIT;
+  }();
+  k_plan_rescore<<<dim3(a.nq, split), RS_THREADS, (size_t)a.ix.d * 8, s>>>(a);
   return 2;
 }
 
