@@ -480,10 +480,46 @@ k_probe_recheck(const float* __restrict__ Q, const float* __restrict__ C, int K,
   const int* cb = cand + (int64_t)b * cap;
   const uint32_t np2 = next_pow2((uint32_t)max(n, 1));
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
-  for (int i = warp; i < n; i += nw) {
-    int id = cb[i];
-    double s = warp_sqdist64(C + (int64_t)id * d, qd, qf, d, false);
-    if (lane == 0) { key[i] = f64_key(s); val[i] = (uint32_t)id; }
+  if (d <= 128) {
+    // two candidates per warp step, every row load issued before the math
+    // (same per-candidate arithmetic order as warp_sqdist64)
+    constexpr int R = 4;  // d <= 32 * R
+    for (int i = warp; i < n; i += 2 * nw) {
+      const int i2 = i + nw;
+      const int id1 = cb[i], id2 = i2 < n ? cb[i2] : id1;
+      const float* c1 = C + (int64_t)id1 * d;
+      const float* c2 = C + (int64_t)id2 * d;
+      float x1[R], x2[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int j = lane + 32 * r;
+        x1[r] = j < d ? __ldg(c1 + j) : 0.f;
+        x2[r] = j < d ? __ldg(c2 + j) : 0.f;
+      }
+      double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int j = lane + 32 * r;
+        if (j < d) {
+          const double t1 = dsub((double)x1[r], qd[j]), t2 = dsub((double)x2[r], qd[j]);
+          s1 = dadd(s1, dmul(t1, t1));
+          s2 = dadd(s2, dmul(t2, t2));
+        }
+      }
+      s1 = warp_sum(s1);
+      s2 = warp_sum(s2);
+      if (lane == 0) {
+        key[i] = f64_key(s1);
+        val[i] = (uint32_t)id1;
+        if (i2 < n) { key[i2] = f64_key(s2); val[i2] = (uint32_t)id2; }
+      }
+    }
+  } else {
+    for (int i = warp; i < n; i += nw) {
+      int id = cb[i];
+      double s = warp_sqdist64(C + (int64_t)id * d, qd, qf, d, false);
+      if (lane == 0) { key[i] = f64_key(s); val[i] = (uint32_t)id; }
+    }
   }
   for (uint32_t i = n + threadIdx.x; i < np2; i += blockDim.x) { key[i] = kKeyPad; val[i] = 0xffffffffu; }
   __syncthreads();
