@@ -376,14 +376,18 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
   __syncthreads();
   int my_a = 0;  // A items of this thread (for the compaction below)
   unsigned long long nA, wA;
+  // the same tests on the float32 keys: f < wlo <=> f < ru(wlo) and
+  // f <= whi <=> f <= rd(whi) for floats f, and f32_key is monotone
+  const uint32_t klo = f32_key(__double2float_ru(wlo));
+  const uint32_t khi = f32_key(__double2float_rd(whi));
   {
     unsigned long long cw = 0;
     for (int64_t f = tid; f < total; f += PA_THREADS) {
-      const double v = (double)key_f32(KEY(f));
-      if (v < wlo) {
+      const uint32_t kf = KEY(f);
+      if (kf < klo) {
         ++my_a;
         cw += (1ull << CW) | (unsigned long long)SIZE(f);
-      } else if (v <= whi && !no_cut) {
+      } else if (kf <= khi && !no_cut) {
         const uint32_t p = atomicAdd(&s_nw, 1u);
         if (p < PA_WCAP) wval[p] = (uint32_t)f;
       }
@@ -408,27 +412,32 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
     PLAN_PHASE(10);
     const int grp = tid >> 3, gl = tid & 7;
     constexpr int NG = PA_THREADS >> 3;
-    for (uint32_t i0 = 0; i0 < nw; i0 += NG * PA_U) {
+    // rows in flight per group: no more than the window needs
+    const int uw = nw <= (uint32_t)NG ? 1 : (nw <= 2u * NG ? 2 : PA_U);
+    for (uint32_t i0 = 0; i0 < nw; i0 += NG * uw) {
       const float* rows[PA_U];
 #pragma unroll
       for (int u = 0; u < PA_U; ++u) {
         const uint32_t i = i0 + u * NG + grp;
-        rows[u] = ix.centroids + (int64_t)(i < nw ? wrow[i] : 0) * d;
+        rows[u] = ix.centroids + (int64_t)(u < uw && i < nw ? wrow[i] : 0) * d;
       }
       double qs2[PA_U];
       if (ix.grouping) {
         if ((d & 3) == 0 && d <= 128) {
-          group8_sqdist64_multi<PA_U>(rows, qd, d >> 2, qs2);
+          if (uw == 1) group8_sqdist64_multi<1>(rows, qd, d >> 2, qs2);
+          else if (uw == 2) group8_sqdist64_multi<2>(rows, qd, d >> 2, qs2);
+          else group8_sqdist64_multi<PA_U>(rows, qd, d >> 2, qs2);
         } else {
 #pragma unroll
-          for (int u = 0; u < PA_U; ++u) qs2[u] = group8_sqdist64(rows[u], qd, d);
+          for (int u = 0; u < PA_U; ++u)
+            if (u < uw) qs2[u] = group8_sqdist64(rows[u], qd, d);
         }
       }
       if (gl == 0) {
 #pragma unroll
         for (int u = 0; u < PA_U; ++u) {
           const uint32_t i = i0 + u * NG + grp;
-          if (i >= nw) continue;
+          if (u >= uw || i >= nw) continue;
           const int p = (int)(wval[i] / G);
           double score = QC(p);
           if (ix.grouping) {
@@ -546,7 +555,7 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
       uint32_t tot;
       uint32_t pos = block_exclusive_scan((uint32_t)my_a, red32, &tot);
       for (int64_t f = tid; f < total; f += PA_THREADS) {
-        if ((double)key_f32(KEY(f)) < wlo) {
+        if (KEY(f) < klo) {
           cf[pos] = (uint32_t)f;
           cl[pos] = (int32_t)SIZE(f);
           ++pos;
@@ -568,7 +577,7 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
   } else {
     for (int64_t f0 = 0; f0 < total; f0 += PA_THREADS) {
       const int64_t f = f0 + tid;
-      const bool isA = f < total && (double)key_f32(KEY(f)) < wlo;
+      const bool isA = f < total && KEY(f) < klo;
       emit_round(isA, (uint32_t)f, isA ? SIZE(f) : 0);
     }
     for (int i0 = 0; i0 <= lastw; i0 += PA_THREADS) {
