@@ -19,6 +19,8 @@
 // Everything strictly below the bucket is scanned whole; the walk decides
 // the bucket's items (partial last group included).  For rerank=False the
 // emitted work list is additionally sorted into the reference scan order.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "plan_common.cuh"
@@ -32,12 +34,11 @@ constexpr int SORT_SMALL = 128;  // boundary buckets up to this size are sorted 
 constexpr int PLAN_SREG = 2048;  // probed regions staged in shared memory
 
 // ---- K3: float64 group scores (search.py:111-121), one CTA per query.
-__global__ void __launch_bounds__(PLAN_THREADS) k_plan_score(PlanArgs a) {
+__device__ void plan_score_one(const PlanArgs& a, const int b) {
   __shared__ double qd[1024];
   __shared__ int32_t sreg[PLAN_SREG];
   const IndexView& ix = a.ix;
-  const int b = blockIdx.x, tid = threadIdx.x;
-  if (a.only && a.only[b] == 0) return;  // fallback mode: flagged queries only
+  const int tid = threadIdx.x;
   const int G = ix.G, d = ix.d, P = a.P;
   const int64_t total = (int64_t)P * G;
   const int* reg = a.regions + (int64_t)b * P;
@@ -106,7 +107,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan_score(PlanArgs a) {
 }
 
 // ---- K4: tau-pruning + budget walk + work-list emission, one CTA per query.
-__global__ void __launch_bounds__(PLAN_THREADS) k_plan_select(PlanArgs a) {
+__device__ void plan_select_one(const PlanArgs& a, const int b) {
   extern __shared__ __align__(16) unsigned char dsm[];
   unsigned long long* hw = reinterpret_cast<unsigned long long*>(dsm);  // (first 4 KB: u32 weights)
   uint32_t* hw32 = reinterpret_cast<uint32_t*>(dsm);
@@ -125,8 +126,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan_select(PlanArgs a) {
   __shared__ uint32_t s_nbk;
 
   const IndexView& ix = a.ix;
-  const int b = blockIdx.x, tid = threadIdx.x;
-  if (a.only && a.only[b] == 0) return;  // fallback mode: flagged queries only
+  const int tid = threadIdx.x;
   const int G = ix.G, P = a.P;
   const int64_t total = (int64_t)P * G;
   const int* reg = a.regions + (int64_t)b * P;
@@ -368,12 +368,38 @@ size_t plan_smem(int d) {
   return (size_t)PLAN_BUCKETS * 8 + SORTCAP * 8 + PLAN_BUCKETS * 4 + SORTCAP * 4 + SORTCAP * 4 + 16;
 }
 
+// One CTA per query, or (fallback mode, a.only set) a grid-stride loop over
+// the queries that only visits the flagged ones: the approximate planner
+// flags few or none, and a 10^4-CTA grid of early exits costs ~20 us.
+__global__ void __launch_bounds__(PLAN_THREADS) k_plan_score(PlanArgs a) {
+  for (int b = blockIdx.x; b < a.nq; b += gridDim.x) {
+    if (a.only && a.only[b] == 0) continue;
+    plan_score_one(a, b);
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(PLAN_THREADS) k_plan_select(PlanArgs a) {
+  for (int b = blockIdx.x; b < a.nq; b += gridDim.x) {
+    if (a.only && a.only[b] == 0) continue;
+    plan_select_one(a, b);
+    __syncthreads();
+  }
+}
+
 int launch_plan(const PlanArgs& a, cudaStream_t s) {
   int n = 0;
   if (a.approx && a.only != nullptr) {
     n += launch_plan_approx(a, s);  // flags the queries it cannot certify
-    k_plan_score<<<a.nq, PLAN_THREADS, 0, s>>>(a);
-    k_plan_select<<<a.nq, PLAN_THREADS, plan_smem(a.ix.d), s>>>(a);
+    int sms = 148;
+    {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int grid = std::min(a.nq, 2 * sms);
+    k_plan_score<<<grid, PLAN_THREADS, 0, s>>>(a);
+    k_plan_select<<<grid, PLAN_THREADS, plan_smem(a.ix.d), s>>>(a);
     return n + 2;
   }
   PlanArgs e = a;
