@@ -9,8 +9,12 @@ k=100) on seeded synthetic data built on the GPU (paper_1802_02422_b200.builder)
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--workload c2|c1|c3|c4|c3mini|c4mini] [--nprobe P] [--tau T] [--candidates C]
 
-N>1 runs under torchrun: every rank holds a slice of every inverted list and
-the per-rank top-k lists are all-gathered over NCCL and merged.
+N>1 runs under torchrun.  Default `--layout queries`: every rank holds the
+whole index and searches a batch of 10^4 queries per step (the synthetic
+query set; queries are independent units: no data-path collective; weak
+scaling, value = all ranks' queries / the slowest rank's time).  `--layout lists`: every
+rank holds a slice of every inverted list and the per-rank top-k lists are
+all-gathered over NCCL and merged by K7 (strong scaling).
 `--impl reference` times the CPU oracle port of the reference path on the
 host cores (rank 0 only).
 """
@@ -349,7 +353,15 @@ def run_ours(args, w):
         arr, queries, gt, build_s = load_or_build(w, args.noise, args.seed, f"cuda:{local}",
                                                   allow_build=False)
     torch.cuda.synchronize()
-    sx = ShardedIndex(arr, rank, world, device=local)
+    # layout: "queries" = every rank holds the whole index and
+    # searches its own batch of nq queries per step (queries are independent
+    # units: no data-path collective, weak scaling); "lists" = every rank
+    # owns a shard of every inverted list, the per-rank top-k lists are
+    # all-gathered over NCCL and merged by K7 (the same nq queries for every
+    # N: strong scaling)
+    lists = args.layout == "lists" and world > 1
+    shards = world if lists else 1
+    sx = ShardedIndex(arr, rank if lists else 0, shards, device=local)
     params = SearchParams(nprobe=w["nprobe"], tau=w["tau"], candidates=w["candidates"],
                           ef_search=w["k"])
     k = w["topk"]
@@ -394,7 +406,8 @@ def run_ours(args, w):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
     nq = queries.shape[0]
-    qps = nq * args.steps / (total_ms / 1e3)
+    units = nq * (1 if lists else world)  # queries all ranks searched per step
+    qps = units * args.steps / (total_ms / 1e3)
     ids_h = ids.cpu().numpy()
     stats_h = stats.cpu().numpy()
     from paper_1802_02422_b200.query import recall_at_r
@@ -425,7 +438,7 @@ def run_ours(args, w):
     e2e_qps = None
     h2d = queries.nbytes
     d2h = nq * k * 8 + nq * 32
-    if world == 1:
+    if not lists:  # every rank: its own batch through the public API
         qh = torch.from_numpy(queries).pin_memory().numpy()
         oi = torch.empty((nq, k), dtype=torch.int32).pin_memory().numpy()
         od = torch.empty((nq, k), dtype=torch.float32).pin_memory().numpy()
@@ -435,10 +448,16 @@ def run_ours(args, w):
         for _ in range(args.steps):
             l2_flush(flush)
             torch.cuda.synchronize()
+            if world > 1:
+                torch.distributed.barrier()
             t0 = time.perf_counter()
             search_batch(sx.dev, qh, params, k=k, out=(oi, od, os_))
             e2e_t += time.perf_counter() - t0
-        e2e_qps = nq * args.steps / e2e_t
+        if world > 1:  # slowest rank
+            t = torch.tensor([e2e_t], device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_t = float(t.item())
+        e2e_qps = units * args.steps / e2e_t
         assert np.array_equal(oi, ids_h), "e2e results differ from the device-resident run"
 
     sweep = latency_sweep(sx.dev, queries, w, k) if (args.latency_sweep and world == 1) else None
@@ -450,7 +469,7 @@ def run_ours(args, w):
     if rank != 0:
         return None
     m = w["m"]
-    scanned_local = float(stats_h[:, 3].sum()) / world  # ~ rows this rank scans
+    scanned_local = float(stats_h[:, 3].sum()) / shards  # ~ rows this rank scans
     # algorithmic bytes: codes_scanned x (M + 1) per query (M code bytes + the
     # constant byte), summed over the step, over the scan kernels' summed time
     scan_ms, scan_n = stages["scan"]
@@ -470,7 +489,7 @@ def run_ours(args, w):
             tr = json.load(open(tr_path))
             # ncu DRAM bytes of one captured scan launch, scaled to this step's
             # queries (same per-query work) so it compares with `achieved`
-            traffic = tr["dram_bytes_per_launch"] / tr["queries_per_launch"] * nq / world
+            traffic = tr["dram_bytes_per_launch"] / tr["queries_per_launch"] * nq / shards
         except Exception:  # noqa: BLE001
             traffic = None
     gemm_ms, gemm_n = stages["probe_gemm"]
@@ -485,7 +504,7 @@ def run_ours(args, w):
         "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps,
         "higher_is_better": True,
-        "scaling": "strong",
+        "scaling": "strong" if args.layout == "lists" else "weak",
         "vs_baseline": None,
         "dtype": "f32/f64 (u8 codes)",
         "data": ("synthetic: seeded SIFT-like uint8 gamma mixture, built on GPU"
@@ -494,12 +513,15 @@ def run_ours(args, w):
         "config": {
             "workload": f"BASELINE configs[{ {'c1': 0, 'c2': 1, 'c4': 3, 'c4mini': 3}.get(args.workload, 2)}] ({args.workload})",
             "n": w["n"], "d": w["d"], "K": w["k"], "L": w["l"], "M": w["m"],
-            "queries_per_step": nq, "nprobe": w["nprobe"], "tau": w["tau"],
+            "queries_per_step": units, "queries_per_rank_step": nq,
+            "nprobe": w["nprobe"], "tau": w["tau"],
             "candidates": w["candidates"], "k": k, "noise": args.noise,
             "recall@1": recall[1], "recall@10": recall[10], "recall@100": recall[100],
             "codes_scanned_mean": float(stats_h[:, 3].mean()),
             "l2": "flushed between steps (512 MB write); codes also exceed L2",
-            "parallelism": f"list-shard x{world}" if world > 1 else "single GPU",
+            "parallelism": (f"list-shard x{world} (NCCL all-gather + K7 merge)" if lists
+                            else f"query-parallel x{world} (index replica per GPU, no collective)"
+                            if world > 1 else "single GPU"),
         },
         "roofline": {
             "kernel": "scan (K6 ADC scan + top-k)",
@@ -562,7 +584,8 @@ def run_reference(args, w):
         "metric": "queries/sec at fixed recall@10 (synthetic, B200)",
         "value": v, "unit": "queries/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * w["nq"] / v,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if args.layout == "lists" else "weak",
+        "vs_baseline": None,
         "dtype": "f32/f64 (u8 codes)", "data": f"synthetic, noise={args.noise}",
         "config": {"workload": args.workload, "nprobe": w["nprobe"], "tau": w["tau"],
                    "candidates": w["candidates"], "k": w["topk"]},
@@ -590,6 +613,9 @@ def main():
     ap.add_argument("--candidates", type=int)
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--layout", default="queries", choices=["queries", "lists"],
+                    help="N>1: query-parallel replicas (weak scaling) or list shards "
+                         "merged over NCCL (strong scaling)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     w = dict(WORKLOADS[args.workload])
