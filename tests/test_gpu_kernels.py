@@ -267,3 +267,31 @@ def test_parity_sift_u8_d128():
         np.testing.assert_array_equal(st, ws)
         for i in range(q.shape[0]):
             assert_topk_equal(ids[i], d[i], wi[i], wd[i])
+
+
+def test_parity_c2_family_at_10m():
+    """BASELINE configs[1]'s index shape except n: K = 2^16 regions, L = 64,
+    M = 16, per-coordinate noise, 10M rows built on the GPU; the full path at
+    the C2 search parameters against the oracle (stats bit-exact, top-100
+    equal outside 1e-4 tie runs), plus a wide-probe setting."""
+    import torch
+
+    from oracle import search_oracle as so
+    from paper_1802_02422_b200 import SearchParams, search_batch
+    from paper_1802_02422_b200.builder import BuildSpec, SynthSpec, build_synthetic
+    from paper_1802_02422_b200.device_index import DeviceIndex
+
+    torch.manual_seed(0)
+    data = SynthSpec(d=96, n_clusters=65536, sigma=0.3, noise="per_coord", seed=11)
+    spec = BuildSpec(n=10_000_000, k=65536, l=64, m=16, n_learn=1_000_000, kmeans_iters=4,
+                     pq_iters=6, seed=11)
+    arr, q, gt = build_synthetic(data, spec, 40, device="cuda", log=lambda *_: None)
+    dev = DeviceIndex(arr)
+    for nprobe, tau, cand in ((64, 0.5, 10_000), (256, 0.25, 30_000)):
+        p = SearchParams(nprobe=nprobe, tau=tau, candidates=cand)
+        ids, d, st = search_batch(dev, q, p, k=100)
+        wi, wd, ws = so.search_topk(arr, q, so.Params(**vars(p)), 100)
+        np.testing.assert_array_equal(st, ws)
+        for i in range(q.shape[0]):
+            assert_topk_equal(ids[i], d[i], wi[i], wd[i])
+    assert dev.fallback_counts()["probe"] == 0
