@@ -433,16 +433,23 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
     constexpr int NC = 32 / M;
     const float4* src = reinterpret_cast<const float4*>(a.luts + (int64_t)b * M * 256);
     const int m = lane % M, sub = lane / M;
-#pragma unroll 2
-    for (int i = warp; i < M * 64 / 32; i += SW_WARPS) {
-      const int chunk = NC * i + sub;  // codes 4*chunk .. 4*chunk+3
-      const float4 v = __ldg(src + m * 64 + chunk);
+    // every load (and the constant table's) in flight before any store
+    constexpr int IT = M * 64 / 32 / SW_WARPS;
+    static_assert(IT * 32 * SW_WARPS == M * 64 && SW_THREADS == 256, "LUT copy shape");
+    float4 v[IT];
+#pragma unroll
+    for (int it = 0; it < IT; ++it) v[it] = __ldg(src + m * 64 + NC * (warp + it * SW_WARPS) + sub);
+    const float cv = ix.ctab[tid];
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int chunk = NC * (warp + it * SW_WARPS) + sub;  // codes 4*chunk .. 4*chunk+3
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc) {
         float* dst = lut + (4 * chunk) * 32 + (cc ^ sub) * M + m;
-        dst[0] = v.x; dst[32] = v.y; dst[64] = v.z; dst[96] = v.w;
+        dst[0] = v[it].x; dst[32] = v[it].y; dst[64] = v[it].z; dst[96] = v[it].w;
       }
     }
+    ctab[tid] = cv;
   } else if (a.luts) {  // prebuilt for the chunk (k_build_luts): one coalesced copy
     const uint4* src = reinterpret_cast<const uint4*>(a.luts + (int64_t)b * M * 256);
     uint4* dst = reinterpret_cast<uint4*>(lut);
@@ -451,7 +458,8 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
   } else {
     build_lut_into(ix, a.Q + (int64_t)b * ix.d, lut, nullptr, qrot);
   }
-  for (int i = tid; i < 256; i += SW_THREADS) ctab[i] = ix.ctab[i];
+  if constexpr (!XL)
+    for (int i = tid; i < 256; i += SW_THREADS) ctab[i] = ix.ctab[i];
   if (tid == 0) { s_thr64 = kKeyPad; s_nmerge = 0; }
   if (tid < SW_WARPS) s_tw[tid] = 0xffffffffu;
   const int k8 = (k + SW_WARPS - 1) / SW_WARPS;
