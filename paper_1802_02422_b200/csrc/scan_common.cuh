@@ -90,41 +90,34 @@ GIVF_DEV float code_sum(const CodeVec<M>& code, const float* lut) {
 // slots adds exactly the same pairs as over e (in swapped order at most, and
 // float addition is commutative): the sum is bit-identical to code_sum.
 //
-// The row is pre-permuted so slot s reads byte s of registers: words by
-// k ^ (x >> 2), bytes inside a word by i ^ (x & 3).
+// The row's words are permuted by k ^ (x >> 2) in registers and byte
+// (s & 3) ^ (x & 3) of word s >> 2 is extracted with a per-lane PRMT
+// selector, so slot s reads byte s ^ x of the row.
+// lane_base = shared-window address of the interleaved LUT + the lane's copy
+// and column offset (c * M + x) * 4 (LUT base 128-byte aligned).
+// xsel[j] = 0x4440 | (j ^ (x & 3)): the PRMT selector that extracts byte
+// (j ^ (x & 3)) of a word, so only the words need permuting.
 template <int M>
-GIVF_DEV CodeVec<M> xl_permute(const CodeVec<M>& c, int x) {
-  static_assert(M == 8 || M == 16, "interleaved LUT: M in {8, 16}");
-  CodeVec<M> p;
+GIVF_DEV float code_sum_xl(const CodeVec<M>& code, uint32_t lane_base, int x,
+                           const uint32_t (&xsel)[4]) {
+  CodeVec<M> p;  // words by k ^ (x >> 2)
   const int xh = x >> 2;
   if constexpr (M == 16) {
     uint32_t t[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) t[k] = (xh & 1) ? c.w[k ^ 1] : c.w[k];
+    for (int k = 0; k < 4; ++k) t[k] = (xh & 1) ? code.w[k ^ 1] : code.w[k];
 #pragma unroll
     for (int k = 0; k < 4; ++k) p.w[k] = (xh & 2) ? t[k ^ 2] : t[k];
   } else {
 #pragma unroll
-    for (int k = 0; k < 2; ++k) p.w[k] = (xh & 1) ? c.w[k ^ 1] : c.w[k];
+    for (int k = 0; k < 2; ++k) p.w[k] = (xh & 1) ? code.w[k ^ 1] : code.w[k];
   }
-  const int xb = x & 3;
-  const uint32_t sel = (uint32_t)(xb | ((1 ^ xb) << 4) | ((2 ^ xb) << 8) | ((3 ^ xb) << 12));
-#pragma unroll
-  for (int k = 0; k < CodeVec<M>::W; ++k) p.w[k] = __byte_perm(p.w[k], 0, sel);
-  return p;
-}
-
-// lane_base = shared-window address of the interleaved LUT + the lane's copy
-// and column offset (c * M + x) * 4 (LUT base 128-byte aligned).
-template <int M>
-GIVF_DEV float code_sum_xl(const CodeVec<M>& code, uint32_t lane_base, int x) {
-  const CodeVec<M> p = xl_permute<M>(code, x);
   float e[M];
 #pragma unroll
   for (int s = 0; s < M; ++s) {
     // base + (c*M + (s^x))*4 + byte*128 == (lane_base + byte*128) ^ (s*4):
     // bits 2..5 of lane_base hold x*4 and nothing else touches them
-    const uint32_t byte = __byte_perm(p.w[s >> 2], 0, 0x4440 | (s & 3));
+    const uint32_t byte = __byte_perm(p.w[s >> 2], 0, xsel[s & 3]);
     const uint32_t addr = (lane_base + (byte << 7)) ^ ((uint32_t)s << 2);
     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(e[s]) : "r"(addr));
   }

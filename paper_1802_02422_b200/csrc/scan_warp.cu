@@ -488,6 +488,9 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
   const int xl_x = lane % M;                                  // XL: column rotation
   // XL: the lane's copy and column inside the interleaved LUT
   const uint32_t xl_base = smem_u32(lut) + (uint32_t)((lane / M) * M + xl_x) * 4u;
+  uint32_t xl_sel[4];  // XL: byte selectors (code_sum_xl)
+#pragma unroll
+  for (int j = 0; j < 4; ++j) xl_sel[j] = 0x4440u | (uint32_t)(j ^ (xl_x & 3));
   struct Slot {  // one batch position of a lane (CPA: code and cb in the ring)
     uint32_t row;
     double base;
@@ -592,7 +595,7 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
           cb = cur.cb;
         }
         float ip;
-        if constexpr (XL) ip = code_sum_xl<M>(code, xl_base, xl_x);
+        if constexpr (XL) ip = code_sum_xl<M>(code, xl_base, xl_x, xl_sel);
         else ip = code_sum<M>(code, lut);
         return (float)dadd(dsub(cur.base, 2.0 * (double)ip), (double)ctab[cb]);
       };
