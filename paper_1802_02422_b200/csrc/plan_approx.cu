@@ -72,12 +72,19 @@ __global__ void __launch_bounds__(PA_THREADS) k_plan_scores_approx(PlanArgs a) {
   const double dsc = (double)a.dscale[b];
   const double al = (double)ix.alphas[r];
   const double oma_qc = dmul(dsub(1.0, al), qc);
-  for (int j = lane; j < G; j += 32) {
-    const int64_t gi = (int64_t)r * G + j;
+  // two groups per lane per step: both gathers in flight at once
+  for (int j0 = 0; j0 < G; j0 += 64) {
+    const int j1 = j0 + lane, j2 = j0 + 32 + lane;
+    const bool v1 = j1 < G, v2 = j2 < G;
+    const int64_t g1 = (int64_t)r * G + (v1 ? j1 : 0), g2 = (int64_t)r * G + (v2 ? j2 : 0);
+    const int n1 = __ldg(ix.nbr + g1), n2 = __ldg(ix.nbr + g2);
+    const float m1 = __ldg(ix.norm + g1), m2 = __ldg(ix.norm + g2);
+    const uint16_t h1 = __ldg(Drow + n1), h2 = __ldg(Drow + n2);
     // fp16-encoded |q - c_s|^2 (ScoreOut in kernels.h), decoded exactly
-    const double qs2 = (double)__half2float(__ushort_as_half(__ldg(Drow + ix.nbr[gi]))) * dsc;
-    const double score = dadd(dadd(oma_qc, dmul(al, qs2)), (double)ix.norm[gi]);
-    akey[j] = f32_key((float)score);
+    const double s1 = (double)__half2float(__ushort_as_half(h1)) * dsc;
+    const double s2 = (double)__half2float(__ushort_as_half(h2)) * dsc;
+    if (v1) akey[j1] = f32_key((float)dadd(dadd(oma_qc, dmul(al, s1)), (double)m1));
+    if (v2) akey[j2] = f32_key((float)dadd(dadd(oma_qc, dmul(al, s2)), (double)m2));
   }
 }
 
