@@ -345,15 +345,29 @@ k_probe_select(const uint16_t* __restrict__ D, int64_t ldD, const float* __restr
     // 16 threads per 128-code tile, one 16-byte load (8 codes) each
     const uint4* r8 = reinterpret_cast<const uint4*>(row.r);
     const int n8 = K >> 3;
-    for (uint32_t e0 = tid; e0 < nt * 16; e0 += blockDim.x) {
-      const int i = (int)tl[e0 >> 4] * 16 + (int)(e0 & 15);
-      if (i >= n8) continue;
-      const uint4 v = __ldg(r8 + i);
-      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    // two 16-byte loads per thread in flight per step
+    for (uint32_t e0 = tid; e0 < nt * 16; e0 += 2 * blockDim.x) {
+      const uint32_t e1 = e0 + blockDim.x;
+      const int i0 = (int)tl[e0 >> 4] * 16 + (int)(e0 & 15);
+      const int i1 = e1 < nt * 16 ? (int)tl[e1 >> 4] * 16 + (int)(e1 & 15) : n8;
+      const bool ok0 = i0 < n8, ok1 = i1 < n8;
+      const uint4 v0 = ok0 ? __ldg(r8 + i0) : make_uint4(0, 0, 0, 0);
+      const uint4 v1 = ok1 ? __ldg(r8 + i1) : make_uint4(0, 0, 0, 0);
+      if (ok0) {
+        const uint32_t w[4] = {v0.x, v0.y, v0.z, v0.w};
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        take(w[k] & 0xffffu, 8 * i + 2 * k);
-        take(w[k] >> 16, 8 * i + 2 * k + 1);
+        for (int k = 0; k < 4; ++k) {
+          take(w[k] & 0xffffu, 8 * i0 + 2 * k);
+          take(w[k] >> 16, 8 * i0 + 2 * k + 1);
+        }
+      }
+      if (ok1) {
+        const uint32_t w[4] = {v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          take(w[k] & 0xffffu, 8 * i1 + 2 * k);
+          take(w[k] >> 16, 8 * i1 + 2 * k + 1);
+        }
       }
     }
   } else {
