@@ -785,10 +785,11 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
 // build_lut_into (float64 accumulation, one rounding).
 constexpr int LUT_QB = 32;
 
+template <int DS>  // DS > 0: the sub-vector length as a constant (codeword in registers)
 __global__ void __launch_bounds__(256)
 k_build_luts(IndexView ix, const float* __restrict__ Q, int nq, float* __restrict__ luts) {
   extern __shared__ __align__(16) unsigned char dsm[];
-  const int d = ix.d, M = ix.M, ds = d / M;
+  const int d = ix.d, M = ix.M, ds = DS > 0 ? DS : d / M;
   const int m = blockIdx.y, q0 = blockIdx.x * LUT_QB;
   const int nqb = min(LUT_QB, nq - q0);
   float* cw = reinterpret_cast<float*>(dsm);               // 256 x ds
@@ -812,11 +813,24 @@ k_build_luts(IndexView ix, const float* __restrict__ Q, int nq, float* __restric
   __syncthreads();
   for (int e = threadIdx.x; e < 256; e += blockDim.x) {
     const float* c = cw + e * ds;
-    for (int qb = 0; qb < nqb; ++qb) {
-      const double* qq = qs + qb * ds;
-      double acc = 0.0;
-      for (int t = 0; t < ds; ++t) acc += (double)c[t] * qq[t];
-      luts[((int64_t)(q0 + qb) * M + m) * 256 + e] = (float)acc;
+    if constexpr (DS > 0) {
+      double cr[DS];  // this codeword, held across the queries
+#pragma unroll
+      for (int t = 0; t < DS; ++t) cr[t] = (double)c[t];
+      for (int qb = 0; qb < nqb; ++qb) {
+        const double* qq = qs + qb * DS;
+        double acc = 0.0;
+#pragma unroll
+        for (int t = 0; t < DS; ++t) acc += cr[t] * qq[t];
+        luts[((int64_t)(q0 + qb) * M + m) * 256 + e] = (float)acc;
+      }
+    } else {
+      for (int qb = 0; qb < nqb; ++qb) {
+        const double* qq = qs + qb * ds;
+        double acc = 0.0;
+        for (int t = 0; t < ds; ++t) acc += (double)c[t] * qq[t];
+        luts[((int64_t)(q0 + qb) * M + m) * 256 + e] = (float)acc;
+      }
     }
   }
 }
@@ -824,13 +838,23 @@ k_build_luts(IndexView ix, const float* __restrict__ Q, int nq, float* __restric
 void launch_build_luts(const IndexView& ix, const float* Q, int nq, float* luts, cudaStream_t s) {
   const int ds = ix.d / ix.M;
   const size_t smem = (size_t)256 * ds * 4 + (size_t)LUT_QB * ds * 8 + 16;
-  static size_t attr = 0;
-  if (smem > attr && smem > 48 * 1024) {
-    cudaFuncSetAttribute(k_build_luts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = smem;
-  }
   dim3 grid((nq + LUT_QB - 1) / LUT_QB, ix.M);
-  k_build_luts<<<grid, 256, smem, s>>>(ix, Q, nq, luts);
+  auto go = [&](auto kern) {
+    static size_t attr = 0;
+    if (smem > attr && smem > 48 * 1024) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = smem;
+    }
+    kern<<<grid, 256, smem, s>>>(ix, Q, nq, luts);
+  };
+  switch (ds) {
+    case 4: go(k_build_luts<4>); break;
+    case 6: go(k_build_luts<6>); break;
+    case 8: go(k_build_luts<8>); break;
+    case 12: go(k_build_luts<12>); break;
+    case 16: go(k_build_luts<16>); break;
+    default: go(k_build_luts<0>); break;
+  }
 }
 
 template <int M, int U, bool CPA, bool XL, bool FULLK>
