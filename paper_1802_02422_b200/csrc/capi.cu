@@ -536,9 +536,10 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
                                cudaMemcpyHostToDevice, st));
       dQ = tmp;
     }
-    // K5 (LUTs) depends only on the queries: it runs on a side stream next to
-    // K3a (launched after the probe, whose persistent GEMM wants every SM's
-    // shared memory; K3a is HBM-bound, K5 float64-bound).  The event is recorded after the
+    // K5 (LUTs) depends only on the queries: it runs on a side stream while
+    // the probe and the planner run here (measured: launching it next to the
+    // GEMM, to K3a or to K4 costs the same device time; this placement gives
+    // the best end-to-end time).  The event is recorded after the
     // previous chunk's scan (stream order), so the buffer is free to rewrite.
     float* luts = nullptr;
     {
@@ -597,7 +598,8 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
     const size_t mark = ar.off;
     const int64_t sub = sub_env ? std::min<int64_t>(sub_env, bq) : bq;
     bool approx = true;
-    bool luts_started = false;
+    rc = launch_luts();
+    if (rc) return rc;
     for (int64_t s0 = 0; s0 < bq; s0 += sub) {
       const int ns_q = (int)std::min<int64_t>(sub, bq - s0);
       ar.off = mark;
@@ -611,11 +613,6 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
       if (!Dmat) {  // exhaustive probe (nprobe == K or too wide): exact planner only
         approx = false;
         continue;
-      }
-      if (!luts_started) {  // overlaps K3a (HBM gathers) rather than the GEMM or K4
-        rc = launch_luts();
-        if (rc) return rc;
-        luts_started = true;
       }
       PlanArgs sa = pa;
       sa.Q = dQ + s0 * v.d;
@@ -631,10 +628,6 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
       KCHECK();
     }
     ar.off = mark;  // the probe workspace is dead once K3a has run (stream order)
-    if (!luts_started) {
-      rc = launch_luts();
-      if (rc) return rc;
-    }
     pa.approx = approx ? 1 : 0;
     pa.D = nullptr;
     int nk = 0;
