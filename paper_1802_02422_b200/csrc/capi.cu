@@ -857,7 +857,7 @@ int givf_index_create(const givf_index_desc* ds, int device, givf_index_t* out) 
   if (e == cudaSuccess && tc_supported(d)) {
     // bf16 split of the centroids for the tensor-core probe (probe_tc.cu)
     void* cs = nullptr;
-    const size_t bytes = (size_t)K * tc_kpad(d) * 2;
+    const size_t bytes = (size_t)K * tc_kpad_b(d) * 2;
     e = cudaMalloc(&cs, bytes);
     if (e == cudaSuccess) {
       ix->allocs.push_back(cs);

@@ -43,7 +43,7 @@ struct IndexView {
   const float* codewords;     // (M, 256, d/M)
   const float* rotation;      // (d, d) or null
   const float* ctab;          // (256) dequantized constants, f32
-  const void* csplit;         // (K, tc_kpad(d)) bf16 [c_hi | c_lo | c_hi] or null
+  const void* csplit;         // (K, tc_kpad_b(d)) bf16 [c_hi | c_lo] or null
   unsigned long long* counters;  // [0] probe fallbacks, [1] plan fallbacks (device)
 };
 
@@ -66,7 +66,8 @@ struct ScoreOut {
 };
 
 // probe_tc.cu: tcgen05 bf16x3 probe GEMM
-int tc_kpad(int d);
+int tc_kpad(int d);    // row width of the split queries (A')
+int tc_kpad_b(int d);  // row width of the split centroids (B')
 bool tc_supported(int d);
 size_t tc_smem_bytes(int d);
 void launch_split_bf16(const float* x, int rows, int d, int centroid, void* out, cudaStream_t s);

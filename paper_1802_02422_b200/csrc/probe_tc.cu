@@ -3,16 +3,20 @@
 //
 // Precision: fp32 inputs are split into bf16 pairs x = x_hi + x_lo, and
 //   q.c ~ q_hi.c_hi + q_hi.c_lo + q_lo.c_hi
-// is ONE bf16 GEMM over a concatenated K axis: A' = [q_hi | q_hi | q_lo],
-// B' = [c_hi | c_lo | c_hi] (3d columns, zero-padded to a multiple of 64),
-// accumulated in fp32 in TMEM.  Its error is bounded a priori (eps_scale in
-// capi.cu) and every decision taken from s~ is re-checked in float64
-// (probe_recheck, k_plan_approx), so the result stays exact.
+// accumulated in fp32 in TMEM.  The centroid operand is B' = [c_hi | c_lo]
+// (2d columns); the query operand A' pairs every 64-column chunk of B' with
+// a q_hi chunk and, for the c_hi chunks, a q_lo chunk (k_split_bf16), so each
+// B chunk crosses L2 -> shared memory once for its one or two MMAs: 2d
+// columns of centroid traffic per tile instead of 3d (this GEMM is bound by
+// L2 traffic: the centroid operand is re-read once per 128-query block).
+// Its error is bounded a priori (eps_scale in capi.cu) and every decision
+// taken from s~ is re-checked in float64 (probe_recheck, k_plan_approx), so
+// the result stays exact.
 //
 // Kernel shape (sm_100a, one CTA per SM, persistent):
 //   tile = 128 queries x 256 centroids, UMMA 128x256x16, cta_group::1
-//   warp 0  TMA producer: the 128 x K' A block once per work unit (resident
-//           in smem), then B chunks of 256 x 64 through a 4-stage ring
+//   warp 0  TMA producer: the 128 x K_A A block once per work unit (resident
+//           in smem), then B chunks of 256 x 64 through a 3-stage ring
 //   warp 1  TMEM allocator + single-thread tcgen05.mma issuer; commits free
 //           the B stages and publish finished accumulators
 //   warps 2-9  epilogue: two warps per TMEM lane quarter, each owning one
@@ -62,23 +66,17 @@ struct Smem {
   uint32_t tmem_base;
 };
 
-struct Smem2 {
-  uint64_t full[8], empty[8];
-  uint64_t a_full, a_empty;
-  uint64_t tm_full[2], tm_empty[2];
-  uint32_t tmem_base;
-};
-
 }  // namespace tc
 
 // smem: [A resident: KC x 16 KB][B ring: STAGES x 32 KB][barriers]
+// KC = A' chunks (tc_ka), KB = B' chunks per tile (tc_kb), KLO = lo chunks.
 // HALF: scores leave as fp16 (ScoreOut in kernels.h), else fp32.  NS: B ring
 // depth (tc_stages).
 template <bool HALF, int NS>
 __global__ void __launch_bounds__(tc::THREADS, 1)
 k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                 const __grid_constant__ CUtensorMap mapD, int use_tma_store,
-                const float* __restrict__ c2, int nq, int K, int KC, int nsplit,
+                const float* __restrict__ c2, int nq, int K, int KC, int KB, int KLO, int nsplit,
                 float* __restrict__ D, uint16_t* __restrict__ D16, int64_t ldD,
                 const float* __restrict__ q2v, const float* __restrict__ qinv,
                 const float* __restrict__ qscale, float* __restrict__ tmin) {
@@ -135,7 +133,7 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
         for (int kc = 0; kc < KC; ++kc)
           tma_load_2d(smA + (size_t)kc * A_CHUNK, &mapA, &sm->a_full, kc * BK, mb * BM);
         for (int t = t0; t < t1; ++t) {
-          for (int kc = 0; kc < KC; ++kc) {
+          for (int kc = 0; kc < KB; ++kc) {
             mbar_wait(&sm->empty[stage], phase ^ 1);
             mbar_expect_tx(&sm->full[stage], B_CHUNK);
             tma_load_2d(smB + (size_t)stage * B_CHUNK, &mapB, &sm->full[stage], kc * BK, t * BN);
@@ -158,16 +156,25 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
         mbar_wait(&sm->tm_empty[acc], acc_phase ^ 1);
         fence_after();
         const uint32_t dcol = tmem + acc * BN;
-        for (int kc = 0; kc < KC; ++kc) {
+        for (int kc = 0; kc < KB; ++kc) {
           mbar_wait(&sm->full[stage], phase);
           fence_after();
           if (lane == 0) {
-            const uint32_t a0 = smem_u32(smA + (size_t)kc * A_CHUNK);
+            // B chunk kc meets A chunk hi_kc and, while it holds c_hi
+            // columns, lo_kc (tc_ka layout: hi_j = j + min(j, KLO))
+            const int ahi = kc + min(kc, KLO);
             const uint32_t b0 = smem_u32(smB + (size_t)stage * B_CHUNK);
+            const uint32_t a0 = smem_u32(smA + (size_t)ahi * A_CHUNK);
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
               mma_bf16(dcol, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32),
                        (kc | k) != 0 ? 1u : 0u);
+            if (kc < KLO) {
+              const uint32_t a1 = a0 + A_CHUNK;
+#pragma unroll
+              for (int k = 0; k < BK / 16; ++k)
+                mma_bf16(dcol, sw128_desc(a1 + k * 32), sw128_desc(b0 + k * 32), 1u);
+            }
             mma_commit(&sm->empty[stage]);  // frees the B stage once these MMAs retire
           }
           __syncwarp();
@@ -356,301 +363,19 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
   }
 }
 
-// Pair variant (small d): a unit is TWO 128-query m-blocks that share every
-// B chunk, so the centroid operand crosses L2->SM once per 256 queries
-// instead of once per 128.  Tiles are 128 centroids wide (UMMA 128x128x16,
-// one accumulator per m-block, double-buffered: 4 x 128 TMEM columns); K is
-// split in 32-element (64 B, SWIZZLE_64B) chunks, so K' = 3d needs no
-// padding for d = 96.  Warp e of the epilogue owns m-block e/4, lane
-// quarter warp%4, all 128 columns of the tile.
-// smem: [A resident: 2 x KC x 8 KB][B ring: STAGES2 x 8 KB][epilogue][barriers]
-template <bool HALF>
-__global__ void __launch_bounds__(tc::THREADS, 1)
-k_probe_gemm_tc2(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                const __grid_constant__ CUtensorMap mapD, int use_tma_store,
-                const float* __restrict__ c2, int nq, int K, int KC, int nsplit,
-                float* __restrict__ D, uint16_t* __restrict__ D16, int64_t ldD,
-                const float* __restrict__ q2v, const float* __restrict__ qinv,
-                const float* __restrict__ qscale, float* __restrict__ tmin) {
-  using namespace tc;
-  constexpr int BN2 = 128, BK2 = 32;
-  constexpr int STAGES2 = HALF ? 7 : 4;           // fp16 staging tiles are half the size
-  constexpr uint32_t SBW = HALF ? 2048 : 4096;    // per-warp output staging tile
-  constexpr uint32_t A2_CHUNK = BM * BK2 * 2, B2_CHUNK = BN2 * BK2 * 2;  // 8 KB each
-  constexpr uint32_t IDESC2 = make_idesc(BM, BN2);
-  extern __shared__ __align__(1024) unsigned char dsm[];
-  unsigned char* base = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(dsm) + 1023) & ~(uintptr_t)1023);
-  unsigned char* smA = base;
-  unsigned char* smB = base + (size_t)2 * KC * A2_CHUNK;
-  Smem2* sm = reinterpret_cast<Smem2*>(smB + (size_t)STAGES2 * B2_CHUNK + EPI_WARPS * (SBW + 512));
+// Operand layouts ("reuse" split, 3 bf16 products per score):
+//   B' (centroids, row width KB * 64): [c_hi (d) | c_lo (d) | 0 pad]
+//   A' (queries, KA * 64): for every 64-column chunk j of B', an A chunk
+//     hi_j with q_hi at the dimension of each column (c_hi and c_lo columns
+//     alike), then -- when chunk j holds c_hi columns -- a chunk lo_j with
+//     q_lo at the c_hi columns and 0 elsewhere.
+// So sum_j hi_j . B_j + lo_j . B_j = q_hi.c_hi + q_hi.c_lo + q_lo.c_hi, and
+// every B chunk crosses L2 -> SMEM once for its one or two MMAs: 2d columns
+// of B per tile instead of 3d.
+__host__ __device__ inline int tc_kb(int d) { return (2 * d + 63) / 64; }
+__host__ __device__ inline int tc_lo_chunks(int d) { return (d + 63) / 64; }
+__host__ __device__ inline int tc_ka(int d) { return tc_kb(d) + tc_lo_chunks(d); }
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m_pairs = (nq + 2 * BM - 1) / (2 * BM);
-  const int n_tiles = (K + BN2 - 1) / BN2;
-  const int units = m_pairs * nsplit;
-  const int per_split = (n_tiles + nsplit - 1) / nsplit;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES2; ++s) { mbar_init(&sm->full[s], 1); mbar_init(&sm->empty[s], 1); }
-    mbar_init(&sm->a_full, 1);
-    mbar_init(&sm->a_empty, 1);
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(&sm->tm_full[a], 1);
-      mbar_init(&sm->tm_empty[a], EPI_WARPS);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&sm->tmem_base)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  fence_before();
-  __syncthreads();
-  fence_after();
-  const uint32_t tmem = sm->tmem_base;
-
-  if (warp == 0) {
-    // ------------------------------------------------ TMA producer
-    if (lane == 0) {
-      uint32_t stage = 0, phase = 0, a_phase = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int mb = u / nsplit, sp = u % nsplit;
-        const int t0 = sp * per_split, t1 = min(n_tiles, t0 + per_split);
-        if (t0 >= t1) continue;
-        mbar_wait(&sm->a_empty, a_phase ^ 1);
-        a_phase ^= 1;
-        mbar_expect_tx(&sm->a_full, (uint32_t)2 * KC * A2_CHUNK);
-        for (int h = 0; h < 2; ++h)
-          for (int kc = 0; kc < KC; ++kc)
-            tma_load_2d(smA + (size_t)(h * KC + kc) * A2_CHUNK, &mapA, &sm->a_full, kc * BK2,
-                        (mb * 2 + h) * BM);
-        for (int t = t0; t < t1; ++t) {
-          for (int kc = 0; kc < KC; ++kc) {
-            mbar_wait(&sm->empty[stage], phase ^ 1);
-            mbar_expect_tx(&sm->full[stage], B2_CHUNK);
-            tma_load_2d(smB + (size_t)stage * B2_CHUNK, &mapB, &sm->full[stage], kc * BK2, t * BN2);
-            if (++stage == STAGES2) { stage = 0; phase ^= 1; }
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer
-    uint32_t stage = 0, phase = 0, a_phase = 0, acc = 0, acc_phase = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int sp = u % nsplit;
-      const int t0 = sp * per_split, t1 = min(n_tiles, t0 + per_split);
-      if (t0 >= t1) continue;
-      mbar_wait(&sm->a_full, a_phase);
-      a_phase ^= 1;
-      fence_after();
-      for (int t = t0; t < t1; ++t) {
-        mbar_wait(&sm->tm_empty[acc], acc_phase ^ 1);
-        fence_after();
-        for (int kc = 0; kc < KC; ++kc) {
-          mbar_wait(&sm->full[stage], phase);
-          fence_after();
-          if (lane == 0) {
-            const uint32_t b0 = smem_u32(smB + (size_t)stage * B2_CHUNK);
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {  // both m-blocks read this B chunk
-              const uint32_t a0 = smem_u32(smA + (size_t)(h * KC + kc) * A2_CHUNK);
-              const uint32_t dcol = tmem + (uint32_t)(acc * 2 + h) * BN2;
-#pragma unroll
-              for (int k = 0; k < BK2 / 16; ++k)
-                tcx::mma_bf16(dcol, sw64_desc(a0 + k * 32), sw64_desc(b0 + k * 32), IDESC2,
-                              (kc | k) != 0 ? 1u : 0u);
-            }
-            mma_commit(&sm->empty[stage]);  // frees the B stage once these MMAs retire
-          }
-          __syncwarp();
-          if (++stage == STAGES2) { stage = 0; phase ^= 1; }
-        }
-        if (lane == 0) mma_commit(&sm->tm_full[acc]);  // accumulator ready
-        __syncwarp();
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-      }
-      if (lane == 0) mma_commit(&sm->a_empty);  // A block may be replaced
-      __syncwarp();
-    }
-  } else {
-    // ------------------------------------------------ epilogue (warps 2..9)
-    const int e = warp - 2;
-    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
-    const int half = e >> 2;       // m-block of the pair
-    const int ntiles128 = n_tiles;
-    // per-warp 32x32 fp32 staging tile for the TMA store (SWIZZLE_128B: the
-    // 16-byte chunk k of row r sits at chunk k ^ (r & 7))
-    unsigned char* sb = smB + (size_t)STAGES2 * B2_CHUNK + (size_t)e * SBW;
-    float* c2s = reinterpret_cast<float*>(smB + (size_t)STAGES2 * B2_CHUNK + EPI_WARPS * SBW) +
-                 e * 128;
-    uint32_t acc = 0, acc_phase = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int mb = u / nsplit, sp = u % nsplit;
-      const int t0 = sp * per_split, t1 = min(n_tiles, t0 + per_split);
-      const int q = (mb * 2 + half) * BM + quarter * 32 + lane;
-      float q2r = 0.f, ir = 1.f;  // fp16 encoding of this row
-      if (HALF && q < nq) { q2r = q2v[q]; ir = qinv[q]; }
-      const float q2ir = q2r * ir;
-      for (int t = t0; t < t1; ++t) {
-        const int colh = t * BN2;
-        // this half tile's |c|^2 terms: loaded before the accumulator wait so
-        // their latency hides behind it, then kept in a per-warp smem copy
-        float c2r[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int col = colh + c * 32 + lane;
-          c2r[c] = col < K ? __ldg(c2 + col) : 0.f;
-        }
-        mbar_wait(&sm->tm_full[acc], acc_phase);
-        fence_after();
-#pragma unroll
-        for (int c = 0; c < 4; ++c) c2s[c * 32 + lane] = c2r[c];
-        __syncwarp();
-        float* drow = HALF ? nullptr : D + (int64_t)q * ldD;
-        uint16_t* hrow = HALF ? D16 + (int64_t)q * ldD : nullptr;
-        float mn = __int_as_float(0x7f800000);
-        __half2 mn2 = __floats2half2_rn(mn, mn);  // HALF: minimum in the encoded domain
-        const uint32_t tb =
-            tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * 2 + half) * BN2;
-        uint32_t ra[32], rb[32];
-        tmem_ld32_async(tb, ra);
-        tmem_wait_ld(ra);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t* r = (c & 1) ? rb : ra;
-          uint32_t* rn = (c & 1) ? ra : rb;
-          if (c < 3) tmem_ld32_async(tb + (c + 1) * 32, rn);  // next chunk in flight
-          const int col0 = colh + c * 32;
-          float v[32];
-          if (col0 + 32 <= K) {
-            const float4* c24 = reinterpret_cast<const float4*>(c2s + c * 32);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const float4 cc = c24[i];  // smem broadcast
-              v[4 * i] = fmaf(-2.f, __uint_as_float(r[4 * i]), cc.x);
-              v[4 * i + 1] = fmaf(-2.f, __uint_as_float(r[4 * i + 1]), cc.y);
-              v[4 * i + 2] = fmaf(-2.f, __uint_as_float(r[4 * i + 2]), cc.z);
-              v[4 * i + 3] = fmaf(-2.f, __uint_as_float(r[4 * i + 3]), cc.w);
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const int col = col0 + i;
-              v[i] = col < K ? fmaf(-2.f, __uint_as_float(r[i]), __ldg(c2 + col))
-                             : __int_as_float(0x7f800000);
-            }
-          }
-          if constexpr (HALF) {
-            // (v + |q|^2) * 2^-e as one FMA (exact scaling), packed f16x2
-            // conversion and a packed running minimum
-            uint32_t hp[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const __half2 h = __floats2half2_rn(fmaf(v[2 * i], ir, q2ir), fmaf(v[2 * i + 1], ir, q2ir));
-              mn2 = __hmin2(mn2, h);
-              hp[i] = *reinterpret_cast<const uint32_t*>(&h);
-            }
-            if (use_tma_store) {
-              if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-              __syncwarp();
-              // 32 rows x 64 B, SWIZZLE_64B: chunk k of row r at k ^ ((r >> 1) & 3)
-#pragma unroll
-              for (int k = 0; k < 4; ++k)
-                *reinterpret_cast<uint4*>(sb + lane * 64 + ((k ^ ((lane >> 1) & 3)) * 16)) =
-                    make_uint4(hp[4 * k], hp[4 * k + 1], hp[4 * k + 2], hp[4 * k + 3]);
-              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-              __syncwarp();
-              if (lane == 0) {
-                asm volatile(
-                    "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                        reinterpret_cast<uint64_t>(&mapD)),
-                    "r"(col0), "r"((mb * 2 + half) * BM + quarter * 32), "r"(smem_u32(sb))
-                    : "memory");
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-              }
-            } else if (q < nq) {
-              if (col0 + 32 <= K && (ldD & 7) == 0) {
-                uint4* dst = reinterpret_cast<uint4*>(hrow + col0);
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                  dst[k] = make_uint4(hp[4 * k], hp[4 * k + 1], hp[4 * k + 2], hp[4 * k + 3]);
-              } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i)
-                  if (col0 + i < K) hrow[col0 + i] = (uint16_t)(hp[i >> 1] >> ((i & 1) * 16));
-              }
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) mn = fminf(mn, v[i]);
-            if (use_tma_store) {
-              // the previous store from this staging tile has read it
-              if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-              __syncwarp();
-#pragma unroll
-              for (int k = 0; k < 8; ++k)
-                *reinterpret_cast<float4*>(sb + lane * 128 + ((k ^ (lane & 7)) * 16)) =
-                    make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
-              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-              __syncwarp();
-              if (lane == 0) {
-                asm volatile(
-                    "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                        reinterpret_cast<uint64_t>(&mapD)),
-                    "r"(col0), "r"((mb * 2 + half) * BM + quarter * 32), "r"(smem_u32(sb))
-                    : "memory");
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-              }
-            } else if (q < nq) {
-              if (col0 + 32 <= K) {
-                float4* dst = reinterpret_cast<float4*>(drow + col0);
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-                  dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-              } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i)
-                  if (col0 + i < K) drow[col0 + i] = v[i];
-              }
-            }
-          }
-          if (c < 3) tmem_wait_ld(rn);
-        }
-        const int h = t;  // the 128-centroid tile
-        if (q < nq && tmin && h < ntiles128) {
-          if (HALF)  // the tile minimum's fp16 code
-            reinterpret_cast<uint16_t*>(tmin)[(int64_t)q * ntiles128 + h] =
-                __half_as_ushort(__hmin(__low2half(mn2), __high2half(mn2)));
-          else
-            tmin[(int64_t)q * ntiles128 + h] = mn;
-        }
-        fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm->tm_empty[acc]);
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-      }
-    }
-    if (use_tma_store && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-  }
-  fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(TMEM_COLS));
-  }
-}
-
-// A' / B' rows: [x_hi | x_hi | x_lo] (queries) or [x_hi | x_lo | x_hi]
-// (centroids), bf16, zero-padded to Kp columns.
 __global__ void k_split_bf16(const float* __restrict__ x, int rows, int d, int Kp, int centroid,
                              __nv_bfloat16* __restrict__ out) {
   const int64_t n = (int64_t)rows * Kp;
@@ -658,14 +383,32 @@ __global__ void k_split_bf16(const float* __restrict__ x, int rows, int d, int K
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / Kp;
     const int c = (int)(e % Kp);
+    int bc = -1;       // column of B' this element pairs with
+    bool lo = false;   // A' lo chunk (q_lo at c_hi columns)
+    if (centroid) {
+      bc = c;
+    } else {
+      int a = c >> 6, j = 0;  // A' chunk a -> (B' chunk j, hi / lo)
+      for (; j < tc_kb(d); ++j) {
+        if (a == 0) break;
+        --a;
+        if (j < tc_lo_chunks(d)) {
+          if (a == 0) { lo = true; break; }
+          --a;
+        }
+      }
+      bc = j * 64 + (c & 63);
+    }
     float v = 0.f;
-    if (c < 3 * d) {
-      const int part = c / d, j = c % d;
-      const float f = x[r * d + j];
-      const __nv_bfloat16 hi = __float2bfloat16_rn(f);
-      const bool take_lo = centroid ? (part == 1) : (part == 2);
-      v = take_lo ? __bfloat162float(__float2bfloat16_rn(f - __bfloat162float(hi)))
-                  : __bfloat162float(hi);
+    if (bc < 2 * d) {
+      const bool chi = bc < d;  // c_hi column (else c_lo)
+      const int dim = chi ? bc : bc - d;
+      const float f = x[r * d + dim];
+      const float hi = __bfloat162float(__float2bfloat16_rn(f));
+      const float flo = __bfloat162float(__float2bfloat16_rn(f - hi));
+      if (centroid) v = chi ? hi : flo;
+      else if (!lo) v = hi;
+      else v = chi ? flo : 0.f;
     }
     out[e] = __float2bfloat16_rn(v);
   }
@@ -734,14 +477,16 @@ int num_sms() {
 
 }  // namespace
 
-int tc_kpad(int d) { return ((3 * d + tc::BK - 1) / tc::BK) * tc::BK; }
+// Row widths of the split operands (tc_ka / tc_kb layout above).
+int tc_kpad(int d) { return tc_ka(d) * tc::BK; }    // queries (A')
+int tc_kpad_b(int d) { return tc_kb(d) * tc::BK; }  // centroids (B')
 
 size_t tc_smem_bytes(int d);
 // A block resident (<= 96 KB) next to the B ring and the epilogue staging
-bool tc_supported(int d) { return tc_kpad(d) <= 6 * tc::BK && tc_smem_bytes(d) <= 227 * 1024; }
+bool tc_supported(int d) { return tc_ka(d) <= 6 && tc_smem_bytes(d) <= 227 * 1024; }
 
 void launch_split_bf16(const float* x, int rows, int d, int centroid, void* out, cudaStream_t s) {
-  const int Kp = tc_kpad(d);
+  const int Kp = centroid ? tc_kpad_b(d) : tc_kpad(d);
   int64_t n = (int64_t)rows * Kp;
   int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
   k_split_bf16<<<blocks, 256, 0, s>>>(x, rows, d, Kp, centroid,
@@ -750,66 +495,45 @@ void launch_split_bf16(const float* x, int rows, int d, int centroid, void* out,
 
 // B ring depth: 3, or 2 when a 6-chunk resident A block (d > 106) leaves no
 // room for the third stage
-int tc_stages(int d) { return tc_kpad(d) / tc::BK >= 6 ? 2 : tc::STAGES; }
+int tc_stages(int d) { return tc_ka(d) >= 6 ? 2 : tc::STAGES; }
 size_t tc_smem_bytes(int d) {
-  const int KC = tc_kpad(d) / tc::BK;
+  const int KC = tc_ka(d);
   return 1024 + (size_t)KC * tc::A_CHUNK + (size_t)tc_stages(d) * tc::B_CHUNK + tc::STAGE_OUT +
          sizeof(tc::Smem) + 64;
 }
 
-// K' of the pair kernel: 3d rounded to 32 (no padding for d = 96)
-int tc2_kpad(int d) { return ((3 * d + 31) / 32) * 32; }
-size_t tc2_smem_bytes(int d, bool half) {
-  const size_t stages = half ? 7 : 4, sbw = half ? 2048 : 4096;
-  return 1024 + (size_t)tc2_kpad(d) * 512 + stages * 8192 + tc::EPI_WARPS * (sbw + 512) +
-         sizeof(tc::Smem2) + 64;
-}
-// The pair kernel halves the centroid operand's L2->SM traffic but measured
-// slower on C2 (the epilogue, not operand traffic, bounds this GEMM):
-// opt-in with GIVF_GEMM_PAIR=1.
-bool tc2_supported(int d) {
-  static const bool on = getenv("GIVF_GEMM_PAIR") && atoi(getenv("GIVF_GEMM_PAIR")) == 1;
-  return on && tc2_smem_bytes(d, true) <= 227 * 1024 && tc2_smem_bytes(d, false) <= 227 * 1024;
-}
-
 bool launch_probe_gemm_tc(const void* Abf, const void* Bbf, const float* c2, int nq, int K, int d,
                           const ScoreOut& o, float* tmin, cudaStream_t s) {
-  const int Kp = tc_kpad(d);
+  const int ka = tc_kpad(d), kb = tc_kpad_b(d);
   const bool half = o.D16 != nullptr;
-  const bool pair = tc2_supported(d);
-  const int kcols = pair ? tc2_kpad(d) : Kp;
-  const int box_k = pair ? 32 : tc::BK;
-  const int box_n = pair ? 128 : tc::BN;
   CUtensorMap ma, mb, md;
-  if (!make_map(&ma, Abf, nq, kcols, Kp, box_k, tc::BM) ||
-      !make_map(&mb, Bbf, K, kcols, Kp, box_k, box_n))
+  if (!make_map(&ma, Abf, nq, ka, ka, tc::BK, tc::BM) ||
+      !make_map(&mb, Bbf, K, kb, kb, tc::BK, tc::BN))
     return false;
   // scores go out through TMA stores when the row pitch allows it (16 B)
   void* dptr = half ? (void*)o.D16 : (void*)o.D32;
   int use_tma_store = ((o.ld * (half ? 2 : 4)) % 16 == 0) ? 1 : 0;
-  if (use_tma_store && !make_map_out(&md, dptr, nq, K, o.ld, half, pair ? 32 : 64))
-    use_tma_store = 0;
+  if (use_tma_store && !make_map_out(&md, dptr, nq, K, o.ld, half, 64)) use_tma_store = 0;
   if (!use_tma_store) md = ma;  // unused
-  const int KC = kcols / box_k;
-  const int m_units = pair ? (nq + 2 * tc::BM - 1) / (2 * tc::BM) : (nq + tc::BM - 1) / tc::BM;
-  const int n_tiles = (K + box_n - 1) / box_n;
+  const int m_units = (nq + tc::BM - 1) / tc::BM;
+  const int n_tiles = (K + tc::BN - 1) / tc::BN;
   const int sms = num_sms();
   int nsplit = std::max(1, std::min(n_tiles, (2 * sms + m_units - 1) / m_units));
   const int units = m_units * nsplit;
   const int grid = std::min(units, sms);
-  const size_t smem = pair ? tc2_smem_bytes(d, half) : tc_smem_bytes(d);
+  const size_t smem = tc_smem_bytes(d);
   const bool ns2 = tc_stages(d) == 2;
-  auto kern = pair ? (half ? k_probe_gemm_tc2<true> : k_probe_gemm_tc2<false>)
-                   : (half ? (ns2 ? k_probe_gemm_tc<true, 2> : k_probe_gemm_tc<true, 3>)
-                           : (ns2 ? k_probe_gemm_tc<false, 2> : k_probe_gemm_tc<false, 3>));
-  static size_t attr[6] = {0, 0, 0, 0, 0, 0};
-  const int slot = (pair ? 2 : ns2 ? 4 : 0) + (half ? 1 : 0);
+  auto kern = half ? (ns2 ? k_probe_gemm_tc<true, 2> : k_probe_gemm_tc<true, 3>)
+                   : (ns2 ? k_probe_gemm_tc<false, 2> : k_probe_gemm_tc<false, 3>);
+  static size_t attr[4] = {0, 0, 0, 0};
+  const int slot = (ns2 ? 2 : 0) + (half ? 1 : 0);
   if (attr[slot] < smem) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr[slot] = smem;
   }
-  kern<<<grid, tc::THREADS, smem, s>>>(ma, mb, md, use_tma_store, c2, nq, K, KC, nsplit, o.D32,
-                                       o.D16, o.ld, o.q2, o.qinv, o.qscale, tmin);
+  kern<<<grid, tc::THREADS, smem, s>>>(ma, mb, md, use_tma_store, c2, nq, K, tc_ka(d), tc_kb(d),
+                                       tc_lo_chunks(d), nsplit, o.D32, o.D16, o.ld, o.q2, o.qinv,
+                                       o.qscale, tmin);
   return true;
 }
 

@@ -1,5 +1,5 @@
 // tcgen05 / TMA / mbarrier helpers shared by the probe GEMM kernels
-// (probe_tc.cu, probe_tc2.cu).  sm_100a only.
+// (probe_tc.cu).  sm_100a only.
 #pragma once
 #include <cuda.h>
 #include <cudaTypedefs.h>

@@ -101,7 +101,6 @@ def default_mode_result():
 
 @pytest.mark.parametrize("env_over", [
     {"GIVF_PROBE": "simt"},                        # SIMT fp32 probe GEMM
-    {"GIVF_GEMM_PAIR": "1"},                       # two m-blocks per B chunk (UMMA 128x128)
     {"GIVF_PROBE_SUB": "5"},                       # probe + K3a in sub-chunks
     {"GIVF_STREAMS": "2", "GIVF_CHUNK_QUERIES": "3"},  # chunks on two streams
     {"GIVF_SCAN": "block"},                        # block-synchronous scan
