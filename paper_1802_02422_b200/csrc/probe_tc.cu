@@ -31,6 +31,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -518,7 +519,23 @@ bool launch_probe_gemm_tc(const void* Abf, const void* Bbf, const float* c2, int
   const int m_units = (nq + tc::BM - 1) / tc::BM;
   const int n_tiles = (K + tc::BN - 1) / tc::BN;
   const int sms = num_sms();
-  int nsplit = std::max(1, std::min(n_tiles, (2 * sms + m_units - 1) / m_units));
+  // Work units = (m-block, slice of the n-tiles), spread over one CTA per
+  // SM.  Pick the slice count that minimises the busiest CTA's tiles, with
+  // one tile's worth of overhead per unit (its A-block load):
+  //   cost(ns) = ceil(m_units * ns / sms) * (ceil(n_tiles / ns) + 1)
+  // (C2: 16 slices -> 9 units of 16 tiles per CTA, 5 % above the even
+  // split; a fixed ~2 units per SM left a third of the SMs a unit behind).
+  int nsplit = 1;
+  {
+    int64_t best = -1;
+    const int hi = std::min(n_tiles, 64);
+    for (int ns = 1; ns <= hi; ++ns) {
+      const int64_t per_cta = ((int64_t)m_units * ns + sms - 1) / sms;
+      const int64_t cost = per_cta * ((n_tiles + ns - 1) / ns + 1);
+      if (best < 0 || cost < best) { best = cost; nsplit = ns; }
+    }
+    if (const char* e = getenv("GIVF_GEMM_SPLIT")) nsplit = std::max(1, std::min(n_tiles, atoi(e)));
+  }
   const int units = m_units * nsplit;
   const int grid = std::min(units, sms);
   const size_t smem = tc_smem_bytes(d);
