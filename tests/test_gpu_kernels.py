@@ -108,6 +108,8 @@ def default_mode_result():
     {"GIVF_SCAN_STAGE": "registers"},              # warp scan, register staging
     {"GIVF_SCAN_GROUP": "2"},                      # warp scan, 2 batches summed together
     {"GIVF_SCAN_LUT": "plain"},                    # warp scan, [m][256] LUT (bank conflicts)
+    {"GIVF_GEMM_SPLIT": "3"},                      # probe GEMM work units: 3 slices per m-block
+    {"GIVF_RS_SPLIT": "5"},                        # K4b: 5 CTAs per query
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_execution_modes_agree(env_over, default_mode_result):
     """Every tuning knob changes how the work is scheduled, never the result:
