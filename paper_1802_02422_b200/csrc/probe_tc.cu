@@ -528,8 +528,7 @@ bool launch_probe_gemm_tc(const void* Abf, const void* Bbf, const float* c2, int
   int nsplit = 1;
   {
     int64_t best = -1;
-    const int hi = std::min(n_tiles, 64);
-    for (int ns = 1; ns <= hi; ++ns) {
+    for (int ns = 1; ns <= n_tiles; ++ns) {
       const int64_t per_cta = ((int64_t)m_units * ns + sms - 1) / sms;
       const int64_t cost = per_cta * ((n_tiles + ns - 1) / ns + 1);
       if (best < 0 || cost < best) { best = cost; nsplit = ns; }
