@@ -42,7 +42,8 @@ constexpr int PA_ITEMS = 4096;    // items staged in shared memory (else read fr
 constexpr int PA_BUCKETS = 1024;
 constexpr int PA_SORT = 1024;     // boundary-bucket sort capacity
 constexpr int PA_SMALL = 128;     // refine further while the bucket is larger
-constexpr int PA_WCAP = 256;      // window capacity
+constexpr int PA_WCAP = 256;      // window capacity (items staged in shared memory)
+constexpr int PA_WCAP_BIG = 1024; // window capacity when the items are not staged
 constexpr int PA_CAND = 1536;     // begun groups (else the exact planner)
 constexpr int PA_PSTAGE = 512;    // probed regions staged in shared memory
 constexpr int PA_U = 4;           // centroid rows in flight per 8-lane group
@@ -92,6 +93,7 @@ __global__ void __launch_bounds__(PA_THREADS) k_plan_scores_approx(PlanArgs a) {
 struct PaSmem {
   // byte offsets into the dynamic shared block
   size_t skey, ssz, pool, wkey, wval, wlen, wrow, wnorm, qd, preg, pqc, pal, bytes;
+  int wcap;  // window capacity: larger when the items' staging space is free
   // small: every group size < 2^16, so the staged sizes are 16-bit
   __host__ __device__ PaSmem(int d, int P, int64_t total, bool small) {
     const bool staged = total <= PA_ITEMS;
@@ -100,15 +102,16 @@ struct PaSmem {
     auto take = [&](size_t n) { size_t r = o; o = (o + n + 15) & ~(size_t)15; return r; };
     pool = take((size_t)3 * PA_CAND * 4 > (size_t)(PA_BUCKETS + PA_SORT) * 8
                     ? (size_t)3 * PA_CAND * 4 : (size_t)(PA_BUCKETS + PA_SORT) * 8);
-    wkey = take((size_t)PA_WCAP * 8);
+    wcap = staged ? PA_WCAP : PA_WCAP_BIG;
+    wkey = take((size_t)wcap * 8);
     qd = take((size_t)d * 8);
     pqc = take(pst ? (size_t)P * 8 : 0);
     pal = take(pst ? (size_t)P * 8 : 0);
     preg = take(pst ? (size_t)P * 4 : 0);
-    wval = take((size_t)PA_WCAP * 4);
-    wlen = take((size_t)PA_WCAP * 4);
-    wrow = take((size_t)PA_WCAP * 4);
-    wnorm = take((size_t)PA_WCAP * 4);
+    wval = take((size_t)wcap * 4);
+    wlen = take((size_t)wcap * 4);
+    wrow = take((size_t)wcap * 4);
+    wnorm = take((size_t)wcap * 4);
     skey = take(staged ? (size_t)PA_ITEMS * 4 : 0);
     ssz = take(staged ? (size_t)PA_ITEMS * (small ? 2 : 4) : 0);
     bytes = o;
@@ -423,7 +426,7 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
         cw += (1ull << CW) | (unsigned long long)SIZE(f);
       } else if (kf <= khi && !no_cut) {
         const uint32_t p = atomicAdd(&s_nw, 1u);
-        if (p < PA_WCAP) wval[p] = (uint32_t)f;
+        if (p < (uint32_t)L.wcap) wval[p] = (uint32_t)f;
       }
     }
     cw = block_sum(cw, red64);
@@ -431,16 +434,16 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
     wA = cw & WMASK;
   }
   const uint32_t nw = s_nw;
-  if (nw > (uint32_t)PA_WCAP && !flag) { flag = true; why = 1; }
+  if (nw > (uint32_t)L.wcap && !flag) { flag = true; why = 1; }
   int lastw = -1;
   unsigned long long wsum = 0;  // lengths of the begun window groups
   if (!flag && !no_cut) {
     // one metadata gather per window group, then the centroid rows
     PLAN_PHASE(1);
-    if (tid < (int)nw) {
-      const int64_t gi = GI(wval[tid]);
-      wrow[tid] = ix.grouping ? ix.nbr[gi] : 0;
-      wnorm[tid] = ix.grouping ? ix.norm[gi] : 0.f;
+    for (int i = tid; i < (int)nw; i += PA_THREADS) {
+      const int64_t gi = GI(wval[i]);
+      wrow[i] = ix.grouping ? ix.nbr[gi] : 0;
+      wnorm[i] = ix.grouping ? ix.norm[gi] : 0.f;
     }
     __syncthreads();
     PLAN_PHASE(10);
