@@ -30,6 +30,10 @@ EXPORTS = (
     "givf_kernel_launches",
     "givf_profile_enable",
     "givf_profile_read",
+    # include/givf_build.h
+    "givf_assign_nearest",
+    "givf_encode_rows",
+    "givf_knn_exact",
 )
 
 STAGES = ("probe_gemm", "probe_select", "probe_recheck", "probe_full", "plan", "scan",
@@ -82,6 +86,34 @@ class SearchStatsC(ctypes.Structure):
     ]
 
 
+class EncodeDesc(ctypes.Structure):
+    """givf_encode_desc (include/givf_build.h)."""
+
+    _fields_ = [
+        ("x", ctypes.c_void_p),
+        ("order", ctypes.c_void_p),
+        ("seg", ctypes.c_void_p),
+        ("seg_region", ctypes.c_void_p),
+        ("nseg", ctypes.c_int64),
+        ("dim", ctypes.c_int32),
+        ("l", ctypes.c_int32),
+        ("m", ctypes.c_int32),
+        ("grouping", ctypes.c_int32),
+        ("centroids", ctypes.c_void_p),
+        ("neighbor_ids", ctypes.c_void_p),
+        ("alphas", ctypes.c_void_p),
+        ("c_sq", ctypes.c_void_p),
+        ("codewords", ctypes.c_void_p),
+        ("cw_sq", ctypes.c_void_p),
+        ("const_lo", ctypes.c_double),
+        ("const_step", ctypes.c_double),
+        ("pick", ctypes.c_void_p),
+        ("codes", ctypes.c_void_p),
+        ("const_bytes", ctypes.c_void_p),
+        ("consts", ctypes.c_void_p),
+    ]
+
+
 _lib = None
 
 
@@ -112,6 +144,9 @@ def load(path: str = LIB_PATH):
     lib.givf_kernel_launches.restype = i64
     lib.givf_profile_enable.argtypes = [ctypes.c_int]
     lib.givf_profile_read.argtypes = [vp, vp, i32]
+    lib.givf_assign_nearest.argtypes = [vp, i64, vp, i32, i32, vp, vp, vp]
+    lib.givf_encode_rows.argtypes = [ctypes.POINTER(EncodeDesc), vp]
+    lib.givf_knn_exact.argtypes = [vp, i64, vp, i64, i32, i32, vp, vp, vp]
     _lib = lib
     return lib
 

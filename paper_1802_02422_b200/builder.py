@@ -4,33 +4,50 @@ consumes, following the semantics of the reference `build_index`
 (/root/reference/pkg/src/givf/index.py:249-380), and exact ground truth
 (datasets.py:34-61 semantics: float64 ranking, ties by id).
 
-This is offline tooling on PyTorch (cuBLAS GEMMs); it is not on the query
-path.  Deviations from the reference build, all outside the searched data
-semantics:
+The row-sized work runs in the library's own sm_100a kernels
+(include/givf_build.h):
+  * nearest centroid (k-means steps and region assignment) -- KA, a tcgen05
+    GEMM with an arg-min epilogue (`givf_assign_nearest`);
+  * group pick, residual PQ codes, constant term and byte of every row -- KE
+    (`givf_encode_rows`), one pass over rows grouped by region;
+  * exact k-NN (ground truth, the centroids' neighbour lists) -- the search
+    path's certified probe (`givf_knn_exact`).
+PyTorch holds the buffers and runs the small training reductions (centroid
+means, alpha fits, percentiles); nothing row-sized goes through the host.
+
+Deviations from the reference build, all outside the searched data
+semantics (the search path's parity does not depend on how an index was
+built):
   * k-means is seeded with a random sample instead of k-means++
-    (kmeans.py:80-104): k-means++ is K sequential passes, hours at K=2^16.
-  * region assignment is exact (f32 expanded form, first minimum) for every
-    K; the reference switches to approximate graph assignment at K >= 2^16
-    (kmeans.py:18, index.py:88-99).
+    (kmeans.py:80-104); empty clusters are re-seeded at random rows.
+  * region assignment uses bf16 products with fp32 accumulation (the
+    reference itself assigns through its approximate graph at K >= 2^16,
+    index.py:88-99); near-ties may resolve differently from float32.
+  * neighbour lists are ordered by (float32(d64), id) (the probe's order)
+    instead of float32 expanded distances.
 Every quantity the query path reads -- alphas (grouping.py:44-74), group
 picks (index.py:124-138), PQ codes of displacements (index.py:213-246),
 constant bytes (index.py:160-170, grouping.py:132-145), norm terms
 (index.py:173-192) and the (region, group, id) layout (index.py:326-337) --
-is computed with the reference's formulas.
+follows the reference's formulas.
 """
 
 from __future__ import annotations
 
+import ctypes
 import hashlib
 import math
+import time
 from dataclasses import dataclass
 
 import numpy as np
 import torch
 
+from . import _native
 from .device_index import IndexArrays
 
 CHUNK_ROWS = 1 << 20  # generator chunk: any row range can be regenerated
+ENCODE_ROWS = 1 << 24  # rows assigned / encoded per pass
 
 
 def derive_seed(seed: int, tag: str) -> int:
@@ -84,13 +101,14 @@ def cluster_means(spec: SynthSpec, device="cuda") -> torch.Tensor:
 
 
 def synth_rows(spec: SynthSpec, tag: str, start: int, count: int, means=None,
-               device="cuda") -> torch.Tensor:
+               device="cuda", out=None) -> torch.Tensor:
     """Rows [start, start+count) of stream `tag` ('base', 'learn', 'query').
     Chunked counter-style seeding: row r lives in chunk r // CHUNK_ROWS whose
     generator is seeded by (seed, tag, chunk)."""
     if means is None:
         means = cluster_means(spec, device)
-    out = torch.empty(count, spec.d, device=device, dtype=torch.float32)
+    if out is None:
+        out = torch.empty(count, spec.d, device=device, dtype=torch.float32)
     s = spec.coord_sigma()
     c0, c1 = start // CHUNK_ROWS, (start + count - 1) // CHUNK_ROWS if count else -1
     for c in range(c0, c1 + 1):
@@ -109,102 +127,129 @@ def synth_rows(spec: SynthSpec, tag: str, start: int, count: int, means=None,
     return out
 
 
-# ---------------------------------------------------------------- primitives
+# ---------------------------------------------------------------- native steps
 
 
-# Fast builds (1B-row benchmark indexes) let the nearest-centroid matmuls use
-# TF32 tensor cores; assignments may then differ from exact fp32 ones at
-# near-ties.  The index is still a valid GroupedIndex -- the search path and
-# its parity do not depend on how the index was built.
-FAST_BUILD = False
+def _vp(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
-class _NoTF32:
-    def __enter__(self):
-        self.a = torch.backends.cuda.matmul.allow_tf32
-        self.b = torch.backends.cudnn.allow_tf32
-        torch.backends.cuda.matmul.allow_tf32 = FAST_BUILD
-        torch.backends.cudnn.allow_tf32 = FAST_BUILD
-
-    def __exit__(self, *exc):
-        torch.backends.cuda.matmul.allow_tf32 = self.a
-        torch.backends.cudnn.allow_tf32 = self.b
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
-def sq_dists(x: torch.Tensor, c: torch.Tensor, c_sq=None) -> torch.Tensor:
-    """f32 expanded-form squared distances, clamped at 0 (util.py:24-33)."""
-    if c_sq is None:
-        c_sq = (c * c).sum(1)
-    d = (x * x).sum(1, keepdim=True) + c_sq[None, :] - 2.0 * (x @ c.T)
-    return d.clamp_min_(0.0)
+def assign_nearest(x: torch.Tensor, cent: torch.Tensor, want_dist: bool = False):
+    """KA: nearest centroid per row (first on ties) and, optionally, its
+    squared distance (bf16-product score + |x|^2)."""
+    x = x.contiguous()
+    cent = cent.contiguous()
+    lab = torch.empty(x.shape[0], dtype=torch.int32, device=x.device)
+    dist = torch.empty(x.shape[0], dtype=torch.float32, device=x.device) if want_dist else None
+    _native.check(_native.load().givf_assign_nearest(
+        _vp(x), x.shape[0], _vp(cent), cent.shape[0], cent.shape[1], _vp(lab), _vp(dist),
+        _stream()))
+    return lab, dist
 
 
-def assign_top1(x: torch.Tensor, c: torch.Tensor, budget_elems=1 << 30):
-    """Nearest centroid (first minimum) and its distance, chunked."""
-    c_sq = (c * c).sum(1)
-    rows = max(1, budget_elems // max(c.shape[0], 1))
-    labels = torch.empty(x.shape[0], dtype=torch.int64, device=x.device)
-    dists = torch.empty(x.shape[0], dtype=torch.float32, device=x.device)
-    with _NoTF32():
-        for s in range(0, x.shape[0], rows):
-            d = sq_dists(x[s:s + rows], c, c_sq)
-            v, i = d.min(dim=1)
-            labels[s:s + rows], dists[s:s + rows] = i, v
-    return labels, dists
+def knn_exact(q: torch.Tensor, base: torch.Tensor, k: int):
+    """Exact top-k rows of `base` per query: ids (int32) and float64
+    squared distances, the set by (d64, id), rows in (f32(d64), id) order."""
+    q = q.contiguous()
+    base = base.contiguous()
+    ids = torch.empty(q.shape[0], k, dtype=torch.int32, device=q.device)
+    dd = torch.empty(q.shape[0], k, dtype=torch.float64, device=q.device)
+    _native.check(_native.load().givf_knn_exact(
+        _vp(q), q.shape[0], _vp(base), base.shape[0], base.shape[1], k, _vp(ids), _vp(dd),
+        _stream()))
+    return ids, dd
+
+
+def lexsort_rows(d: torch.Tensor, i: torch.Tensor):
+    """Per row, (d, i) ascending: stable sort by id, then stable by distance."""
+    o = torch.argsort(i, dim=1, stable=True)
+    d, i = d.gather(1, o), i.gather(1, o)
+    o = torch.argsort(d, dim=1, stable=True)
+    return d.gather(1, o), i.gather(1, o)
+
+
+class Model:
+    """Trained coarse/grouping/PQ state (everything but the rows)."""
+
+    def __init__(self, cent, nbr, alphas, cw, lo, hi, grouping, l):
+        self.cent = cent.contiguous()
+        self.k, self.d = cent.shape
+        self.nbr = nbr.int().contiguous() if grouping else None
+        self.alphas = alphas.float().contiguous()
+        self.cw = cw.contiguous()
+        self.m = cw.shape[0]
+        self.lo, self.hi = lo, hi
+        self.step = (hi - lo) / 256.0
+        self.grouping = grouping
+        self.l = l if grouping else 1
+        self.csq = (cent.double() ** 2).sum(1).contiguous()
+        self.cwsq = (cw * cw).sum(-1).contiguous()  # (M, 256) f32 (pq row norms)
+
+
+def encode_rows(x: torch.Tensor, region: torch.Tensor, md: Model, want_consts=False,
+                want_bytes=True):
+    """KE over rows grouped by region: (pick int16, codes (n, M) u8,
+    const bytes u8 or None, consts f64 or None), indexed like x."""
+    n = x.shape[0]
+    dev = x.device
+    reg_s, order = torch.sort(region, stable=True)
+    vals, counts = torch.unique_consecutive(reg_s, return_counts=True)
+    seg = torch.zeros(vals.shape[0] + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(counts, 0, out=seg[1:])
+    order = order.int().contiguous()
+    vals = vals.int().contiguous()
+    pick = torch.empty(n, dtype=torch.int16, device=dev)
+    codes = torch.empty(n, md.m, dtype=torch.uint8, device=dev)
+    cb = torch.empty(n, dtype=torch.uint8, device=dev) if want_bytes else None
+    consts = torch.empty(n, dtype=torch.float64, device=dev) if want_consts else None
+    desc = _native.EncodeDesc(
+        x=_vp(x.contiguous()), order=_vp(order), seg=_vp(seg), seg_region=_vp(vals),
+        nseg=vals.shape[0], dim=md.d, l=md.l, m=md.m, grouping=1 if md.grouping else 0,
+        centroids=_vp(md.cent), neighbor_ids=_vp(md.nbr), alphas=_vp(md.alphas), c_sq=_vp(md.csq),
+        codewords=_vp(md.cw), cw_sq=_vp(md.cwsq), const_lo=md.lo, const_step=md.step,
+        pick=_vp(pick), codes=_vp(codes), const_bytes=_vp(cb), consts=_vp(consts))
+    _native.check(_native.load().givf_encode_rows(ctypes.byref(desc), _stream()))
+    return pick, codes, cb, consts
+
+
+# ---------------------------------------------------------------- training
 
 
 def kmeans(x: torch.Tensor, k: int, iters: int, seed: int) -> torch.Tensor:
     """Lloyd iterations (kmeans.py:132-142) from a random-sample seeding;
-    empty clusters take the farthest point of the largest cluster
-    (kmeans.py:115-126)."""
+    empty clusters are re-seeded at random rows."""
     n = x.shape[0]
     g = _gen(seed, x.device)
     cent = x[torch.randperm(n, generator=g, device=x.device)[:k]].clone()
     for _ in range(iters):
-        labels, dists = assign_top1(x, cent)
+        lab, _ = assign_nearest(x, cent)
+        lab = lab.long()
         sums = torch.zeros(k, x.shape[1], dtype=torch.float64, device=x.device)
-        sums.index_add_(0, labels, x.double())
-        counts = torch.bincount(labels, minlength=k)
+        sums.index_add_(0, lab, x.double())
+        counts = torch.bincount(lab, minlength=k)
         cent = (sums / counts.clamp_min(1)[:, None]).float()
-        if FAST_BUILD:  # re-seed empty clusters at random points, vectorised
-            empty = torch.nonzero(counts == 0).flatten()
-            if empty.numel():
-                cent[empty] = x[torch.randint(0, n, (empty.numel(),), generator=g,
-                                              device=x.device)]
-            continue
-        empty = torch.nonzero(counts == 0).flatten().tolist()
-        for e in empty:
-            donor = int(torch.argmax(counts))
-            members = torch.nonzero(labels == donor).flatten()
-            far = members[torch.argmax(dists[members])]
-            cent[e] = x[far]
-            labels[far] = e
-            dists[far] = 0.0
-            counts[donor] -= 1
-            counts[e] = 1
-    return cent
+        empty = torch.nonzero(counts == 0).flatten()
+        if empty.numel():
+            cent[empty] = x[torch.randint(0, n, (empty.numel(),), generator=g, device=x.device)]
+    return cent.contiguous()
 
 
 def neighbor_centroids(c: torch.Tensor, l: int) -> torch.Tensor:
-    """l nearest other centroids per centroid, (distance, id) order
-    (grouping.py:25-41), via f32 expanded distances."""
+    """l nearest other centroids per centroid (grouping.py:25-41): the exact
+    top-(l+1) of every centroid, itself removed."""
     k = c.shape[0]
-    out = torch.empty(k, l, dtype=torch.int64, device=c.device)
-    c_sq = (c * c).sum(1)
-    rows = max(1, (1 << 28) // k)
-    ar = torch.arange(k, device=c.device)
-    with _NoTF32():
-        for s in range(0, k, rows):
-            d = sq_dists(c[s:s + rows], c, c_sq)
-            d[torch.arange(d.shape[0], device=c.device), ar[s:s + rows]] = float("inf")
-            v, i = torch.topk(d, l + 1, dim=1, largest=False, sorted=False)
-            # (distance, id) order: stable sort by id, then stable by distance
-            o = torch.argsort(i, dim=1, stable=True)
-            v, i = v.gather(1, o), i.gather(1, o)
-            o = torch.argsort(v, dim=1, stable=True)
-            i = i.gather(1, o)
-            out[s:s + rows] = i[:, :l]
-    return out
+    ids, _ = knn_exact(c, c, l + 1)
+    ar = torch.arange(k, device=c.device, dtype=torch.int32)[:, None]
+    is_self = ids == ar
+    # position of the row's own id (l + 1 when absent: drop the last)
+    pos = torch.where(is_self.any(1), is_self.int().argmax(1), torch.full_like(ar[:, 0], l))
+    j = torch.arange(l, device=c.device)[None, :]
+    j = j + (j >= pos[:, None]).long()
+    return ids.gather(1, j)
 
 
 def learn_alphas(x, labels, c, nbr, k) -> torch.Tensor:
@@ -212,6 +257,8 @@ def learn_alphas(x, labels, c, nbr, k) -> torch.Tensor:
     num = torch.zeros(k, dtype=torch.float64, device=x.device)
     den = torch.zeros(k, dtype=torch.float64, device=x.device)
     c64 = c.double()
+    nbr = nbr.long()
+    labels = labels.long()
     rows = max(1, (1 << 27) // (nbr.shape[1] * c.shape[1]))
     for s in range(0, x.shape[0], rows):
         lab = labels[s:s + rows]
@@ -234,33 +281,15 @@ def learn_alphas(x, labels, c, nbr, k) -> torch.Tensor:
     return alpha.float()
 
 
-def anchors_of(c, nbr, alphas, region, pick=None):
-    """Anchor t = c + a (s - c) in float32 (grouping.py:77-82, index.py:141-157).
-    pick=None returns all L anchors (n, L, d)."""
+def anchors_of(c, nbr, alphas, region, pick):
+    """Anchor t = c + a (s - c) in float32 (grouping.py:77-82, index.py:141-157)."""
+    region = region.long()
     cr = c[region]
+    if nbr is None:
+        return cr
     a = alphas[region]
-    if pick is None:
-        s = c[nbr[region]]
-        return cr[:, None, :] + a[:, None, None] * (s - cr[:, None, :])
-    s = c[nbr[region, pick]]
+    s = c[nbr.long()[region, pick.long()]]
     return cr + a[:, None] * (s - cr)
-
-
-def pick_groups(x, region, c, nbr, alphas):
-    """Nearest anchor per point, lowest group on ties, 0 when alpha == 0
-    (index.py:124-138)."""
-    out = torch.zeros(x.shape[0], dtype=torch.int64, device=x.device)
-    rows = max(1, (1 << 27) // (nbr.shape[1] * c.shape[1]))
-    with _NoTF32():
-        for s in range(0, x.shape[0], rows):
-            xs, rs = x[s:s + rows], region[s:s + rows]
-            t = anchors_of(c, nbr, alphas, rs)                     # (n, L, d)
-            d = (xs * xs).sum(1, keepdim=True) + (t * t).sum(-1) - 2.0 * torch.einsum("nd,nld->nl", xs, t)
-            d.clamp_min_(0.0)
-            p = torch.argmin(d, dim=1)
-            p[alphas[rs] == 0.0] = 0
-            out[s:s + rows] = p
-    return out
 
 
 def pq_train(disp: torch.Tensor, m: int, iters: int, seed: int) -> torch.Tensor:
@@ -273,86 +302,22 @@ def pq_train(disp: torch.Tensor, m: int, iters: int, seed: int) -> torch.Tensor:
     return cw
 
 
-def pq_encode(disp: torch.Tensor, cw: torch.Tensor) -> torch.Tensor:
-    """Nearest codeword per subspace, lowest index on ties (pq.py:56-66)."""
-    m, _, sub = cw.shape
-    out = torch.empty(disp.shape[0], m, dtype=torch.uint8, device=disp.device)
-    with _NoTF32():
-        for j in range(m):
-            x = disp[:, j * sub:(j + 1) * sub]
-            for s in range(0, x.shape[0], 1 << 21):
-                out[s:s + (1 << 21), j] = sq_dists(x[s:s + (1 << 21)], cw[j]).argmin(1).to(torch.uint8)
-    return out
-
-
-def pq_decode(codes: torch.Tensor, cw: torch.Tensor) -> torch.Tensor:
-    m = cw.shape[0]
-    return torch.cat([cw[j][codes[:, j].long()] for j in range(m)], dim=1)
-
-
-def const_terms(c, nbr, alphas, region, pick, codes, cw, grouping=True) -> torch.Tensor:
-    """|t + r|^2 - (1-a)|c|^2 - a|s|^2 in float64 (index.py:141-170)."""
-    c64 = c.double()
-    if grouping:
-        t = anchors_of(c, nbr, alphas, region, pick)
-        s64 = c64[nbr[region, pick]]
-        s_sq = (s64 * s64).sum(1)
-        a = alphas[region].double()
-    else:
-        t = c[region]
-        s_sq = torch.zeros(region.shape[0], dtype=torch.float64, device=c.device)
-        a = torch.zeros(region.shape[0], dtype=torch.float64, device=c.device)
-    tpr = (t + pq_decode(codes, cw)).double()
-    cr = c64[region]
-    return (tpr * tpr).sum(1) - (1.0 - a) * (cr * cr).sum(1) - a * s_sq
-
-
 def norm_terms(c, nbr, alphas) -> torch.Tensor:
     """Per-group constants that turn scores into anchor distances
     (index.py:173-192), float64 then float32."""
     c64 = c.double()
     c_sq = (c64 * c64).sum(1)
-    a = alphas.double()[:, None, None]
-    cc = c64[:, None, :]
-    ss = c64[nbr]
-    t = cc + a * (ss - cc)
-    t_sq = (t * t).sum(-1)
-    return (t_sq - (1.0 - a[:, :, 0]) * c_sq[:, None] - a[:, :, 0] * c_sq[nbr]).float()
-
-
-# ---------------------------------------------------------------- ground truth
-
-
-class TopT:
-    """Running exact top-t (float64 distance, id) per query over base chunks."""
-
-    def __init__(self, queries: torch.Tensor, t: int = 10, pre: int = 16):
-        self.q = queries
-        self.q64 = queries.double()
-        self.t, self.pre = t, max(pre, t)
-        nq = queries.shape[0]
-        self.d = torch.full((nq, self.t), float("inf"), dtype=torch.float64, device=queries.device)
-        self.i = torch.full((nq, self.t), -1, dtype=torch.int64, device=queries.device)
-
-    def update(self, x: torch.Tensor, first_id: int):
-        with _NoTF32():
-            for s in range(0, x.shape[0], 1 << 16):
-                xs = x[s:s + (1 << 16)]
-                d = sq_dists(self.q, xs)
-                v, j = torch.topk(d, min(self.pre, xs.shape[0]), dim=1, largest=False)
-                cand = xs[j]                                     # (nq, pre, d)
-                d64 = ((cand.double() - self.q64[:, None, :]) ** 2).sum(-1)
-                ids = j + (first_id + s)
-                alld = torch.cat([self.d, d64], 1)
-                alli = torch.cat([self.i, ids], 1)
-                # (d64, id) lexicographic: sort by id then stable by distance
-                o = torch.argsort(alli, dim=1, stable=True)
-                alld, alli = alld.gather(1, o), alli.gather(1, o)
-                o = torch.argsort(alld, dim=1, stable=True)[:, : self.t]
-                self.d, self.i = alld.gather(1, o), alli.gather(1, o)
-
-    def result(self) -> np.ndarray:
-        return self.i.to(torch.int32).cpu().numpy()
+    out = torch.empty(nbr.shape, dtype=torch.float32, device=c.device)
+    nbr = nbr.long()
+    for s in range(0, c.shape[0], 1 << 14):
+        e = min(c.shape[0], s + (1 << 14))
+        a = alphas[s:e].double()[:, None, None]
+        cc = c64[s:e, None, :]
+        ss = c64[nbr[s:e]]
+        t = cc + a * (ss - cc)
+        t_sq = (t * t).sum(-1)
+        out[s:e] = (t_sq - (1.0 - a[:, :, 0]) * c_sq[s:e, None] - a[:, :, 0] * c_sq[nbr[s:e]]).float()
+    return out
 
 
 # ---------------------------------------------------------------- build
@@ -369,97 +334,150 @@ class BuildSpec:
     kmeans_iters: int = 10
     pq_iters: int = 15
     seed: int = 0
-    fast: bool = False          # TF32 assignment matmuls (1B-scale builds)
+    fast: bool = False          # kept for cache keys of older workloads (unused)
+    alpha_rows: int = 4_000_000   # learn rows the alpha fit reads
+    pq_rows: int = 1_000_000      # learn rows the PQ k-means reads
 
     def learn_rows(self) -> int:
         return self.n_learn or max(100_000, 32 * self.k)
 
 
-def build_synthetic(data: SynthSpec, spec: BuildSpec, n_queries: int, gt_t: int = 10,
-                    device="cuda", log=print):
-    """Generate, train, encode and lay out a grouped index on the GPU.
-
-    Returns (IndexArrays on host, queries (nq, d) f32 numpy, gt (nq, gt_t) i32).
-    """
-    import time
-
-    global FAST_BUILD
-    FAST_BUILD = spec.fast
+def train_model(data: SynthSpec, spec: BuildSpec, means, device, log=print) -> Model:
+    """Coarse k-means, neighbour lists, alphas, PQ codebooks and the constant
+    quantizer on the held-out learn stream (index.py:214-312)."""
     t0 = time.perf_counter()
-    means = cluster_means(data, device)
     learn = synth_rows(data, "learn", 0, spec.learn_rows(), means, device)
-    queries = synth_rows(data, "query", 0, n_queries, means, device)
     k, l = spec.k, spec.l
     cent = kmeans(learn, k, spec.kmeans_iters, derive_seed(spec.seed, "kmeans"))
     log(f"[build] kmeans K={k} on {learn.shape[0]} learn rows: {time.perf_counter()-t0:.1f}s")
-
-    lr, _ = assign_top1(learn, cent)
+    lr, _ = assign_nearest(learn, cent)
     if spec.grouping:
         nbr = neighbor_centroids(cent, l)
-        alphas = learn_alphas(learn, lr, cent, nbr, k)
-        lp = pick_groups(learn, lr, cent, nbr, alphas)
-        t_learn = anchors_of(cent, nbr, alphas, lr, lp)
+        na = min(learn.shape[0], spec.alpha_rows)
+        alphas = learn_alphas(learn[:na], lr[:na], cent, nbr, k)
     else:
-        nbr = torch.zeros(k, 1, dtype=torch.int64, device=device)
+        nbr = None
         alphas = torch.zeros(k, dtype=torch.float32, device=device)
-        lp = torch.zeros_like(lr)
-        t_learn = cent[lr]
-    cw = pq_train(learn - t_learn, spec.m, spec.pq_iters, derive_seed(spec.seed, "pq"))
-    lcodes = pq_encode(learn - t_learn, cw)
-    lconst = const_terms(cent, nbr, alphas, lr, lp, lcodes, cw, spec.grouping)
-    # grouping.py:132-145: percentile bounds rounded through float32
+    log(f"[build] neighbours + alphas: {time.perf_counter()-t0:.1f}s")
+    # group picks of the learn rows (KE with a placeholder codebook), then
+    # the PQ codebooks on their displacements (index.py:213-246)
+    d = cent.shape[1]
+    tmp = Model(cent, nbr if nbr is not None else torch.zeros(k, 1, dtype=torch.int32, device=device),
+                alphas, torch.zeros(spec.m, 256, d // spec.m, device=device), 0.0, 0.0,
+                spec.grouping, l)
+    lp, _, _, _ = encode_rows(learn, lr, tmp, want_bytes=False)
+    np_ = min(learn.shape[0], spec.pq_rows)
+    disp = learn[:np_] - anchors_of(cent, nbr, alphas, lr[:np_], lp[:np_])
+    cw = pq_train(disp, spec.m, spec.pq_iters, derive_seed(spec.seed, "pq"))
+    del disp
+    # constant quantizer from the learn rows' own constants (grouping.py:132-145):
+    # percentile bounds rounded through float32
+    md = Model(cent, tmp.nbr, alphas, cw, 0.0, 0.0, spec.grouping, l)
+    _, _, _, lconst = encode_rows(learn, lr, md, want_consts=True, want_bytes=False)
     qlo, qhi = (float(np.float32(v)) for v in np.percentile(lconst.cpu().numpy(), [0.1, 99.9]))
     lo_, hi_ = min(qlo, qhi), max(qlo, qhi)
-    step = (hi_ - lo_) / 256.0
     log(f"[build] grouping + PQ(M={spec.m}) trained: {time.perf_counter()-t0:.1f}s")
-    del learn, t_learn, lcodes, lconst
+    del learn, lconst
+    return Model(cent, tmp.nbr, alphas, cw, lo_, hi_, spec.grouping, l)
+
+
+class GroundTruth:
+    """Running exact top-t (float64 distance, id) per query over base row
+    blocks (datasets.py:34-61), through the certified probe."""
+
+    BLOCK = 1 << 20
+
+    def __init__(self, queries: torch.Tensor, t: int = 10):
+        self.q = queries.contiguous()
+        self.t = t
+        nq = queries.shape[0]
+        self.d = torch.full((nq, t), float("inf"), dtype=torch.float64, device=queries.device)
+        self.i = torch.full((nq, t), -1, dtype=torch.int64, device=queries.device)
+
+    def update(self, x: torch.Tensor, first_id: int):
+        for s in range(0, x.shape[0], self.BLOCK):
+            xs = x[s:s + self.BLOCK]
+            kk = min(self.t, xs.shape[0])
+            ids, dd = knn_exact(self.q, xs, kk)
+            d = torch.cat([self.d, dd], 1)
+            i = torch.cat([self.i, ids.long() + (first_id + s)], 1)
+            d, i = lexsort_rows(d, i)
+            self.d, self.i = d[:, : self.t].contiguous(), i[:, : self.t].contiguous()
+
+    def result(self) -> np.ndarray:
+        return self.i.to(torch.int32).cpu().numpy()
+
+
+def build_synthetic(data: SynthSpec, spec: BuildSpec, n_queries: int, gt_t: int = 10,
+                    device="cuda", log=print, rows_on_device: bool = False):
+    """Generate, train, encode and lay out a grouped index on the GPU.
+
+    Returns (IndexArrays, queries (nq, d) f32 numpy, gt (nq, gt_t) i32).
+    With rows_on_device the row arrays (point_ids, codes, const_bytes) stay
+    torch CUDA tensors (1B-row indexes never visit the host); otherwise every
+    array is numpy.
+    """
+    t0 = time.perf_counter()
+    means = cluster_means(data, device)
+    queries = synth_rows(data, "query", 0, n_queries, means, device)
+    md = train_model(data, spec, means, device, log)
+    k, l = spec.k, spec.l
+    groups = l if spec.grouping else 1
 
     n = spec.n
-    region = torch.empty(n, dtype=torch.int32, device=device)
-    pick = torch.empty(n, dtype=torch.int16, device=device)
+    key = torch.empty(n, dtype=torch.int32, device=device)
     codes = torch.empty(n, spec.m, dtype=torch.uint8, device=device)
     cbytes = torch.empty(n, dtype=torch.uint8, device=device)
-    gt = TopT(queries, gt_t)
-    for s in range(0, n, CHUNK_ROWS):
-        e = min(n, s + CHUNK_ROWS)
-        x = synth_rows(data, "base", s, e - s, means, device)
-        r, _ = assign_top1(x, cent)
-        p = pick_groups(x, r, cent, nbr, alphas) if spec.grouping else torch.zeros_like(r)
-        t = anchors_of(cent, nbr, alphas, r, p) if spec.grouping else cent[r]
-        cd = pq_encode(x - t, cw)
-        ct = const_terms(cent, nbr, alphas, r, p, cd, cw, spec.grouping)
-        if step > 0:
-            b = torch.floor((ct - lo_) / step).clamp(0, 255).to(torch.uint8)
-        else:
-            b = torch.zeros_like(ct, dtype=torch.uint8)
-        region[s:e], pick[s:e], codes[s:e], cbytes[s:e] = r.int(), p.short(), cd, b
+    gt = GroundTruth(queries, gt_t)
+    x = None
+    for s in range(0, n, ENCODE_ROWS):
+        e = min(n, s + ENCODE_ROWS)
+        x = synth_rows(data, "base", s, e - s, means, device,
+                       out=x[: e - s] if x is not None and x.shape[0] >= e - s else None)
+        r, _ = assign_nearest(x, md.cent)
+        p, cd, cb, _ = encode_rows(x, r, md)
+        key[s:e] = r * groups + p.int()
+        codes[s:e] = cd
+        cbytes[s:e] = cb
         gt.update(x, s)
-        del x, t
-        if n >= 100 * CHUNK_ROWS and (s // CHUNK_ROWS) % 100 == 99:
+        if n >= 8 * ENCODE_ROWS and (s // ENCODE_ROWS) % 8 == 7:
+            torch.cuda.synchronize()
             log(f"[build]   {e} rows encoded: {time.perf_counter()-t0:.1f}s")
+    del x
+    torch.cuda.synchronize()
     log(f"[build] {n} base rows assigned/encoded + ground truth: {time.perf_counter()-t0:.1f}s")
 
-    groups = l if spec.grouping else 1
-    key = region.long() * groups + pick.long()
-    order = torch.sort(key, stable=True).indices                # ties keep id order
-    gsize = torch.bincount(key, minlength=k * groups).reshape(k, groups).int()
+    # (region, group, id) layout (index.py:326-337): a stable sort by key
+    order = torch.sort(key, stable=True).indices
+    gsize = torch.bincount(key.long(), minlength=k * groups).reshape(k, groups).int()
+    del key
     offs = torch.zeros(k + 1, dtype=torch.int64, device=device)
     offs[1:] = torch.cumsum(gsize.sum(1).long(), 0)
+    pids = order.int()
+    codes_s = codes[order]
+    del codes
+    cb_s = cbytes[order]
+    del cbytes, order
+    torch.cuda.synchronize()
+    log(f"[build] layout done: {time.perf_counter()-t0:.1f}s")
+
+    def rowarr(t):
+        return t if rows_on_device else t.cpu().numpy()
+
     arr = IndexArrays(
-        centroids=cent.cpu().numpy(),
-        alphas=alphas.cpu().numpy(),
-        neighbor_ids=nbr.int().cpu().numpy() if spec.grouping else None,
-        norm_terms=norm_terms(cent, nbr, alphas).cpu().numpy() if spec.grouping else None,
+        centroids=md.cent.cpu().numpy(),
+        alphas=md.alphas.cpu().numpy(),
+        neighbor_ids=md.nbr.cpu().numpy() if spec.grouping else None,
+        norm_terms=norm_terms(md.cent, md.nbr, md.alphas).cpu().numpy() if spec.grouping else None,
         group_sizes=gsize.cpu().numpy(),
         region_offsets=offs.cpu().numpy(),
-        point_ids=order.int().cpu().numpy(),
-        codes=codes[order].cpu().numpy(),
-        const_bytes=cbytes[order].cpu().numpy(),
-        codewords=cw.cpu().numpy(),
+        point_ids=rowarr(pids),
+        codes=rowarr(codes_s),
+        const_bytes=rowarr(cb_s),
+        codewords=md.cw.cpu().numpy(),
         rotation=None,
-        const_lo=lo_,
-        const_hi=hi_,
+        const_lo=md.lo,
+        const_hi=md.hi,
         grouping=spec.grouping,
     )
-    log(f"[build] layout done: {time.perf_counter()-t0:.1f}s")
     return arr, queries.cpu().numpy(), gt.result()

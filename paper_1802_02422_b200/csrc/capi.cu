@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -16,6 +17,42 @@
 #include "kernels.h"
 
 using namespace givf;
+
+namespace givf {
+
+int num_sms_cur() {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    n = 148;
+  }
+  cache[dev] = n;
+  return n;
+}
+
+cudaError_t ensure_max_smem(const void* fn, size_t bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& have = done[{fn, dev}];
+  if (have >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
+
+}  // namespace givf
 
 namespace {
 
@@ -77,6 +114,11 @@ int fail(int code, const std::string& msg) {
     }                                                                              \
   } while (0)
 
+#define ARENA_CHECK(ar)                                                          \
+  do {                                                                           \
+    if ((ar).over) return fail(GIVF_ENOMEM, "workspace estimate exceeded (internal)"); \
+  } while (0)
+
 #define KCHECK()                                                                   \
   do {                                                                             \
     cudaError_t _e = cudaGetLastError();                                           \
@@ -127,10 +169,15 @@ struct Arena {
     if (e == cudaSuccess) cap = want;
     return e;
   }
-  void reset() { off = 0; }
+  bool over = false;  // a take() ran past cap: nothing taken may be used
+  void reset() { off = 0; over = false; }
   template <typename T>
   T* take(size_t count) {
     size_t bytes = ((count * sizeof(T)) + 255) & ~(size_t)255;
+    if (off + bytes > cap) {
+      over = true;
+      return static_cast<T*>(base);
+    }
     T* p = reinterpret_cast<T*>(static_cast<char*>(base) + off);
     off += bytes;
     return p;
@@ -154,10 +201,6 @@ struct givf_index {
   int64_t dev_bytes = 0;
   Arena arena;
   std::mutex mu;
-  // internal pipeline streams (chunks of one call run on them round-robin)
-  std::vector<cudaStream_t> pstreams;
-  std::vector<cudaEvent_t> ev_done;
-  cudaEvent_t ev_start = nullptr;
 
   cudaStream_t side = nullptr;  // LUT builds overlap the probe / planner
   cudaEvent_t ev_q = nullptr, ev_lut = nullptr;
@@ -168,23 +211,7 @@ struct givf_index {
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_lut, cudaEventDisableTiming);
     return e;
   }
-  cudaError_t ensure_streams(int n) {
-    if (!ev_start) {
-      cudaError_t e = cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
-      if (e != cudaSuccess) return e;
-    }
-    while ((int)pstreams.size() < n) {
-      cudaStream_t s;
-      cudaEvent_t ev;
-      cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
-      if (e != cudaSuccess) return e;
-      e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-      if (e != cudaSuccess) return e;
-      pstreams.push_back(s);
-      ev_done.push_back(ev);
-    }
-    return cudaSuccess;
-  }
+
 };
 
 namespace {
@@ -257,27 +284,6 @@ size_t l2_budget() {
   return (size_t)(s ? atoll(s) : (1ll << 20)) << 20;
 }
 
-// 0: warp-independent scan (default), 1: block scan (GIVF_SCAN=block),
-// 2: cp.async-staged block scan (GIVF_SCAN=async)
-int scan_mode() {
-  const char* s = getenv("GIVF_SCAN");
-  if (s && strcmp(s, "async") == 0) return 2;
-  if (s && strcmp(s, "block") == 0) return 1;
-  return 0;
-}
-
-int nstreams_default() {
-  const char* s = getenv("GIVF_STREAMS");
-  // measured on C2 with the current kernels: one stream and the largest
-  // chunks win (every stage fills the GPU on its own)
-  return std::max(1, std::min(8, s ? atoi(s) : 1));
-}
-
-int64_t probe_sub_default() {
-  const char* s = getenv("GIVF_PROBE_SUB");
-  return s ? std::max<int64_t>(0, atoll(s)) : 0;
-}
-
 size_t workspace_budget() {
   const char* s = getenv("GIVF_WORKSPACE_MB");
   size_t mb = s ? (size_t)atoll(s) : 8192;
@@ -347,6 +353,7 @@ int run_probe(givf_index* ix, const Plan& pl, const float* dQ, int nq, int* regi
   uint64_t* sk2 = ar.take<uint64_t>((size_t)kFullSlots * pp2);
   uint32_t* sv2 = ar.take<uint32_t>((size_t)kFullSlots * pp2);
   double* sdv = ar.take<double>((size_t)kFullSlots * pp2);
+  ARENA_CHECK(ar);
   const int slots = std::min(kFullSlots, nq);
   if (pl.ps.exhaustive) {
     // nprobe == K: search.py:80-84 formula; larger P: exact f64 ranking of all.
@@ -378,8 +385,10 @@ int run_probe(givf_index* ix, const Plan& pl, const float* dQ, int nq, int* regi
   const int ntiles = probe_tiles(K);
   float* tmin = ar.take<float>((size_t)nq * ntiles);
   const bool tc = use_tensor_cores(v);
+  uint32_t* tup = ar.take<uint32_t>(nq);
+  void* abf = tc ? ar.take<uint16_t>((size_t)nq * tc_kpad(d)) : nullptr;
+  ARENA_CHECK(ar);
   if (tc) {
-    void* abf = ar.take<uint16_t>((size_t)nq * tc_kpad(d));
     staged(ST_GEMM, st, [&] {
       launch_query_scale(dQ, nq, d, v.cmax, q2f, qinv, qscale, st);
       launch_split_bf16(dQ, nq, d, 0, abf, st);
@@ -391,7 +400,6 @@ int run_probe(givf_index* ix, const Plan& pl, const float* dQ, int nq, int* regi
       launch_probe_gemm(dQ, v.centroids, v.c2f, nq, K, d, so, tmin, st);
     }, 2);
   }
-  uint32_t* tup = ar.take<uint32_t>(nq);
   staged(ST_SELECT, st, [&] {
     launch_probe_select(so.D16, K, q2f, qscale, nq, K, pl.ps.Tmin, pl.ps.cap, tmin, ntiles, tup,
                         cand, cand_n, theta, st);
@@ -487,12 +495,8 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
   if (om == OUT_FULL && rerank) per_q += (size_t)full_p2 * 8;
   if (!out_dev) per_q += (size_t)width * 8 + 512;
   per_q += aligned_bytes<float>((size_t)v.M * 256);  // prebuilt LUTs
-  // Probe sub-chunks (GIVF_PROBE_SUB queries): GEMM -> select -> recheck ->
-  // K3a run per sub-chunk so the fp32 score matrix D they share stays in L2
-  // instead of making three HBM round trips; 0 = one sub-chunk per chunk.
-  const int64_t sub_env = probe_sub_default();
-  const size_t fixed = probe_fixed_bytes(pl) + (1 << 16) + (sub_env ? probe_q * sub_env : 0);
-  if (!sub_env) per_q += probe_q;
+  per_q += probe_q;
+  const size_t fixed = probe_fixed_bytes(pl) + (1 << 16);
   const size_t budget = workspace_budget();
   int64_t chunk = budget > fixed ? (int64_t)((budget - fixed) / per_q) : 1;
   // Keep one chunk's probe scores + plan scratch resident in the 126 MB L2:
@@ -500,31 +504,19 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
   const size_t hot = (pl.ps.exhaustive ? 0 : (size_t)pl.K * 4) + (size_t)pl.total * 20 +
                      (size_t)pl.cap_w * 32;
   chunk = std::min<int64_t>(chunk, std::max<int64_t>(128, (int64_t)(l2_budget() / hot)));
-  // Chunks run round-robin on `ns` internal streams with disjoint arena
-  // slices, so one chunk's latency-bound kernels overlap another's and the
-  // kernel tails fill in; the caller's stream is fenced on both ends.
-  int ns = nstreams_default();
-  chunk = std::max<int64_t>(1, chunk / ns);
   if (const char* e = getenv("GIVF_CHUNK_QUERIES")) chunk = std::max<int64_t>(1, atoll(e));
   chunk = std::max<int64_t>(1, std::min<int64_t>(chunk, nq));
   chunk = std::min<int64_t>(chunk, 65535);
   // equal chunks (no small tail chunk that leaves the GPU half empty)
   chunk = (nq + (nq + chunk - 1) / chunk - 1) / ((nq + chunk - 1) / chunk);
-  const int64_t nchunks = (nq + chunk - 1) / chunk;
-  ns = (int)std::min<int64_t>(ns, nchunks);
   const size_t slice = ((fixed + per_q * (size_t)chunk + (1 << 20)) + 4095) & ~(size_t)4095;
-  CUDA_TRY(ix->arena.reserve(slice * ns));
-  CUDA_TRY(ix->ensure_streams(ns));
-  CUDA_TRY(cudaEventRecord(ix->ev_start, st));
-  for (int i = 0; i < ns; ++i) CUDA_TRY(cudaStreamWaitEvent(ix->pstreams[i], ix->ev_start, 0));
-  const cudaStream_t caller = st;
-
-  for (int64_t q0 = 0, ci = 0; q0 < nq; q0 += chunk, ++ci) {
+  CUDA_TRY(ix->arena.reserve(slice));
+  // Chunks run in order on the caller's stream, each reusing the arena
+  // (stream order makes the reuse safe without host synchronisation).
+  for (int64_t q0 = 0; q0 < nq; q0 += chunk) {
     const int bq = (int)std::min<int64_t>(chunk, nq - q0);
-    const int si = (int)(ci % ns);
-    st = ix->pstreams[si];
     Arena ar;
-    ar.base = static_cast<char*>(ix->arena.base) + slice * si;
+    ar.base = ix->arena.base;
     ar.cap = slice;
     ar.reset();
     const float* dQ;
@@ -532,6 +524,7 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
       dQ = queries + q0 * v.d;
     } else {
       float* tmp = ar.take<float>((size_t)bq * v.d);
+      ARENA_CHECK(ar);
       CUDA_TRY(cudaMemcpyAsync(tmp, queries + q0 * v.d, sizeof(float) * bq * v.d,
                                cudaMemcpyHostToDevice, st));
       dQ = tmp;
@@ -547,7 +540,7 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
       la.ix = v;
       la.mode = om == OUT_TOPK ? 0 : 1;
       la.k = (int)(om == OUT_TOPK ? width : 0);
-      if (om == OUT_TOPK && scan_mode() == 0 && scan_warp_ok(la)) {
+      if (om == OUT_TOPK && scan_warp_ok(la)) {
         luts = ar.take<float>((size_t)bq * v.M * 256);
         CUDA_TRY(ix->ensure_side());
       }
@@ -590,42 +583,34 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
     pa.ldD = v.K;
     pa.cmax = v.cmax;
     pa.only = ar.take<int>(bq);
+    ARENA_CHECK(ar);
     // the approximate planner's keys alias the exact scratch, which the exact
     // kernels only write after the approximate planner has finished
     pa.akey = reinterpret_cast<uint32_t*>(pa.sbase);
 
-    // probe + K3a per sub-chunk; the probe workspace (D included) is reused
+    // probe + K3a; the probe workspace (D included) is dead afterwards
     const size_t mark = ar.off;
-    const int64_t sub = sub_env ? std::min<int64_t>(sub_env, bq) : bq;
     bool approx = true;
     rc = launch_luts();
     if (rc) return rc;
-    for (int64_t s0 = 0; s0 < bq; s0 += sub) {
-      const int ns_q = (int)std::min<int64_t>(sub, bq - s0);
-      ar.off = mark;
+    {
       const uint16_t* Dmat = nullptr;
       const float* dscale = nullptr;
       float eps_scale = 0.f;
-      rc = run_probe(ix, pl, dQ + s0 * v.d, ns_q, regions + s0 * pl.P, qc2 + s0 * pl.P, ar, st,
-                     &Dmat, &dscale, &eps_scale);
+      rc = run_probe(ix, pl, dQ, bq, regions, qc2, ar, st, &Dmat, &dscale, &eps_scale);
       if (rc) return rc;
       pa.eps_scale = eps_scale;
       if (!Dmat) {  // exhaustive probe (nprobe == K or too wide): exact planner only
         approx = false;
-        continue;
+      } else {
+        PlanArgs sa = pa;
+        sa.D = Dmat;
+        sa.dscale = dscale;
+        int nk = 0;
+        staged(ST_PLAN, st, [&] { nk = launch_plan_scores(sa, st); }, 0);
+        g_launches += nk;
+        KCHECK();
       }
-      PlanArgs sa = pa;
-      sa.Q = dQ + s0 * v.d;
-      sa.regions = regions + s0 * pl.P;
-      sa.qc2 = qc2 + s0 * pl.P;
-      sa.nq = ns_q;
-      sa.akey = pa.akey + s0 * pl.total;
-      sa.D = Dmat;
-      sa.dscale = dscale;
-      int nk = 0;
-      staged(ST_PLAN, st, [&] { nk = launch_plan_scores(sa, st); }, 0);
-      g_launches += nk;
-      KCHECK();
     }
     ar.off = mark;  // the probe workspace is dead once K3a has run (stream order)
     pa.approx = approx ? 1 : 0;
@@ -664,11 +649,9 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
         CUDA_TRY(cudaStreamWaitEvent(st, ix->ev_lut, 0));
         sa.luts = luts;
       }
+      ARENA_CHECK(ar);
       staged(ST_SCAN, st, [&] {
-        const int mode = scan_mode();
-        if (mode == 2 && launch_scan_async(sa, st)) return;
-        if (mode == 0 && launch_scan_warp(sa, st)) return;
-        launch_scan(sa, st);
+        if (!launch_scan_warp(sa, st)) launch_scan(sa, st);  // k_scan: full mode, other M / k
       });
       KCHECK();
       if (om == OUT_FULL) {
@@ -678,6 +661,7 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
         KCHECK();
       }
     } else {
+      ARENA_CHECK(ar);
       staged(ST_FINISH, st, [&] {
         launch_scan_order(v, pa.work, pl.cap_w, pa.nwork, pa.order, bq, oid, od, width, st);
       });
@@ -693,14 +677,8 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
       CUDA_TRY(cudaMemcpyAsync(stats + q0, dstats, sizeof(int64_t) * 4 * bq,
                                cudaMemcpyDeviceToHost, st));
     }
-    // chunk ci + ns reuses this arena slice on the same stream: ordered after
-    // this chunk's copies and kernels, so no host synchronisation
   }
-  for (int i = 0; i < ns; ++i) {
-    CUDA_TRY(cudaEventRecord(ix->ev_done[i], ix->pstreams[i]));
-    CUDA_TRY(cudaStreamWaitEvent(caller, ix->ev_done[i], 0));
-  }
-  if (host_out || !q_dev) CUDA_TRY(cudaStreamSynchronize(caller));
+  if (host_out || !q_dev) CUDA_TRY(cudaStreamSynchronize(st));
   return GIVF_OK;
 }
 
@@ -884,15 +862,9 @@ int givf_index_destroy(givf_index_t ix) {
   for (void* p : ix->allocs) cudaFree(p);
   if (ix->arena.base) cudaFree(ix->arena.base);
   if (ix->stream) cudaStreamDestroy(ix->stream);
-  for (auto s : ix->pstreams) {
-    cudaStreamSynchronize(s);
-    cudaStreamDestroy(s);
-  }
-  for (auto e : ix->ev_done) cudaEventDestroy(e);
   if (ix->side) cudaStreamDestroy(ix->side);
   if (ix->ev_q) cudaEventDestroy(ix->ev_q);
   if (ix->ev_lut) cudaEventDestroy(ix->ev_lut);
-  if (ix->ev_start) cudaEventDestroy(ix->ev_start);
   delete ix;
   return GIVF_OK;
 }
@@ -1027,6 +999,188 @@ int givf_merge_topk(const int32_t* ids, const float* dists, int32_t shards, int6
     }
   }
   KCHECK();
+  return GIVF_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ builder
+#include "givf_build.h"
+
+namespace {
+
+// Per-device scratch of the builder entry points (grow-only arena, device
+// counters for the certified probe).
+givf_index* builder_ctx(int device) {
+  static std::mutex mu;
+  static std::map<int, givf_index*> ctx;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = ctx.find(device);
+  if (it != ctx.end()) return it->second;
+  givf_index* ix = new givf_index();
+  ix->device = device;
+  unsigned long long* cnt = nullptr;
+  if (cudaMalloc(&cnt, 256) != cudaSuccess || cudaMemset(cnt, 0, 256) != cudaSuccess) {
+    cudaGetLastError();
+    delete ix;
+    return nullptr;
+  }
+  ix->allocs.push_back(cnt);
+  ix->v.counters = cnt;
+  ctx[device] = ix;
+  return ix;
+}
+
+int device_of(const void* p, int* dev) {
+  cudaPointerAttributes at;
+  if (!p || cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(GIVF_EINVAL, "expected a device pointer");
+  }
+  if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged)
+    return fail(GIVF_EINVAL, "expected a device pointer");
+  *dev = at.device;
+  return GIVF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int givf_assign_nearest(const float* x, int64_t rows, const float* centroids, int32_t k,
+                        int32_t dim, int32_t* labels, float* dists, void* stream) {
+  if (rows < 0 || k < 1 || dim < 1) return fail(GIVF_EINVAL, "bad shape");
+  if (!assign_supported(dim)) return fail(GIVF_EINVAL, "assign needs dim <= 128");
+  if (rows == 0) return GIVF_OK;
+  int dev = 0, rc;
+  if ((rc = device_of(x, &dev)) || (rc = device_of(centroids, &dev)) || (rc = device_of(labels, &dev)))
+    return rc;
+  CUDA_TRY(cudaSetDevice(dev));
+  givf_index* ix = builder_ctx(dev);
+  if (!ix) return fail(GIVF_ENOMEM, "builder context");
+  std::lock_guard<std::mutex> lock(ix->mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int Kp = assign_kpad(dim);
+  const int64_t chunk = std::min<int64_t>(rows, (int64_t)1 << 24);
+  const int nsplit = assign_nsplit(chunk, k);
+  const size_t need = aligned_bytes<uint16_t>((size_t)k * Kp) + aligned_bytes<float>(k) +
+                      aligned_bytes<uint16_t>((size_t)chunk * Kp) +
+                      (size_t)nsplit * (aligned_bytes<float>(chunk) + aligned_bytes<int32_t>(chunk)) +
+                      aligned_bytes<float>(chunk) + (1 << 16);
+  CUDA_TRY(ix->arena.reserve(need));
+  Arena& ar = ix->arena;
+  ar.reset();
+  void* cbf = ar.take<uint16_t>((size_t)k * Kp);
+  float* c2 = ar.take<float>(k);
+  void* xbf = ar.take<uint16_t>((size_t)chunk * Kp);
+  float* pv = ar.take<float>((size_t)nsplit * chunk);
+  int32_t* pi = ar.take<int32_t>((size_t)nsplit * chunk);
+  float* x2 = dists ? ar.take<float>(chunk) : nullptr;
+  ARENA_CHECK(ar);
+  launch_rows_bf16(centroids, k, dim, cbf, st);
+  launch_row_norms(centroids, k, dim, c2, nullptr, nullptr, st);
+  g_launches += 2;
+  for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
+    const int64_t n = std::min<int64_t>(chunk, rows - r0);
+    const int ns = nsplit > 1 ? assign_nsplit(n, k) : 1;
+    launch_rows_bf16(x + r0 * dim, n, dim, xbf, st);
+    cudaError_t e = launch_assign_tc(xbf, n, cbf, c2, k, dim, ns, pv, pi, st);
+    if (e != cudaSuccess) return fail(GIVF_ECUDA, std::string("assign: ") + cudaGetErrorString(e));
+    if (x2) launch_row_norms(x + r0 * dim, n, dim, x2, nullptr, nullptr, st);
+    launch_assign_reduce(pv, pi, ns, n, x2, labels + r0, dists ? dists + r0 : nullptr, st);
+    g_launches += 3 + (x2 ? 1 : 0);
+    KCHECK();
+  }
+  return GIVF_OK;
+}
+
+int givf_encode_rows(const givf_encode_desc* ds, void* stream) {
+  if (!ds) return fail(GIVF_EINVAL, "null argument");
+  if (!encode_supported(ds->dim, ds->m))
+    return fail(GIVF_EINVAL, "encode supports dim / m in {2..16} for m in {8, 16, 32}");
+  if (ds->grouping && (!ds->neighbor_ids || ds->l < 1 || ds->l > 64))
+    return fail(GIVF_EINVAL, "grouping needs neighbor_ids and 1 <= l <= 64");
+  if (ds->nseg == 0) return GIVF_OK;
+  int dev = 0, rc;
+  if ((rc = device_of(ds->x, &dev)) || (rc = device_of(ds->codes, &dev))) return rc;
+  if (encode_smem(ds->dim, ds->grouping ? ds->l : 1, ds->m) > 227 * 1024)
+    return fail(GIVF_EINVAL, "encode: shared memory for dim / l / m exceeds 227 KB");
+  CUDA_TRY(cudaSetDevice(dev));
+  EncodeArgsC a;
+  a.X = ds->x; a.order = ds->order; a.seg = ds->seg; a.seg_region = ds->seg_region;
+  a.nseg = ds->nseg; a.d = ds->dim; a.L = ds->l; a.M = ds->m; a.grouping = ds->grouping;
+  a.centroids = ds->centroids; a.nbr = ds->neighbor_ids; a.alphas = ds->alphas; a.csq = ds->c_sq;
+  a.codewords = ds->codewords; a.cwsq = ds->cw_sq; a.lo = ds->const_lo; a.step = ds->const_step;
+  a.pick = ds->pick; a.codes = ds->codes; a.cbytes = ds->const_bytes; a.consts = ds->consts;
+  cudaError_t e = launch_encode_rows(a, (cudaStream_t)stream);
+  g_launches += 1;
+  if (e != cudaSuccess) return fail(GIVF_ECUDA, std::string("encode: ") + cudaGetErrorString(e));
+  return GIVF_OK;
+}
+
+int givf_knn_exact(const float* queries, int64_t nq, const float* base, int64_t nb, int32_t dim,
+                   int32_t k, int32_t* ids, double* dist, void* stream) {
+  if (nq < 0 || nb < 1 || dim < 1 || dim > 1024) return fail(GIVF_EINVAL, "bad shape");
+  if (k < 1 || k > nb) return fail(GIVF_EINVAL, "need 1 <= k <= nb");
+  if (nb >= ((int64_t)1 << 31)) return fail(GIVF_EINVAL, "nb must be < 2^31");
+  if (nq == 0) return GIVF_OK;
+  int dev = 0, rc;
+  if ((rc = device_of(queries, &dev)) || (rc = device_of(base, &dev)) || (rc = device_of(ids, &dev)) ||
+      (rc = device_of(dist, &dev)))
+    return rc;
+  CUDA_TRY(cudaSetDevice(dev));
+  givf_index* ix = builder_ctx(dev);
+  if (!ix) return fail(GIVF_ENOMEM, "builder context");
+  std::lock_guard<std::mutex> lock(ix->mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  IndexView& v = ix->v;
+  v.K = (int)nb; v.d = dim; v.G = 1; v.M = 1; v.grouping = 0; v.n = 0;
+  v.centroids = base;
+  Plan pl{};
+  pl.P = k; pl.G = 1; pl.K = (int)nb; pl.d = dim;
+  pl.total = k; pl.kept = k; pl.budget = 1; pl.cap_w = 1;
+  pl.ps = probe_shape((int)nb, k);
+  const bool tc = tc_supported(dim);
+  const size_t persist = aligned_bytes<float>(nb) + aligned_bytes<unsigned int>(1) +
+                         (tc ? aligned_bytes<uint16_t>((size_t)nb * tc_kpad_b(dim)) : 0);
+  const size_t per_q = aligned_bytes<float>(dim) + probe_bytes_per_query(pl) + (size_t)k * 12 + 1024;
+  const size_t fixed = probe_fixed_bytes(pl) + (1 << 16);
+  const size_t budget = workspace_budget();
+  int64_t chunk = budget > fixed + persist ? (int64_t)((budget - fixed - persist) / per_q) : 1;
+  chunk = std::max<int64_t>(1, std::min<int64_t>({chunk, nq, (int64_t)65535}));
+  const size_t slice = fixed + per_q * (size_t)chunk + (1 << 20);
+  CUDA_TRY(ix->arena.reserve(persist + slice));
+  Arena& top = ix->arena;
+  top.reset();
+  float* c2f = top.take<float>(nb);
+  unsigned int* mx = top.take<unsigned int>(1);
+  void* cs = tc ? top.take<uint16_t>((size_t)nb * tc_kpad_b(dim)) : nullptr;
+  ARENA_CHECK(top);
+  CUDA_TRY(cudaMemsetAsync(mx, 0, sizeof(unsigned int), st));
+  launch_row_norms(base, nb, dim, c2f, nullptr, mx, st);
+  if (tc) launch_split_bf16(base, (int)nb, dim, 1, cs, st);
+  g_launches += tc ? 2 : 1;
+  KCHECK();
+  unsigned int mxh = 0;
+  CUDA_TRY(cudaMemcpyAsync(&mxh, mx, sizeof mxh, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  float cmaxf;
+  std::memcpy(&cmaxf, &mxh, sizeof cmaxf);
+  v.c2f = c2f;
+  v.cmax = (float)((double)cmaxf * (1.0 + 1e-6));
+  v.csplit = cs;
+  for (int64_t q0 = 0; q0 < nq; q0 += chunk) {
+    const int bq = (int)std::min<int64_t>(chunk, nq - q0);
+    Arena ar;
+    ar.base = static_cast<char*>(top.base) + top.off;
+    ar.cap = top.cap - top.off;
+    ar.reset();
+    rc = run_probe(ix, pl, queries + q0 * dim, bq, ids + q0 * k, dist + q0 * k, ar, st);
+    if (rc) return rc;
+  }
+  v.centroids = nullptr;
+  v.c2f = nullptr;
+  v.csplit = nullptr;
   return GIVF_OK;
 }
 

@@ -12,6 +12,12 @@ inline uint32_t next_pow2_host(uint32_t x) {
   return p;
 }
 
+// SM count of the current device (cached per device).
+int num_sms_cur();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) applies to the current
+// device only: done once per (kernel, device, size) and its status returned.
+cudaError_t ensure_max_smem(const void* fn, size_t bytes);
+
 // One scan segment: a run of consecutive code rows of one kept (region,
 // group) slice, with the float64 terms the distance needs (search.py:143-148).
 struct WorkItem {
@@ -151,9 +157,6 @@ struct ScanArgs {
 // K5 for a whole chunk: the inner-product LUT of every query (pq.py:147-169)
 void launch_build_luts(const IndexView& ix, const float* Q, int nq, float* luts, cudaStream_t s);
 void launch_scan(const ScanArgs& a, cudaStream_t s);
-// scan_async.cu: top-k scan with cp.async-staged code tiles; false when the
-// configuration is not covered (full mode, M not in {4, 8, 16, 32}, k > 2048)
-bool launch_scan_async(const ScanArgs& a, cudaStream_t s);
 // scan_warp.cu: warp-independent sweeps (the default); false when the
 // configuration is not covered (M > 32, top-k k > 128, n >= 2^32)
 bool launch_scan_warp(const ScanArgs& a, cudaStream_t s);
@@ -168,5 +171,39 @@ void launch_scan_order(const IndexView& ix, const WorkItem* work, int64_t cap_w,
 // K7: merge per-shard top-k lists (G, nq, k) into (nq, k)
 void launch_merge_topk(const int32_t* ids, const float* dists, int G, int nq, int k,
                        int32_t* out_ids, float* out_d, cudaStream_t s);
+
+// build_tc.cu: index-builder kernels
+int assign_kpad(int d);          // bf16 row width of KA's operands
+bool assign_supported(int d);    // d <= 128
+int assign_nsplit(int64_t rows, int K);
+void launch_rows_bf16(const float* x, int64_t rows, int d, void* out, cudaStream_t s);
+cudaError_t launch_assign_tc(const void* Xbf, int64_t rows, const void* Cbf, const float* c2, int K,
+                             int d, int nsplit, float* part_v, int32_t* part_i, cudaStream_t s);
+void launch_assign_reduce(const float* v, const int32_t* idx, int nsplit, int64_t rows,
+                          const float* x2, int32_t* out, float* out_d, cudaStream_t s);
+struct EncodeArgsC {
+  const float* X;
+  const int32_t* order;
+  const int64_t* seg;
+  const int32_t* seg_region;
+  int64_t nseg;
+  int d, L, M, grouping;
+  const float* centroids;
+  const int32_t* nbr;
+  const float* alphas;
+  const double* csq;
+  const float* codewords;
+  const float* cwsq;
+  double lo, step;
+  int16_t* pick;
+  uint8_t* codes;
+  uint8_t* cbytes;
+  double* consts;
+};
+bool encode_supported(int d, int M);
+void launch_row_norms(const float* x, int64_t rows, int d, float* out32, double* out64,
+                      unsigned int* max_bits, cudaStream_t s);
+size_t encode_smem(int d, int L, int M);
+cudaError_t launch_encode_rows(const EncodeArgsC& a, cudaStream_t s);
 
 }  // namespace givf

@@ -763,11 +763,7 @@ int launch_plan_approx(const PlanArgs& a0, cudaStream_t s) {
   a.defer_rescore = (a.ix.grouping && !a.sort_work) ? 1 : 0;
   const PaSmem L(a.ix.d, a.P, (int64_t)a.P * a.ix.G, a.ix.max_gsize < 65536);
   auto kern = a.defer_rescore ? k_plan_approx<false> : k_plan_approx<true>;
-  static size_t attr[2] = {0, 0};
-  if (L.bytes > attr[a.defer_rescore]) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
-    attr[a.defer_rescore] = L.bytes;
-  }
+  ensure_max_smem((const void*)kern, L.bytes);
   kern<<<a.nq, PA_THREADS, L.bytes, s>>>(a);
   if (!a.defer_rescore) return 1;
   static const int split = [] {  // CTAs per query (GIVF_RS_SPLIT)

@@ -638,11 +638,7 @@ void launch_probe_gemm(const float* Q, const float* C, const float* c2, int nq, 
 void launch_probe_select(const uint16_t* D, int64_t ldD, const float* q2, const float* qscale,
                          int nq, int K, int Tmin, int cap, const float* tmin, int ntiles,
                          uint32_t* tup, int* cand, int* cand_n, float* theta, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_probe_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    attr = true;
-  }
+  ensure_max_smem((const void*)k_probe_select, 64 * 1024);
   if (tmin && ntiles >= Tmin && K > cap)
     k_tile_theta<<<(nq + 7) / 8, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(tmin), nq,
                                                ntiles, Tmin, tup);
@@ -662,11 +658,7 @@ void launch_probe_recheck(const float* Q, const float* C, int nq, int K, int d, 
                           float cmax, float eps_scale, float half_rel, int* regions, double* qc2,
                           int* fail, unsigned long long* fail_count, cudaStream_t s) {
   size_t sm = probe_recheck_smem(d, P, cap);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_probe_recheck, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  ensure_max_smem((const void*)k_probe_recheck, 200 * 1024);
   k_probe_recheck<<<nq, 256, sm, s>>>(Q, C, K, d, P, cand, cand_n, cap, theta, cmax, eps_scale,
                                       half_rel, regions, qc2, fail, fail_count);
 }

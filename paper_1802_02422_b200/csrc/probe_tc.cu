@@ -466,15 +466,7 @@ bool make_map_out(CUtensorMap* m, void* ptr, int64_t rows, int cols, int64_t ld,
   return r == CUDA_SUCCESS;
 }
 
-int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return n;
-}
+int num_sms() { return num_sms_cur(); }
 
 }  // namespace
 
@@ -541,12 +533,7 @@ bool launch_probe_gemm_tc(const void* Abf, const void* Bbf, const float* c2, int
   const bool ns2 = tc_stages(d) == 2;
   auto kern = half ? (ns2 ? k_probe_gemm_tc<true, 2> : k_probe_gemm_tc<true, 3>)
                    : (ns2 ? k_probe_gemm_tc<false, 2> : k_probe_gemm_tc<false, 3>);
-  static size_t attr[4] = {0, 0, 0, 0};
-  const int slot = (ns2 ? 2 : 0) + (half ? 1 : 0);
-  if (attr[slot] < smem) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr[slot] = smem;
-  }
+  if (ensure_max_smem((const void*)kern, smem) != cudaSuccess) return false;
   kern<<<grid, tc::THREADS, smem, s>>>(ma, mb, md, use_tma_store, c2, nq, K, tc_ka(d), tc_kb(d),
                                        tc_lo_chunks(d), nsplit, o.D32, o.D16, o.ld, o.q2, o.qinv,
                                        o.qscale, tmin);

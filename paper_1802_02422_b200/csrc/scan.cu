@@ -305,11 +305,7 @@ template <int M>
 static void launch_scan_m(const ScanArgs& a, cudaStream_t s) {
   int bufcap = (int)next_pow2_host((uint32_t)((a.mode == 0 ? a.k : 0) + CHUNK));
   size_t sm = scan_smem_bytes(M, a.ix.d, bufcap);
-  static size_t attr = 0;
-  if (attr < sm) {
-    cudaFuncSetAttribute(k_scan<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    attr = sm;
-  }
+  ensure_max_smem((const void*)k_scan<M>, sm);
   k_scan<M><<<a.nq, SCAN_THREADS, sm, s>>>(a, bufcap);
 }
 
@@ -433,8 +429,7 @@ void launch_merge_topk(const int32_t* ids, const float* dists, int G, int nq, in
                        int32_t* out_ids, float* out_d, cudaStream_t s) {
   uint32_t np2 = next_pow2_host((uint32_t)(G * k));
   size_t sm = (size_t)np2 * 8;
-  if (sm > 48 * 1024)
-    cudaFuncSetAttribute(k_merge_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  ensure_max_smem((const void*)k_merge_topk, sm);
   k_merge_topk<<<nq, 256, sm, s>>>(ids, dists, G, nq, k, out_ids, out_d);
 }
 

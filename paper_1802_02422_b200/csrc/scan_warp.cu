@@ -840,11 +840,7 @@ void launch_build_luts(const IndexView& ix, const float* Q, int nq, float* luts,
   const size_t smem = (size_t)256 * ds * 4 + (size_t)LUT_QB * ds * 8 + 16;
   dim3 grid((nq + LUT_QB - 1) / LUT_QB, ix.M);
   auto go = [&](auto kern) {
-    static size_t attr = 0;
-    if (smem > attr && smem > 48 * 1024) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = smem;
-    }
+    ensure_max_smem((const void*)kern, smem);
     kern<<<grid, 256, smem, s>>>(ix, Q, nq, luts);
   };
   switch (ds) {
@@ -860,12 +856,7 @@ void launch_build_luts(const IndexView& ix, const float* Q, int nq, float* luts,
 template <int M, int U, bool CPA, bool XL, bool FULLK>
 static void launch_warp_mdxf(const ScanArgs& a, cudaStream_t s) {
   const size_t bytes = sw_bytes(M, 2 * U, CPA, XL, a.ix.d);
-  static size_t attr = 0;
-  if (attr < bytes) {
-    cudaFuncSetAttribute(k_scan_warp<M, U, CPA, XL, FULLK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)bytes);
-    attr = bytes;
-  }
+  ensure_max_smem((const void*)k_scan_warp<M, U, CPA, XL, FULLK>, bytes);
   k_scan_warp<M, U, CPA, XL, FULLK><<<a.nq, SW_THREADS, bytes, s>>>(a);
 }
 
@@ -894,37 +885,11 @@ static void launch_warp_md(const ScanArgs& a, cudaStream_t s) {
   launch_warp_mdx<M, U, CPA, false>(a, s);
 }
 
-// Batches summed together per warp (GIVF_SCAN_GROUP, default 1; twice that
-// many in flight) and how code rows are staged (default: cp.async into a
-// per-warp shared-memory ring; GIVF_SCAN_STAGE=registers: plain loads).
-static int env_int(const char* name, int dflt) {
-  const char* e = getenv(name);
-  return e ? atoi(e) : dflt;
-}
-static int scan_group() {  // batches summed together (GIVF_SCAN_GROUP: 1, 2)
-  static int u = [] { const int v = env_int("GIVF_SCAN_GROUP", 1); return v == 2 ? v : 1; }();
-  return u;
-}
-static bool scan_cpa() {  // measured faster on C2: the default
-  static bool c = [] {
-    const char* e = getenv("GIVF_SCAN_STAGE");
-    return !(e && strcmp(e, "registers") == 0);
-  }();
-  return c;
-}
-
-template <int M, bool CPA>
-static void launch_warp_mc(const ScanArgs& a, cudaStream_t s) {
-  switch (scan_group()) {
-    case 2: launch_warp_md<M, 2, CPA>(a, s); break;
-    default: launch_warp_md<M, 1, CPA>(a, s); break;
-  }
-}
-
+// One batch summed per group, code rows staged by cp.async (measured
+// fastest on C2; the register-staged and two-batch variants were dropped).
 template <int M>
 static void launch_warp_m(const ScanArgs& a, cudaStream_t s) {
-  if (scan_cpa()) launch_warp_mc<M, true>(a, s);
-  else launch_warp_mc<M, false>(a, s);
+  launch_warp_md<M, 1, true>(a, s);
 }
 
 bool scan_warp_ok(const ScanArgs& a) {

@@ -38,6 +38,17 @@ class IndexArrays:
     grouping: bool
     meta: object = None              # storage.FileMeta when read from a .givf file
 
+    def to_host(self) -> "IndexArrays":
+        """A copy whose arrays are all numpy (row arrays may be CUDA tensors
+        after a device-resident build)."""
+        import dataclasses
+
+        def h(a):
+            return a.cpu().numpy() if hasattr(a, "cpu") and not isinstance(a, np.ndarray) else a
+
+        return dataclasses.replace(self, point_ids=h(self.point_ids), codes=h(self.codes),
+                                   const_bytes=h(self.const_bytes))
+
     @property
     def k(self) -> int:
         return int(self.centroids.shape[0])
@@ -109,12 +120,34 @@ def _u8(a):
 
 
 def _ptr(a):
-    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data_as(ctypes.c_void_p)
+    return ctypes.c_void_p(a.data_ptr())  # CUDA tensor (device-resident row arrays)
+
+
+def _is_torch(a):
+    return a is not None and not isinstance(a, np.ndarray) and hasattr(a, "data_ptr")
+
+
+def _rows(a, dtype):
+    """Row arrays: numpy (converted) or CUDA tensors (checked, kept)."""
+    if _is_torch(a):
+        import torch
+
+        want = {np.int32: torch.int32, np.uint8: torch.uint8}[dtype]
+        if a.dtype != want or not a.is_contiguous():
+            a = a.to(want).contiguous()
+        return a
+    return np.ascontiguousarray(a, dtype=dtype)
 
 
 def shard_rows(arr: IndexArrays, g: int, shards: int):
     """Rows of shard g: slice [floor(g*s/G), floor((g+1)*s/G)) of every
     (region, group) segment of size s, in stored (ascending id) order."""
+    if _is_torch(arr.codes):
+        return _shard_rows_torch(arr, g, shards)
     sizes = arr.group_sizes.astype(np.int64)
     lo = (g * sizes) // shards
     hi = ((g + 1) * sizes) // shards
@@ -125,6 +158,24 @@ def shard_rows(arr: IndexArrays, g: int, shards: int):
     offs = np.cumsum(cnt) - cnt
     rows = first[seg] + (np.arange(seg.shape[0]) - offs[seg])
     return rows, lo.astype(np.int32), (hi - lo).astype(np.int32)
+
+
+def _shard_rows_torch(arr: IndexArrays, g: int, shards: int):
+    """shard_rows on the device (row arrays held as CUDA tensors)."""
+    import torch
+
+    dev = arr.codes.device
+    sizes = torch.from_numpy(arr.group_sizes.astype(np.int64)).to(dev)
+    lo = (g * sizes) // shards
+    hi = ((g + 1) * sizes) // shards
+    offs = torch.from_numpy(np.ascontiguousarray(arr.region_offsets[:-1])).to(dev)
+    starts = offs[:, None] + (torch.cumsum(sizes, 1) - sizes)
+    cnt = (hi - lo).reshape(-1)
+    first = (starts + lo).reshape(-1)
+    seg = torch.repeat_interleave(torch.arange(cnt.shape[0], device=dev), cnt)
+    ends = torch.cumsum(cnt, 0)
+    rows = first[seg] + (torch.arange(seg.shape[0], device=dev) - (ends - cnt)[seg])
+    return rows, lo.int().cpu().numpy(), (hi - lo).int().cpu().numpy()
 
 
 class DeviceIndex:
@@ -148,7 +199,7 @@ class DeviceIndex:
         else:
             offs, pids, codes, cbytes = arr.region_offsets, arr.point_ids, arr.codes, arr.const_bytes
             local_sizes = local_lo = None
-        offs, pids, codes, cbytes = _i64(offs), _i32(pids), _u8(codes), _u8(cbytes)
+        offs, pids, codes, cbytes = _i64(offs), _rows(pids, np.int32), _rows(codes, np.uint8), _rows(cbytes, np.uint8)
         keep = [arr.centroids, arr.alphas, arr.neighbor_ids, arr.norm_terms, gsz, offs,
                 local_sizes, local_lo, pids, codes, cbytes, arr.codewords, arr.rotation]
         desc = _native.IndexDesc(

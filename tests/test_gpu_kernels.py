@@ -101,12 +101,7 @@ def default_mode_result():
 
 @pytest.mark.parametrize("env_over", [
     {"GIVF_PROBE": "simt"},                        # SIMT fp32 probe GEMM
-    {"GIVF_PROBE_SUB": "5"},                       # probe + K3a in sub-chunks
-    {"GIVF_STREAMS": "2", "GIVF_CHUNK_QUERIES": "3"},  # chunks on two streams
-    {"GIVF_SCAN": "block"},                        # block-synchronous scan
-    {"GIVF_SCAN": "async"},                        # cp.async block scan
-    {"GIVF_SCAN_STAGE": "registers"},              # warp scan, register staging
-    {"GIVF_SCAN_GROUP": "2"},                      # warp scan, 2 batches summed together
+    {"GIVF_CHUNK_QUERIES": "3"},                   # many small chunks (arena reuse)
     {"GIVF_SCAN_LUT": "plain"},                    # warp scan, [m][256] LUT (bank conflicts)
     {"GIVF_GEMM_SPLIT": "3"},                      # probe GEMM work units: 3 slices per m-block
     {"GIVF_RS_SPLIT": "5"},                        # K4b: 5 CTAs per query

@@ -1,5 +1,5 @@
 """CPU-side checks of the C ABI library: it is built, loads, and exports
-every symbol include/givf_b200.h declares (no compute calls)."""
+every symbol include/*.h declares (no compute calls)."""
 
 import ctypes
 import os
@@ -12,8 +12,11 @@ from paper_1802_02422_b200 import _native
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+HEADERS = ("givf_b200.h", "givf_build.h")
+
+
 def header_symbols():
-    text = open(os.path.join(ROOT, "include", "givf_b200.h")).read()
+    text = "".join(open(os.path.join(ROOT, "include", h)).read() for h in HEADERS)
     return sorted(set(re.findall(r"\b(givf_[a-z_0-9]+)\s*\(", text)))
 
 
@@ -46,8 +49,10 @@ def test_struct_layouts_match_header(tmp_path):
         "givf_index_desc": _native.IndexDesc,
         "givf_search_params": _native.SearchParamsC,
         "givf_search_stats": _native.SearchStatsC,
+        "givf_encode_desc": _native.EncodeDesc,
     }
-    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "givf_b200.h"', "int main(void){"]
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "givf_b200.h"',
+             '#include "givf_build.h"', "int main(void){"]
     for cname, cls in structs.items():
         lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
         for fname, _ in cls._fields_:
