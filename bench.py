@@ -3,20 +3,24 @@ queries/sec at fixed recall@10; ADC scan GB/s vs HBM).
 
 A step = one pass of the search path (probe -> group scores/prune/budget ->
 LUT + ADC scan -> top-k) over one batch of queries.  Default workload =
-BASELINE.json configs[1] (N=100M, d=96, K=2^16, L=64, M=16, 10^4 queries,
-k=100) on seeded synthetic data built on the GPU (paper_1802_02422_b200.builder).
+BASELINE.json configs[2] at its full size on one B200: N = 1B, d = 96,
+K = 2^20, L = 64, M = 16, 10^4 queries, k = 100, the nprobe 32-512 sweep and
+(configs[4]) the batch x budget latency sweep on the same index.  The index
+is built on the GPU at the start of the run from seeded synthetic data
+(paper_1802_02422_b200.builder: fused sm_100a assignment / encode kernels,
+exact ground truth).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c2|c1|c3|c4|c3mini|c4mini] [--nprobe P] [--tau T] [--candidates C]
+                    [--workload c3|c3m8|c4|c2|c1|c3mini|c4mini] [--noise total|per_coord]
+                    [--nprobe P] [--tau T] [--candidates C]
 
-N>1 runs under torchrun.  Default `--layout queries`: every rank holds the
-whole index and searches a batch of 10^4 queries per step (the synthetic
-query set; queries are independent units: no data-path collective; weak
-scaling, value = all ranks' queries / the slowest rank's time).  `--layout lists`: every
-rank holds a slice of every inverted list and the per-rank top-k lists are
-all-gathered over NCCL and merged by K7 (strong scaling).
-`--impl reference` times the CPU oracle port of the reference path on the
-host cores (rank 0 only).
+N>1 runs under torchrun.  Default `--layout lists`: every rank
+owns a slice of every inverted list and the per-rank top-k lists are
+all-gathered over NCCL and merged by K7 (strong scaling: the same index and
+queries for every N).  `--layout queries`: every rank holds a whole replica
+and searches its own batch (weak scaling, no data-path collective).
+`--impl reference` times the reference's CPU query path (the oracle port of
+search.py, all host cores, rank 0 only) on the same workload.
 """
 
 from __future__ import annotations
@@ -35,33 +39,34 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+_C3 = dict(n=1_000_000_000, d=96, n_clusters=1 << 20, k=1 << 20, l=64, m=16, nq=10_000,
+           nprobe=64, tau=0.5, candidates=10_000, topk=100, kmeans_iters=4, pq_iters=8,
+           n_learn=8_000_000, config=2,
+           sweep="32:0.5,64:0.5,128:0.5,256:0.5,512:0.5,64:0.25,256:0.25,512:0.25",
+           latency_sweep=True)
 WORKLOADS = {
-    # BASELINE.json configs[1]: the single-B200 configuration
+    # BASELINE.json configs[2] on one B200: 1B x 96, K = 2^20, M = 16 (the
+    # 8-GPU layout shards these lists); configs[4]'s latency sweep runs on it
+    "c3": _C3,
+    # configs[2] with M = 8
+    "c3m8": dict(_C3, m=8, latency_sweep=False),
+    # BASELINE.json configs[3]: 1B x 128 SIFT-like uint8 rows, K = 2^20, M = 16
+    "c4": dict(_C3, d=128, kind="sift_u8", config=3, latency_sweep=False,
+               sweep="32:0.5,128:0.5,512:0.5"),
+    # BASELINE.json configs[1]: 100M x 96, K = 2^16, M = 16
     "c2": dict(n=100_000_000, d=96, n_clusters=65536, k=65536, l=64, m=16, nq=10_000,
                nprobe=64, tau=0.5, candidates=10_000, topk=100, kmeans_iters=8, pq_iters=10,
-               n_learn=2_000_000),
+               n_learn=2_000_000, config=1,
+               sweep="16:0.5,32:0.5,64:0.5,128:0.5,256:0.5,64:0.25,256:0.25"),
     # BASELINE.json configs[0]: the reference's CPU-runnable case
     "c1": dict(n=1_000_000, d=96, n_clusters=4096, k=4096, l=64, m=8, nq=1000,
                nprobe=32, tau=0.5, candidates=10_000, topk=100, kmeans_iters=10, pq_iters=15,
-               n_learn=100_000),
-    # BASELINE.json configs[2] on one B200 (1B x 96, K = 2^20, M = 16; the
-    # 8-GPU layout shards these lists).  Built with TF32 assignments, 8M learn
-    # rows and 3 Lloyd iterations so the build fits a session.
-    "c3": dict(n=1_000_000_000, d=96, n_clusters=1 << 20, k=1 << 20, l=64, m=16, nq=10_000,
-               nprobe=64, tau=0.5, candidates=10_000, topk=100, kmeans_iters=3, pq_iters=8,
-               n_learn=8_000_000, fast=True),
-    # BASELINE.json configs[3] on one B200: 1B x 128 SIFT-like uint8 rows
-    # (builder.SynthSpec kind='sift_u8'), K = 2^20, M = 16
-    "c4": dict(n=1_000_000_000, d=128, n_clusters=1 << 20, k=1 << 20, l=64, m=16, nq=10_000,
-               nprobe=64, tau=0.5, candidates=10_000, topk=100, kmeans_iters=3, pq_iters=8,
-               n_learn=8_000_000, fast=True, kind="sift_u8"),
-    "c4mini": dict(n=50_000_000, d=128, n_clusters=1 << 18, k=1 << 18, l=64, m=16, nq=10_000,
-                   nprobe=64, tau=0.5, candidates=10_000, topk=100, kmeans_iters=3, pq_iters=8,
-                   n_learn=2_000_000, fast=True, kind="sift_u8"),
-    # a smaller rehearsal of the c3 build path
-    "c3mini": dict(n=50_000_000, d=96, n_clusters=1 << 18, k=1 << 18, l=64, m=16, nq=10_000,
-                   nprobe=64, tau=0.5, candidates=10_000, topk=100, kmeans_iters=3, pq_iters=8,
-                   n_learn=2_000_000, fast=True),
+               n_learn=100_000, config=0),
+    # smaller rehearsals of the 1B shapes
+    "c3mini": dict(_C3, n=50_000_000, n_clusters=1 << 18, k=1 << 18, n_learn=2_000_000,
+                   latency_sweep=False, sweep=""),
+    "c4mini": dict(_C3, n=50_000_000, d=128, n_clusters=1 << 18, k=1 << 18, n_learn=2_000_000,
+                   kind="sift_u8", config=3, latency_sweep=False, sweep=""),
 }
 
 
@@ -79,7 +84,7 @@ BUILD_KEYS = ("n", "d", "n_clusters", "k", "l", "m", "nq", "kmeans_iters", "pq_i
 def workload_key(w, noise, seed):
     """Cache key over the fields that shape the index (not the search params)."""
     b = {k_: w[k_] for k_ in BUILD_KEYS if k_ in w}
-    s = json.dumps({**b, "noise": noise, "seed": seed, "v": 4}, sort_keys=True)
+    s = json.dumps({**b, "noise": noise, "seed": seed, "v": 5}, sort_keys=True)
     return hashlib.blake2b(s.encode(), digest_size=8).hexdigest()
 
 
@@ -162,14 +167,17 @@ def latency_sweep(dev, queries, w, k, batches=(1, 16, 256, 4096, 10000),
 
 
 def load_or_build(w, noise, seed, device, allow_build=True):
-    """Index arrays + queries + ground truth.  Built on the GPU; cached under
-    /tmp (a speed-up only -- nothing depends on the cache being present)."""
+    """Index arrays + queries + ground truth, built on the GPU.  Indexes up
+    to 200M rows are cached under /tmp (a speed-up only -- nothing depends on
+    the cache being present); larger ones keep their row arrays on the device
+    and are rebuilt every run."""
     from paper_1802_02422_b200.builder import BuildSpec, SynthSpec, build_synthetic
     from paper_1802_02422_b200.device_index import IndexArrays
 
+    big = w["n"] > 200_000_000
     cache_dir = os.environ.get("GIVF_BENCH_CACHE", "/tmp/givf_bench_cache")
     path = os.path.join(cache_dir, workload_key(w, noise, seed) + ".npz")
-    if os.path.exists(path):
+    if not big and os.path.exists(path):
         try:
             z = np.load(path)
             arr = IndexArrays(
@@ -189,16 +197,15 @@ def load_or_build(w, noise, seed, device, allow_build=True):
     data = SynthSpec(d=w["d"], n_clusters=w["n_clusters"], sigma=0.3, noise=noise, seed=seed,
                      kind=w.get("kind", "gauss"))
     spec = BuildSpec(n=w["n"], k=w["k"], l=w["l"], m=w["m"], n_learn=w["n_learn"],
-                     kmeans_iters=w["kmeans_iters"], pq_iters=w["pq_iters"], seed=seed,
-                     fast=w.get("fast", False))
-    arr, queries, gt = build_synthetic(data, spec, w["nq"], gt_t=10, device=device, log=log)
+                     kmeans_iters=w["kmeans_iters"], pq_iters=w["pq_iters"], seed=seed)
+    arr, queries, gt = build_synthetic(data, spec, w["nq"], gt_t=10, device=device, log=log,
+                                       rows_on_device=big)
     build_s = time.perf_counter() - t0
     import torch
 
     torch.cuda.empty_cache()  # the build's temporaries; the index allocates its own
-    if (w["n"] > 200_000_000 and not os.environ.get("GIVF_BENCH_CACHE")
-            and int(os.environ.get("WORLD_SIZE", "1")) == 1):
-        return arr, queries, gt, build_s  # tens of GB: cache only on request
+    if big:
+        return arr, queries, gt, build_s
     try:
         os.makedirs(cache_dir, exist_ok=True)
         tmp = path + f".tmp{os.getpid()}.npz"
@@ -268,60 +275,76 @@ class ClockSampler:
 # ---------------------------------------------------------------- CPU arms
 
 
-def _cpu_worker(args):
-    """Oracle port of the reference path on one core over a query slice."""
-    arr_path, qi, params, deadline = args
+_CPU_STATE = {}
+
+
+def _cpu_worker(qi):
+    """Oracle port of the reference path (search.py:93-163, exact probe via a
+    BLAS shortlist re-checked in float64) on one core over a query slice."""
     from threadpoolctl import threadpool_limits
 
     threadpool_limits(1)  # one BLAS thread per forked worker (no oversubscription)
     from oracle import search_oracle as so
 
-    arr = _CPU_STATE["arr"]
-    queries = _CPU_STATE["queries"]
-    c = arr.centroids
-    c_sq = np.einsum("kd,kd->k", c.astype(np.float64), c.astype(np.float64))
-    cmax = float(np.sqrt(c_sq.max()))
+    st = _CPU_STATE
+    arr, queries, params = st["arr"], st["queries"], st["params"]
+    c_sq, cmax, gstarts = st["c_sq"], st["cmax"], st["gstarts"]
 
     def probe(cc, q, nprobe):
         return so.probe_exact_fast(cc, q, nprobe, c_sq=c_sq, cmax=cmax)
 
-    done = 0
     t0 = time.perf_counter()
     for i in qi:
-        if time.perf_counter() > deadline:
-            break
-        so.search_one(arr, queries[i], params, probe=probe)
-        done += 1
-    return done, time.perf_counter() - t0
+        so.search_one(arr, queries[i], params, probe=probe, gstarts=gstarts)
+    return len(qi), time.perf_counter() - t0
 
 
-_CPU_STATE = {}
+class CpuOracle:
+    """The reference CPU query path on every host core: one forked worker
+    per core (created once), each searching its share of a query sample."""
 
+    def __init__(self, arr, queries, w, cores=None):
+        import multiprocessing as mproc
 
-def cpu_port_qps(arr, queries, w, seconds=20.0, cores=None):
-    """Time the oracle port (numpy restatement of search.py:93-163 with the
-    exact probe) on the host cores: fork one worker per core, each takes a
-    strided slice of the queries until the time budget runs out."""
-    import multiprocessing as mproc
+        from oracle import search_oracle as so
 
-    from oracle import search_oracle as so
+        self.cores = cores or os.cpu_count() or 1
+        host = arr.to_host() if hasattr(arr, "to_host") else arr
+        c64 = host.centroids.astype(np.float64)
+        c_sq = np.einsum("kd,kd->k", c64, c64)
+        _CPU_STATE.update(
+            arr=host, queries=queries,
+            params=so.Params(nprobe=w["nprobe"], tau=w["tau"], candidates=w["candidates"]),
+            c_sq=c_sq, cmax=float(np.sqrt(c_sq.max())),
+            gstarts=so.group_starts(host.group_sizes, host.region_offsets))
+        os.environ["OPENBLAS_NUM_THREADS"] = "1"
+        self.pool = mproc.get_context("fork").Pool(self.cores)
+        self.nq = queries.shape[0]
+        self.next = 0
 
-    cores = cores or os.cpu_count() or 1
-    _CPU_STATE["arr"] = arr
-    _CPU_STATE["queries"] = queries
-    p = so.Params(nprobe=w["nprobe"], tau=w["tau"], candidates=w["candidates"])
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    ctx = mproc.get_context("fork")
-    t0 = time.perf_counter()
-    deadline = time.time() + seconds
-    deadline_pc = time.perf_counter() + seconds
-    jobs = [(None, list(range(r, len(queries), cores)), p, deadline_pc) for r in range(cores)]
-    with ctx.Pool(cores) as pool:
-        res = pool.map(_cpu_worker, jobs)
-    wall = time.perf_counter() - t0
-    done = sum(r[0] for r in res)
-    del deadline
-    return done / wall, done, wall, cores
+    def run(self, count):
+        """Search `count` queries (the next ones in the set); returns
+        (queries done, wall seconds)."""
+        idx = [(self.next + i) % self.nq for i in range(count)]
+        self.next = (self.next + count) % self.nq
+        jobs = [idx[r::self.cores] for r in range(self.cores)]
+        t0 = time.perf_counter()
+        res = self.pool.map(_cpu_worker, jobs)
+        return sum(r[0] for r in res), time.perf_counter() - t0
+
+    def rate(self, seconds):
+        """Queries/s over about `seconds` of work, in rounds of 4 per core."""
+        self.run(self.cores)  # warm-up (imports, page-in of the index)
+        done, wall = 0, 0.0
+        while wall < seconds:
+            d, t = self.run(4 * self.cores)
+            done += d
+            wall += t
+        return done / wall, done, wall
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
 
 
 # ---------------------------------------------------------------- GPU arm
@@ -329,6 +352,17 @@ def cpu_port_qps(arr, queries, w, seconds=20.0, cores=None):
 
 def l2_flush(buf):
     buf.add_(1.0)  # writes > L2 (126 MB) between timed steps
+
+
+def config_of(args, w, units):
+    """The workload description shared by both arms (same keys, same values)."""
+    return {
+        "workload": f"BASELINE configs[{w['config']}] ({args.workload})",
+        "n": w["n"], "d": w["d"], "K": w["k"], "L": w["l"], "M": w["m"],
+        "data": w.get("kind", "gauss"), "noise": args.noise if w.get("kind") != "sift_u8" else None,
+        "queries_per_step": units, "nprobe": w["nprobe"], "tau": w["tau"],
+        "candidates": w["candidates"], "k": w["topk"],
+    }
 
 
 def run_ours(args, w):
@@ -345,24 +379,16 @@ def run_ours(args, w):
     from paper_1802_02422_b200 import SearchParams, _native
     from paper_1802_02422_b200.sharded import ShardedIndex
 
-    # rank 0 builds (or loads) the workload; the others load it from the cache
-    if rank == 0:
-        arr, queries, gt, build_s = load_or_build(w, args.noise, args.seed, f"cuda:{local}")
-    if world > 1:
-        torch.distributed.barrier()
-    if rank != 0:
-        arr, queries, gt, build_s = load_or_build(w, args.noise, args.seed, f"cuda:{local}",
-                                                  allow_build=False)
+    # every rank builds the same index (deterministic seeds); ranks of the
+    # lists layout keep only their shard of it
+    arr, queries, gt, build_s = load_or_build(w, args.noise, args.seed, f"cuda:{local}")
     torch.cuda.synchronize()
-    # layout: "queries" = every rank holds the whole index and
-    # searches its own batch of nq queries per step (queries are independent
-    # units: no data-path collective, weak scaling); "lists" = every rank
-    # owns a shard of every inverted list, the per-rank top-k lists are
-    # all-gathered over NCCL and merged by K7 (the same nq queries for every
-    # N: strong scaling)
     lists = args.layout == "lists" and world > 1
     shards = world if lists else 1
     sx = ShardedIndex(arr, rank if lists else 0, shards, device=local)
+    if lists:  # the shard is on the device; drop the full row arrays
+        arr = None
+        torch.cuda.empty_cache()
     params = SearchParams(nprobe=w["nprobe"], tau=w["tau"], candidates=w["candidates"],
                           ef_search=w["k"])
     k = w["topk"]
@@ -400,7 +426,7 @@ def run_ours(args, w):
     fallbacks = {k_: (fb1[k_] - fb0[k_]) / args.steps for k_ in fb0}
     rs1 = sx.dev.plan_fallback_reasons()
     plan_reasons = {k_: (rs1[k_] - rs0[k_]) / args.steps for k_ in rs0 if rs1[k_] > rs0[k_]}
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    step_ms = [s_.elapsed_time(e_) for s_, e_ in zip(starts, ends)]
     total_ms = float(np.sum(step_ms))
     if world > 1:
         t = torch.tensor([total_ms], device="cuda")
@@ -416,9 +442,6 @@ def run_ours(args, w):
     recall = {r: recall_at_r(list(ids_h), gt, r) for r in (1, 10, 100)}
 
     # ---- per-stage kernel time (separate pass, events on the launching stream)
-    # one internal stream here, so each kernel's event-timed duration is its own
-    saved_streams = os.environ.get("GIVF_STREAMS")
-    os.environ["GIVF_STREAMS"] = "1"
     _native.profile_enable(True)
     _native.profile_read()
     prof_steps = max(1, min(3, args.steps))
@@ -428,43 +451,58 @@ def run_ours(args, w):
     torch.cuda.synchronize()
     stages = _native.profile_read()
     _native.profile_enable(False)
-    if saved_streams is None:
-        os.environ.pop("GIVF_STREAMS", None)
-    else:
-        os.environ["GIVF_STREAMS"] = saved_streams
 
     # ---- end to end through the public API with host buffers (pinned)
     from paper_1802_02422_b200.query import search_batch
 
-    e2e_qps = None
     h2d = queries.nbytes
     d2h = nq * k * 8 + nq * 32
+    qh = torch.from_numpy(queries).pin_memory()
     if not lists:  # every rank: its own batch through the public API
-        qh = torch.from_numpy(queries).pin_memory().numpy()
+        qn = qh.numpy()
         oi = torch.empty((nq, k), dtype=torch.int32).pin_memory().numpy()
         od = torch.empty((nq, k), dtype=torch.float32).pin_memory().numpy()
         os_ = torch.empty((nq, 4), dtype=torch.int64).pin_memory().numpy()
-        search_batch(sx.dev, qh, params, k=k, out=(oi, od, os_))
-        e2e_t = 0.0
-        for _ in range(args.steps):
-            l2_flush(flush)
-            torch.cuda.synchronize()
-            if world > 1:
-                torch.distributed.barrier()
-            t0 = time.perf_counter()
-            search_batch(sx.dev, qh, params, k=k, out=(oi, od, os_))
-            e2e_t += time.perf_counter() - t0
-        if world > 1:  # slowest rank
-            t = torch.tensor([e2e_t], device="cuda")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            e2e_t = float(t.item())
-        e2e_qps = units * args.steps / e2e_t
-        assert np.array_equal(oi, ids_h), "e2e results differ from the device-resident run"
 
-    sweep = latency_sweep(sx.dev, queries, w, k) if (args.latency_sweep and world == 1) else None
+        def e2e_step():
+            search_batch(sx.dev, qn, params, k=k, out=(oi, od, os_))
+            return oi
+    else:  # H2D of the queries, sharded search + NCCL merge, D2H of the results
+        oi_t = torch.empty((nq, k), dtype=torch.int32).pin_memory()
+        od_t = torch.empty((nq, k), dtype=torch.float32).pin_memory()
+        os_t = torch.empty((nq, 4), dtype=torch.int64).pin_memory()
+
+        def e2e_step():
+            qd = qh.to("cuda", non_blocking=True)
+            i_, d_, s_ = sx.search_topk(qd, params, k)
+            oi_t.copy_(i_, non_blocking=True)
+            od_t.copy_(d_, non_blocking=True)
+            os_t.copy_(s_, non_blocking=True)
+            torch.cuda.synchronize()
+            return oi_t.numpy()
+    e2e_step()
+    e2e_t = 0.0
+    for _ in range(args.steps):
+        l2_flush(flush)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        got = e2e_step()
+        e2e_t += time.perf_counter() - t0
+    if world > 1:  # slowest rank
+        t = torch.tensor([e2e_t], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_t = float(t.item())
+    e2e_qps = units * args.steps / e2e_t
+    assert np.array_equal(got, ids_h), "e2e results differ from the device-resident run"
+
+    sweep_on = (args.latency_sweep or w.get("latency_sweep", False)) and not args.no_sweeps
+    sweep = latency_sweep(sx.dev, queries, w, k) if (sweep_on and world == 1) else None
     psweep = None
-    if args.sweep and world == 1:
-        settings = [(int(a), float(b)) for a, b in (x.split(":") for x in args.sweep.split(","))]
+    sweep_spec = args.sweep if args.sweep is not None else ("" if args.no_sweeps else w.get("sweep", ""))
+    if sweep_spec and world == 1:
+        settings = [(int(a), float(b)) for a, b in (x.split(":") for x in sweep_spec.split(","))]
         psweep = param_sweep(sx, q_dev, gt, w, k, settings, flush)
 
     if rank != 0:
@@ -488,14 +526,25 @@ def run_ours(args, w):
     if os.path.exists(tr_path):
         try:
             tr = json.load(open(tr_path))
-            # ncu DRAM bytes of one captured scan launch, scaled to this step's
-            # queries (same per-query work) so it compares with `achieved`
+            # ncu DRAM bytes of one captured scan launch of this workload,
+            # per query, scaled to this step's queries
             traffic = tr["dram_bytes_per_launch"] / tr["queries_per_launch"] * nq / shards
         except Exception:  # noqa: BLE001
             traffic = None
     gemm_ms, gemm_n = stages["probe_gemm"]
     probe_flops = 2.0 * w["k"] * w["d"] * nq
-    step_stage_ms = {s: v[0] / prof_steps for s, v in stages.items() if v[1]}
+    step_stage_ms = {s_: v[0] / prof_steps for s_, v in stages.items() if v[1]}
+    cfg = config_of(args, w, units)
+    cfg.update({
+        "queries_per_rank_step": nq,
+        "recall@1": recall[1], "recall@10": recall[10], "recall@100": recall[100],
+        "codes_scanned_mean": float(stats_h[:, 3].mean()),
+        "l2": "flushed between steps (512 MB write); codes also exceed L2",
+        "parallelism": (f"list-shard x{world} (NCCL all-gather + K7 merge)" if lists
+                        else f"query-parallel x{world} (index replica per GPU, no collective)"
+                        if world > 1 else "single GPU"),
+        "build_s": build_s,
+    })
     line = {
         "metric": "queries/sec at fixed recall@10 (synthetic, B200)",
         "value": qps,
@@ -505,25 +554,13 @@ def run_ours(args, w):
         "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps,
         "higher_is_better": True,
-        "scaling": "strong" if args.layout == "lists" else "weak",
+        "scaling": "strong" if lists else "weak",
         "vs_baseline": None,
         "dtype": "f32/f64 (u8 codes)",
         "data": ("synthetic: seeded SIFT-like uint8 gamma mixture, built on GPU"
                  if w.get("kind") == "sift_u8"
                  else f"synthetic: seeded gaussian mixture, noise={args.noise}, built on GPU"),
-        "config": {
-            "workload": f"BASELINE configs[{ {'c1': 0, 'c2': 1, 'c4': 3, 'c4mini': 3}.get(args.workload, 2)}] ({args.workload})",
-            "n": w["n"], "d": w["d"], "K": w["k"], "L": w["l"], "M": w["m"],
-            "queries_per_step": units, "queries_per_rank_step": nq,
-            "nprobe": w["nprobe"], "tau": w["tau"],
-            "candidates": w["candidates"], "k": k, "noise": args.noise,
-            "recall@1": recall[1], "recall@10": recall[10], "recall@100": recall[100],
-            "codes_scanned_mean": float(stats_h[:, 3].mean()),
-            "l2": "flushed between steps (512 MB write); codes also exceed L2",
-            "parallelism": (f"list-shard x{world} (NCCL all-gather + K7 merge)" if lists
-                            else f"query-parallel x{world} (index replica per GPU, no collective)"
-                            if world > 1 else "single GPU"),
-        },
+        "config": cfg,
         "roofline": {
             "kernel": "scan (K6 ADC scan + top-k)",
             "bound": "hbm",
@@ -552,46 +589,69 @@ def run_ours(args, w):
         "e2e": {"value": e2e_qps, "unit": "queries/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
         "clocks": clocks.summary(),
-        "build_s": build_s,
     }
+    ref_recall = reference_recall(args.workload, args.noise)
+    if ref_recall:
+        line["reference_recall"] = ref_recall
     if world == 1 and not args.no_cpu_baseline:
-        cps, done, wall, cores = cpu_port_qps(arr, queries, w, seconds=args.cpu_seconds)
-        line["cpu_baseline"] = {"value": cps, "unit": "queries/s", "cores": cores, "kind": "port",
-                                "sample": f"{done} of {nq} queries in {wall:.1f}s "
-                                          f"(oracle port, exact probe, fork x{cores})"}
+        cpu = CpuOracle(arr, queries, w)
+        cps, done, wall = cpu.rate(args.cpu_seconds)
+        cpu.close()
+        line["cpu_baseline"] = {"value": cps, "unit": "queries/s", "cores": cpu.cores, "kind": "port",
+                                "sample": f"{done} of the {nq} step queries in {wall:.1f}s "
+                                          f"(oracle port of search.py, exact probe, fork x{cpu.cores})"}
     return line
 
 
+def reference_recall(workload, noise):
+    """The reference's own recall@10 on the same data family, measured with
+    the reference package (tools/reference_recall.py, committed result)."""
+    path = os.path.join(ROOT, "profiles", "reference_recall.json")
+    if not os.path.exists(path):
+        return None
+    try:
+        return json.load(open(path))
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def run_reference(args, w):
+    """The reference's CPU query path (oracle port of search.py:93-163 with
+    the exact probe) on the host cores, same workload; each step is a
+    bounded sample of 8 queries per core (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
     import torch
 
-    arr, queries, gt, _ = load_or_build(w, args.noise, args.seed, "cuda:0")
-    del torch
-    per_step = []
-    total_done = 0
-    cores = os.cpu_count() or 1
-    secs = max(2.0, args.cpu_seconds / max(args.steps + args.warmup, 1))
-    for i in range(args.warmup + args.steps):
-        qps, done, wall, cores = cpu_port_qps(arr, queries, w, seconds=secs, cores=cores)
-        if i >= args.warmup:
-            per_step.append(qps)
-            total_done += done
-    v = float(np.mean(per_step))
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    arr, queries, gt, _ = load_or_build(w, args.noise, args.seed, "cuda")
+    torch.cuda.empty_cache()
+    cpu = CpuOracle(arr, queries, w)
+    del arr
+    per = 8 * cpu.cores
+    for _ in range(args.warmup):
+        cpu.run(per)
+    walls, done = [], 0
+    for _ in range(args.steps):
+        d, t = cpu.run(per)
+        walls.append(t)
+        done += d
+    cpu.close()
+    total = float(np.sum(walls))
+    v = done / total
     return {
         "impl": "reference",
         "metric": "queries/sec at fixed recall@10 (synthetic, B200)",
         "value": v, "unit": "queries/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * w["nq"] / v,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "strong" if args.layout == "lists" else "weak",
         "vs_baseline": None,
         "dtype": "f32/f64 (u8 codes)", "data": f"synthetic, noise={args.noise}",
-        "config": {"workload": args.workload, "nprobe": w["nprobe"], "tau": w["tau"],
-                   "candidates": w["candidates"], "k": w["topk"]},
-        "cpu_baseline": {"value": v, "unit": "queries/s", "cores": cores, "kind": "port",
-                         "sample": f"{total_done} queries over {args.steps} steps of {secs:.1f}s"},
+        "config": dict(config_of(args, w, w["nq"]), queries_per_step_timed=per,
+                       sample=f"each step: {per} of the {w['nq']} queries (8 per core)"),
+        "cpu_baseline": {"value": v, "unit": "queries/s", "cores": cpu.cores, "kind": "port",
+                         "sample": f"{done} queries over {args.steps} steps of {per}"},
         "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -602,21 +662,24 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--latency-sweep", action="store_true",
-                    help="add BASELINE configs[4]'s batch x budget latency sweep (N=1)")
-    ap.add_argument("--sweep", default="",
-                    help="extra nprobe:tau settings on the same index, e.g. 32:0.5,128:0.25 (N=1)")
-    ap.add_argument("--noise", default="per_coord", choices=["per_coord", "total"])
+                    help="add BASELINE configs[4]'s batch x budget latency sweep (N=1; on by "
+                         "default for c3)")
+    ap.add_argument("--sweep", default=None,
+                    help="nprobe:tau settings on the same index, e.g. 32:0.5,128:0.25 (N=1; "
+                         "default: the workload's BASELINE sweep)")
+    ap.add_argument("--no-sweeps", action="store_true", help="skip both sweeps")
+    ap.add_argument("--noise", default="total", choices=["per_coord", "total"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--nprobe", type=int)
     ap.add_argument("--tau", type=float)
     ap.add_argument("--candidates", type=int)
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--layout", default="queries", choices=["queries", "lists"],
-                    help="N>1: query-parallel replicas (weak scaling) or list shards "
-                         "merged over NCCL (strong scaling)")
+    ap.add_argument("--layout", default="lists", choices=["queries", "lists"],
+                    help="N>1: list shards merged over NCCL (strong scaling, default) or "
+                         "query-parallel replicas (weak scaling)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     w = dict(WORKLOADS[args.workload])
