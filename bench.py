@@ -65,6 +65,8 @@ WORKLOADS = {
     # smaller rehearsals of the 1B shapes
     "c3mini": dict(_C3, n=50_000_000, n_clusters=1 << 18, k=1 << 18, n_learn=2_000_000,
                    latency_sweep=False, sweep=""),
+    # K = 2^20 probe / planner shapes on a 100M-row index (quick iterations)
+    "c3k": dict(_C3, n=100_000_000, latency_sweep=False, sweep=""),
     "c4mini": dict(_C3, n=50_000_000, d=128, n_clusters=1 << 18, k=1 << 18, n_learn=2_000_000,
                    kind="sift_u8", config=3, latency_sweep=False, sweep=""),
 }

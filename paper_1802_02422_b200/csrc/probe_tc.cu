@@ -94,6 +94,11 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
   const int n_tiles = (K + BN - 1) / BN;
   const int units = m_blocks * nsplit;
   const int per_split = (n_tiles + nsplit - 1) / nsplit;
+  // Units run slice-major: the CTAs resident at any moment work on the same
+  // centroid slice for different query blocks, so each B tile comes from HBM
+  // once and is re-read from L2 by the others (at K = 2^20 the split
+  // centroids, 400 MB, do not fit in L2: m-block-major order re-streamed
+  // them from HBM once per query block).
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) { mbar_init(&sm->full[s], 1); mbar_init(&sm->empty[s], 1); }
@@ -125,7 +130,7 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
     if (lane == 0) {
       uint32_t stage = 0, phase = 0, a_phase = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int mb = u / nsplit, sp = u % nsplit;
+        const int mb = u % m_blocks, sp = u / m_blocks;  // slice-major (see below)
         const int t0 = sp * per_split, t1 = min(n_tiles, t0 + per_split);
         if (t0 >= t1) continue;
         mbar_wait(&sm->a_empty, a_phase ^ 1);
@@ -147,7 +152,7 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
     // ------------------------------------------------ MMA issuer
     uint32_t stage = 0, phase = 0, a_phase = 0, acc = 0, acc_phase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int sp = u % nsplit;
+      const int sp = u / m_blocks;
       const int t0 = sp * per_split, t1 = min(n_tiles, t0 + per_split);
       if (t0 >= t1) continue;
       mbar_wait(&sm->a_full, a_phase);
@@ -201,7 +206,7 @@ k_probe_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
                  e * 128;
     uint32_t acc = 0, acc_phase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int mb = u / nsplit, sp = u % nsplit;
+      const int mb = u % m_blocks, sp = u / m_blocks;
       const int t0 = sp * per_split, t1 = min(n_tiles, t0 + per_split);
       const int q = mb * BM + quarter * 32 + lane;
       float q2r = 0.f, ir = 1.f;  // fp16 encoding of this row

@@ -11,7 +11,7 @@ import numpy as np
 import pytest
 
 import golden_io
-from parity import assert_topk_equal
+from parity import assert_ranked_equal, assert_topk_equal
 
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -291,3 +291,11 @@ def test_parity_c2_family_at_10m():
         for i in range(q.shape[0]):
             assert_topk_equal(ids[i], d[i], wi[i], wd[i])
     assert dev.fallback_counts()["probe"] == 0
+    # full reference semantics (every scanned code): candidate-id sets
+    # bit-exact, ranked lists equal outside tie runs
+    p = SearchParams(nprobe=64, tau=0.5, candidates=10_000)
+    for i, r in enumerate(search_batch(dev, q[:16], p)):
+        fi, fd, fs = so.search_one(arr, q[i], so.Params(**vars(p)))
+        assert (r.stats.regions_visited, r.stats.subregions_visited, r.stats.subregions_pruned,
+                r.stats.codes_scanned) == tuple(fs)
+        assert_ranked_equal(r.ids, r.distances, fi, fd)
