@@ -37,7 +37,7 @@ EXPORTS = (
 )
 
 STAGES = ("probe_gemm", "probe_select", "probe_recheck", "probe_full", "plan", "scan",
-          "finish", "merge", "lut")
+          "finish", "merge", "lut", "probe_sample", "plan_scores")
 
 
 class IndexDesc(ctypes.Structure):

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <random>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -60,7 +61,8 @@ thread_local std::string g_err;
 std::atomic<int64_t> g_launches{0};
 
 // Per-stage device timing: CUDA events around every launch, on its stream.
-enum Stage { ST_GEMM, ST_SELECT, ST_RECHECK, ST_FULL, ST_PLAN, ST_SCAN, ST_FINISH, ST_MERGE, ST_LUT, ST_N };
+enum Stage { ST_GEMM, ST_SELECT, ST_RECHECK, ST_FULL, ST_PLAN, ST_SCAN, ST_FINISH, ST_MERGE, ST_LUT,
+             ST_SAMPLE, ST_K3A, ST_N };
 struct Profiler {
   std::mutex mu;
   std::atomic<bool> on{false};
@@ -294,6 +296,10 @@ size_t workspace_budget() {
 struct ProbeShape {
   int Tmin, cap;
   bool exhaustive;  // rank all K regions exactly (nprobe == K or P too large)
+  // fused probe (probe_fused.cu): survivors targeted by the sample
+  // threshold, the sample order statistic that estimates it, the survivor
+  // list capacity and the re-check set capacity
+  int ftarget, fj, fcap, fcap2;
 };
 ProbeShape probe_shape(int K, int P) {
   ProbeShape s;
@@ -303,13 +309,30 @@ ProbeShape probe_shape(int K, int P) {
   s.Tmin = std::min(K, P + std::max(extra, P / 4));
   s.cap = std::min(K, std::max(2 * s.Tmin, capmin));
   if (s.cap > 4096) s.exhaustive = true;  // recheck sorts in <= 4096-entry smem
+  s.ftarget = s.fj = s.fcap = s.fcap2 = 0;
   return s;
+}
+
+// Fused-probe sizes for a sample of Ks of the K centroids: aim the
+// threshold at ~3P + 128 survivors (the sample's j-th smallest chunk minimum
+// estimates the ftarget-th smallest score; with j >= 16 the chance that it
+// falls below the P-th is negligible), list capacity 6x that.
+void fused_shape(ProbeShape* s, int K, int Ks, int P) {
+  static const int mul = getenv("GIVF_FUSED_TARGET") ? atoi(getenv("GIVF_FUSED_TARGET")) : 3;
+  const int64_t target = std::min<int64_t>(K, (int64_t)mul * P + 128);
+  s->ftarget = (int)target;
+  s->fj = (int)std::max<int64_t>(1, (target * Ks + K - 1) / K);
+  s->fcap = (int)std::min<int64_t>(65536, std::max<int64_t>(8192, 8 * target));
+  s->fcap2 = (int)std::min<int64_t>(4096, std::max<int64_t>(256, 4 * (int64_t)P));
+  if (s->fcap2 < P) s->exhaustive = true;
 }
 
 constexpr int kFullSlots = 32;
 
 struct Plan {
   int P, G, K, d;
+  bool fused;  // probe_fused.cu (no score matrix), K3a from fp16 rows
+  int Ks;
   int64_t total, kept, budget, cap_w;
   ProbeShape ps;
 };
@@ -336,16 +359,31 @@ bool use_tensor_cores(const IndexView& v) {
   return mode == 1 && v.csplit != nullptr;
 }
 
+// The fused probe (no score matrix) from K = 2^17 up, where the fp16 score
+// matrix (2 K bytes per query) costs more HBM traffic than K3a's direct
+// reads of the probed regions' neighbor rows (P G 2 d bytes); GIVF_PROBE =
+// fused | dmat | simt overrides.
+bool use_fused(const IndexView& v) {
+  static const int mode = [] {  // 1 forced, 0 off, -1 by K
+    const char* e = getenv("GIVF_PROBE");
+    return !e ? -1 : strcmp(e, "fused") == 0 ? 1 : 0;
+  }();
+  if (!v.c16) return false;
+  return mode == 1 || (mode == -1 && v.K >= (1 << 17));
+}
+
 // Probe for one chunk of queries: regions (nq, P) and qc2 (nq, P).  *D_out
 // receives the fp16-encoded score matrix (nq, K) when the GEMM path ran, else
 // null, *scale_out its per-query decode scale and *eps_out the GEMM's
 // error-bound scale.
 int run_probe(givf_index* ix, const Plan& pl, const float* dQ, int nq, int* regions,
               double* qc2, Arena& ar, cudaStream_t st, const uint16_t** D_out = nullptr,
-              const float** scale_out = nullptr, float* eps_out = nullptr) {
+              const float** scale_out = nullptr, float* eps_out = nullptr,
+              bool* fused_out = nullptr) {
   const IndexView& v = ix->v;
   const int P = pl.P, K = v.K, d = v.d;
   if (D_out) *D_out = nullptr;
+  if (fused_out) *fused_out = false;
   int* failf = ar.take<int>(nq);
   const uint32_t kp2 = next_pow2_host((uint32_t)K), pp2 = next_pow2_host((uint32_t)P);
   uint64_t* sk = ar.take<uint64_t>((size_t)kFullSlots * kp2);
@@ -363,6 +401,55 @@ int run_probe(givf_index* ix, const Plan& pl, const float* dQ, int nq, int* regi
     }
     staged(ST_FULL, st, [&] {
       launch_probe_full(dQ, v.centroids, nq, K, d, P, mode, failf, slots, sk, sv, sk2, sv2, sdv,
+                        regions, qc2, st);
+    });
+    KCHECK();
+    return GIVF_OK;
+  }
+  if (pl.fused) {
+    // F0-F3 + K2 (probe_fused.cu): no score matrix
+    const ProbeShape& ps = pl.ps;
+    const int dp = f16_pitch(d);
+    const int nch = (v.Ks + 31) / 32;
+    uint16_t* q16 = ar.take<uint16_t>((size_t)nq * dp);
+    float* ms = ar.take<float>(nq);
+    float* q2f = ar.take<float>(nq);
+    float* cmin = ar.take<float>((size_t)nq * nch);
+    float* thr = ar.take<float>(nq);
+    int nseg = 0, cap_u = 0;
+    filter_segments(nq, K, ps.fcap, &nseg, &cap_u);
+    int* cnt = ar.take<int>((size_t)nq * nseg);
+    int* cid = ar.take<int>((size_t)nq * nseg * cap_u);
+    float* cval = ar.take<float>((size_t)nq * nseg * cap_u);
+    int* cand = ar.take<int>((size_t)nq * ps.fcap2);
+    int* cand_n = ar.take<int>(nq);
+    float* theta = ar.take<float>(nq);
+    ARENA_CHECK(ar);
+    const float eps = probe_f16_eps(d);
+    cudaError_t ce = cudaSuccess;
+    staged(ST_SAMPLE, st, [&] {
+      launch_query_f16(dQ, nq, d, v.c16x, q16, ms, q2f, st);
+      ce = launch_probe_sample(q16, v.s16, v.sc2, nq, v.Ks, d, ms, cmin, st);
+      launch_probe_thresh(cmin, nch, ps.fj, q2f, v.cmax, eps, nq, thr, st);
+    }, 3);
+    if (ce != cudaSuccess) return fail(GIVF_ECUDA, std::string("probe sample: ") + cudaGetErrorString(ce));
+    staged(ST_GEMM, st, [&] {
+      ce = launch_probe_filter(q16, v.c16, v.c2f, nq, K, d, ms, thr, nseg, cap_u, cnt, cid, cval,
+                               st);
+    });
+    if (ce != cudaSuccess) return fail(GIVF_ECUDA, std::string("probe filter: ") + cudaGetErrorString(ce));
+    staged(ST_SELECT, st, [&] {
+      launch_probe_pick(cnt, cid, cval, nseg, cap_u, ps.fcap, thr, q2f, v.cmax, eps, P, ps.fcap2,
+                        nq, cand, cand_n, theta, st);
+    });
+    if (eps_out) *eps_out = direct_f16_eps(d);  // K3a's bound (direct rows)
+    if (fused_out) *fused_out = true;
+    staged(ST_RECHECK, st, [&] {
+      launch_probe_recheck(dQ, v.centroids, nq, K, d, P, cand, cand_n, ps.fcap2, theta, v.cmax,
+                           eps, 0.f, regions, qc2, failf, v.counters, st);
+    });
+    staged(ST_FULL, st, [&] {
+      launch_probe_full(dQ, v.centroids, nq, K, d, P, 1, failf, slots, sk, sv, sk2, sv2, sdv,
                         regions, qc2, st);
     });
     KCHECK();
@@ -420,7 +507,11 @@ int run_probe(givf_index* ix, const Plan& pl, const float* dQ, int nq, int* regi
 
 size_t probe_bytes_per_query(const Plan& pl) {
   size_t b = aligned_bytes<int>(1) * 4 + aligned_bytes<int>(pl.P) + aligned_bytes<double>(pl.P);
-  if (!pl.ps.exhaustive)
+  if (!pl.ps.exhaustive && pl.fused)
+    b += (size_t)f16_pitch(pl.d) * 2 + 8 * aligned_bytes<float>(1) +
+         (size_t)((pl.Ks + 31) / 32) * 4 + (size_t)pl.ps.fcap * 8 + 2048 * 4 +
+         (size_t)pl.ps.fcap2 * 4 + 512;
+  else if (!pl.ps.exhaustive)
     b += (size_t)pl.K * 2 + 4 * aligned_bytes<float>(1) + (size_t)pl.ps.cap * 4 +
          aligned_bytes<float>(probe_tiles(pl.K)) +
          (size_t)tc_kpad(pl.d) * 2 + 256;
@@ -444,6 +535,10 @@ int build_plan(givf_index* ix, const givf_search_params* p, Plan* pl) {
   pl->budget = p->candidates;
   pl->cap_w = std::max<int64_t>(1, std::min(pl->kept, pl->budget));
   pl->ps = probe_shape(pl->K, pl->P);
+  pl->fused = !pl->ps.exhaustive && use_fused(ix->v);
+  pl->Ks = ix->v.Ks;
+  if (pl->fused) fused_shape(&pl->ps, pl->K, pl->Ks, pl->P);
+  if (pl->ps.exhaustive) pl->fused = false;
   return GIVF_OK;
 }
 
@@ -582,6 +677,7 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
     }
     pa.ldD = v.K;
     pa.cmax = v.cmax;
+    pa.half_rel = (float)kHalfRel;
     pa.only = ar.take<int>(bq);
     ARENA_CHECK(ar);
     // the approximate planner's keys alias the exact scratch, which the exact
@@ -597,17 +693,23 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
       const uint16_t* Dmat = nullptr;
       const float* dscale = nullptr;
       float eps_scale = 0.f;
-      rc = run_probe(ix, pl, dQ, bq, regions, qc2, ar, st, &Dmat, &dscale, &eps_scale);
+      bool fused = false;
+      rc = run_probe(ix, pl, dQ, bq, regions, qc2, ar, st, &Dmat, &dscale, &eps_scale, &fused);
       if (rc) return rc;
       pa.eps_scale = eps_scale;
-      if (!Dmat) {  // exhaustive probe (nprobe == K or too wide): exact planner only
+      if (!Dmat && !fused) {  // exhaustive probe (nprobe == K or too wide): exact planner only
         approx = false;
       } else {
         PlanArgs sa = pa;
         sa.D = Dmat;
         sa.dscale = dscale;
+        if (fused) {
+          sa.direct = 1;
+          sa.half_rel = 0.f;
+          pa.half_rel = 0.f;
+        }
         int nk = 0;
-        staged(ST_PLAN, st, [&] { nk = launch_plan_scores(sa, st); }, 0);
+        staged(ST_K3A, st, [&] { nk = launch_plan_scores(sa, st); }, 0);
         g_launches += nk;
         KCHECK();
       }
@@ -845,6 +947,47 @@ int givf_index_create(const givf_index_desc* ds, int device, givf_index_t* out) 
       v.csplit = cs;
     }
   }
+  if (e == cudaSuccess && fused_supported(d)) {
+    // fused probe (probe_fused.cu): fp16 centroids scaled by 2^-ec (max
+    // |c_ij| in [2^13, 2^14)), and a seeded random sample of them
+    float amax = 0.f;
+    for (size_t i = 0; i < (size_t)K * d; ++i) amax = std::max(amax, std::fabs(ds->centroids[i]));
+    const int ec = amax > 0.f ? std::ilogb(amax) - 13 : 0;
+    v.c16e = ec;
+    v.c16x = std::ldexp(1.0f, ec);
+    const int dp = f16_pitch(d);
+    // sample: every centroid up to 8192, else K/8 (at most 2^17)
+    const int Ks = K <= 8192 ? K : std::min(1 << 17, std::max(8192, K / 8));
+    std::vector<int32_t> ids((size_t)K);
+    for (int i = 0; i < K; ++i) ids[i] = i;
+    if (Ks < K) {
+      std::mt19937_64 rng(0x9e3779b97f4a7c15ull);
+      for (int i = 0; i < Ks; ++i) {
+        std::uniform_int_distribution<int> pick(i, K - 1);
+        std::swap(ids[i], ids[pick(rng)]);
+      }
+      std::sort(ids.begin(), ids.begin() + Ks);
+    }
+    void *c16 = nullptr, *s16 = nullptr;
+    float* sc2 = nullptr;
+    const int32_t* dids = nullptr;
+    const size_t cb = (size_t)K * dp * 2, sb = (size_t)Ks * dp * 2;
+    e = cudaMalloc(&c16, cb);
+    if (e == cudaSuccess) { ix->allocs.push_back(c16); ix->dev_bytes += (int64_t)cb; e = cudaMalloc(&s16, sb); }
+    if (e == cudaSuccess) { ix->allocs.push_back(s16); ix->dev_bytes += (int64_t)sb; e = cudaMalloc(&sc2, (size_t)Ks * 4); }
+    if (e == cudaSuccess) { ix->allocs.push_back(sc2); e = upload(ix, ids.data(), (size_t)Ks, &dids); }
+    if (e == cudaSuccess) {
+      launch_rows_f16(v.centroids, nullptr, K, d, ec, c16, nullptr, nullptr, 0);
+      launch_rows_f16(v.centroids, dids, Ks, d, ec, s16, v.c2f, sc2, 0);
+      e = cudaDeviceSynchronize();
+    }
+    if (e == cudaSuccess) {
+      v.c16 = c16;
+      v.s16 = s16;
+      v.sc2 = sc2;
+      v.Ks = Ks;
+    }
+  }
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ix->stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
     givf_index_destroy(ix);
@@ -905,7 +1048,14 @@ int givf_probe_scores(givf_index_t ix, const float* queries, int64_t nq, float* 
   const IndexView& v = ix->v;
   const int K = v.K, d = v.d;
   const bool q_dev = is_device_ptr(queries), o_dev = is_device_ptr(scores);
-  const size_t bytes = (size_t)nq * (d * 4 + (size_t)K * 4 + tc_kpad(d) * 2 + probe_tiles(K) * 4) +
+  const bool fz = use_fused(v);
+  int nseg = 0, cap_u = 0;
+  if (fz) {  // every centroid survives thr = +inf: segments sized for a whole slice
+    filter_segments((int)nq, K, K, &nseg, &cap_u);
+    cap_u = (K + nseg / 2 - 1) / (nseg / 2) + 256;
+  }
+  const size_t bytes = (size_t)nq * (d * 4 + (size_t)K * 4 + (size_t)nseg * cap_u * 8 + nseg * 4 +
+                                     tc_kpad(d) * 2 + probe_tiles(K) * 4 + f16_pitch(d) * 2 + 64) +
                        (1 << 20);
   CUDA_TRY(ix->arena.reserve(bytes));
   Arena& ar = ix->arena;
@@ -917,6 +1067,40 @@ int givf_probe_scores(givf_index_t ix, const float* queries, int64_t nq, float* 
     dQ = t;
   }
   float* D = o_dev ? scores : ar.take<float>((size_t)nq * K);
+  if (fz) {
+    // the fused GEMM's own fp32 scores: its filter with thr = +inf keeps all
+    uint16_t* q16 = ar.take<uint16_t>((size_t)nq * f16_pitch(d));
+    float* ms = ar.take<float>(nq);
+    float* thr = ar.take<float>(nq);
+    int* cnt = ar.take<int>((size_t)nq * nseg);
+    int* cid = ar.take<int>((size_t)nq * nseg * cap_u);
+    float* cval = ar.take<float>((size_t)nq * nseg * cap_u);
+    ARENA_CHECK(ar);
+    std::vector<float> inf((size_t)nq, INFINITY);
+    CUDA_TRY(cudaMemcpyAsync(thr, inf.data(), sizeof(float) * nq, cudaMemcpyHostToDevice, st));
+    launch_query_f16(dQ, (int)nq, d, v.c16x, q16, ms, nullptr, st);
+    cudaError_t ce = launch_probe_filter(q16, v.c16, v.c2f, (int)nq, K, d, ms, thr, nseg, cap_u,
+                                         cnt, cid, cval, st);
+    if (ce != cudaSuccess) return fail(GIVF_ECUDA, std::string("probe filter: ") + cudaGetErrorString(ce));
+    g_launches += 2;
+    const size_t ne = (size_t)nq * nseg * cap_u;
+    std::vector<int> hc((size_t)nq * nseg), hi(ne);
+    std::vector<float> hv(ne), out((size_t)nq * K, NAN);
+    CUDA_TRY(cudaMemcpyAsync(hc.data(), cnt, sizeof(int) * nq * nseg, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(hi.data(), cid, sizeof(int) * ne, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(hv.data(), cval, sizeof(float) * ne, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    for (int64_t b = 0; b < nq; ++b)
+      for (int sg = 0; sg < nseg; ++sg) {
+        const size_t o = ((size_t)b * nseg + sg) * cap_u;
+        for (int i = 0; i < std::min(hc[(size_t)b * nseg + sg], cap_u); ++i)
+          out[(size_t)b * K + hi[o + i]] = hv[o + i];
+      }
+    CUDA_TRY(cudaMemcpy(scores, out.data(), sizeof(float) * nq * K,
+                        o_dev ? cudaMemcpyHostToDevice : cudaMemcpyHostToHost));
+    if (eps_scale_out) *eps_scale_out = probe_f16_eps(d);
+    return GIVF_OK;
+  }
   float* tmin = ar.take<float>((size_t)nq * probe_tiles(K));
   const bool tc = use_tensor_cores(v);
   ScoreOut so;  // the GEMM's own fp32 scores (the search path stores fp16)

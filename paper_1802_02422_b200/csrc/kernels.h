@@ -50,6 +50,13 @@ struct IndexView {
   const float* rotation;      // (d, d) or null
   const float* ctab;          // (256) dequantized constants, f32
   const void* csplit;         // (K, tc_kpad_b(d)) bf16 [c_hi | c_lo] or null
+  // fused probe (probe_fused.cu): fp16 centroids c 2^-c16e, pitch f16_pitch(d)
+  const void* c16;            // (K, dp) or null
+  int c16e;                   // scale exponent ec
+  float c16x;                 // 2^ec
+  const void* s16;            // (Ks, dp) fp16 rows of a random centroid sample
+  const float* sc2;           // (Ks) their f32 |c|^2
+  int Ks;
   unsigned long long* counters;  // [0] probe fallbacks, [1] plan fallbacks (device)
 };
 
@@ -79,6 +86,28 @@ size_t tc_smem_bytes(int d);
 void launch_split_bf16(const float* x, int rows, int d, int centroid, void* out, cudaStream_t s);
 bool launch_probe_gemm_tc(const void* Abf, const void* Bbf, const float* c2, int nq, int K, int d,
                           const ScoreOut& o, float* tmin, cudaStream_t s);
+
+// probe_fused.cu: the probe without a score matrix (large K)
+int f16_pitch(int d);
+bool fused_supported(int d);
+float probe_f16_eps(int d);   // GEMM bound, units of cmax^2 + 2 |q| cmax
+float direct_f16_eps(int d);  // K3a-from-fp16-rows bound, same units
+void launch_rows_f16(const float* x, const int32_t* ids, int64_t rows, int d, int e, void* out,
+                     const float* c2in, float* c2out, cudaStream_t s);
+void launch_query_f16(const float* Q, int nq, int d, float cexp, void* q16, float* ms, float* q2,
+                      cudaStream_t s);
+cudaError_t launch_probe_sample(const void* q16, const void* s16, const float* sc2, int nq, int Ks,
+                                int d, const float* ms, float* cmin, cudaStream_t s);
+void filter_segments(int nq, int K, int fcap, int* nseg, int* cap_u);
+cudaError_t launch_probe_filter(const void* q16, const void* c16, const float* c2, int nq, int K,
+                                int d, const float* ms, const float* thr, int nseg, int cap_u,
+                                int* cnt, int* cid, float* cval, cudaStream_t s);
+void launch_probe_thresh(const float* cmin, int nch, int j, const float* q2, float cmax,
+                         float eps_scale, int nq, float* thr, cudaStream_t s);
+void launch_probe_pick(const int* cnt, const int* cid, const float* cval, int nseg, int cap_u,
+                       int fcap, const float* thr, const float* q2, float cmax, float eps_scale,
+                       int P, int cap2, int nq, int* cand, int* cand_n, float* theta,
+                       cudaStream_t s);
 
 // probe.cu
 int probe_tiles(int K);  // per-query tile minima the GEMM epilogue emits
@@ -126,6 +155,10 @@ struct PlanArgs {
   int* only;            // (nq) fallback flags: exact kernels run where only[b] != 0
   uint32_t* akey;       // (nq, P*G) scratch: float32 order key of the approximate score
   int defer_rescore;    // set by launch_plan_approx: base/score by k_plan_rescore
+  // K3a without D: qs2~ from the fp16 centroid rows (ix.c16); half_rel is the
+  // relative storage error of the approximate qs2 (kHalfRel for D, 0 here)
+  int direct;
+  float half_rel;
   int approx;           // akey holds K3a's keys: run the approximate-first planner
 };
 // plan_approx.cu: K3a, the approximate group scores (needs D; may run per

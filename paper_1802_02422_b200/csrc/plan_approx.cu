@@ -89,6 +89,73 @@ __global__ void __launch_bounds__(PA_THREADS) k_plan_scores_approx(PlanArgs a) {
   }
 }
 
+// K3a without the score matrix (fused probe, probe_fused.cu): qs2~ =
+// |q|^2 + |c_s|^2 - 2 q.c~_s from the neighbor's fp16 centroid row (192 B at
+// d = 96) and the float32 query, float32 dot product; error bound
+// direct_f16_eps (units of cmax^2 + 2 |q| cmax), no storage term (half_rel 0).
+// One warp per (query, probed region) as above, a lane per group.
+template <int DP8>
+__global__ void __launch_bounds__(PA_THREADS) k_plan_scores_direct(PlanArgs a) {
+  __shared__ __align__(16) float qsm[PA_THREADS / 32][DP8 * 8];
+  const IndexView& ix = a.ix;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t wid = (int64_t)blockIdx.x * (PA_THREADS / 32) + w;
+  const int P = a.P, G = ix.G, d = ix.d;
+  if (wid >= (int64_t)a.nq * P) return;
+  const int b = (int)(wid / P), p = (int)(wid % P);
+  const int64_t total = (int64_t)P * G;
+  const int r = a.regions[(int64_t)b * P + p];
+  const double qc = a.qc2[(int64_t)b * P + p];
+  uint32_t* akey = a.akey + (int64_t)b * total + (int64_t)p * G;
+  if (!ix.grouping) {
+    const uint32_t k = f32_key((float)qc);
+    for (int j = lane; j < G; j += 32) akey[j] = k;
+    return;
+  }
+  float* qs = qsm[w];
+  double s = 0.0;
+  for (int j = lane; j < DP8 * 8; j += 32) {
+    const float x = j < d ? a.Q[(int64_t)b * d + j] : 0.f;
+    qs[j] = x;
+    s += (double)x * x;
+  }
+  const double q2 = warp_sum(s);
+  __syncwarp();
+  const double al = (double)ix.alphas[r];
+  const double oma_qc = dmul(dsub(1.0, al), qc);
+  const double cx2 = 2.0 * (double)ix.c16x;
+  const uint4* C16 = reinterpret_cast<const uint4*>(ix.c16);
+  const float4* q4 = reinterpret_cast<const float4*>(qs);
+  for (int j = lane; j < G; j += 32) {
+    const int64_t g = (int64_t)r * G + j;
+    const int n = __ldg(ix.nbr + g);
+    const float m = __ldg(ix.norm + g);
+    const uint4* row = C16 + (int64_t)n * DP8;
+    uint4 u[DP8];
+#pragma unroll
+    for (int c = 0; c < DP8; ++c) u[c] = __ldg(row + c);
+    float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+    for (int c = 0; c < DP8; ++c) {
+      const float4 qa = q4[2 * c], qb = q4[2 * c + 1];  // shared-memory broadcast
+      const float2 h0 = __half22float2(*reinterpret_cast<const __half2*>(&u[c].x));
+      const float2 h1 = __half22float2(*reinterpret_cast<const __half2*>(&u[c].y));
+      const float2 h2 = __half22float2(*reinterpret_cast<const __half2*>(&u[c].z));
+      const float2 h3 = __half22float2(*reinterpret_cast<const __half2*>(&u[c].w));
+      acc0 = fmaf(qa.x, h0.x, acc0);
+      acc1 = fmaf(qa.y, h0.y, acc1);
+      acc0 = fmaf(qa.z, h1.x, acc0);
+      acc1 = fmaf(qa.w, h1.y, acc1);
+      acc0 = fmaf(qb.x, h2.x, acc0);
+      acc1 = fmaf(qb.y, h2.y, acc1);
+      acc0 = fmaf(qb.z, h3.x, acc0);
+      acc1 = fmaf(qb.w, h3.y, acc1);
+    }
+    const double qs2 = dsub(dadd(q2, (double)__ldg(ix.c2f + n)), dmul(cx2, (double)(acc0 + acc1)));
+    akey[j] = f32_key((float)dadd(dadd(oma_qc, dmul(al, qs2)), (double)m));
+  }
+}
+
 // ---------------------------------------------------------------- K4
 struct PaSmem {
   // byte offsets into the dynamic shared block
@@ -287,7 +354,7 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
   // fp16 error is relative to the stored distance itself.
   const double eps_g = (double)a.eps_scale * ((double)a.cmax * a.cmax + 2.0 * qn * a.cmax);
   const double E_loose = ix.grouping
-      ? 1.0001 * alx * (eps_g + 1.001 * kHalfRel * cq * cq) + amax * 1.2e-7 + 1e-12 * cq * cq
+      ? 1.0001 * alx * (eps_g + 1.001 * (double)a.half_rel * cq * cq) + amax * 1.2e-7 + 1e-12 * cq * cq
       : amax * 1.2e-7;  // float32 key rounding only
   PLAN_PHASE(0);
 
@@ -400,7 +467,7 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
   // item above lies above v* + 2E exactly: the certification below holds.
   double E = E_loose;
   if (ix.grouping && ix.rneg && aln >= 0.0 && alx <= 1.0 && !no_cut) {
-    const double rr = 1.001 * kHalfRel;
+    const double rr = 1.001 * (double)a.half_rel;
     const double Eabs = 1.001 * alx * eps_g + alx * 4e-12 * cq * cq +
                         amax * 1.2e-7 * (1.0 + rr) + 1e-12 * cq * cq;
     const double Et = (Eabs + rr * fmax(0.0, vstar + amax * 1.2e-7 + nng)) / (1.0 - 3.0 * rr);
@@ -777,7 +844,17 @@ int launch_plan_approx(const PlanArgs& a0, cudaStream_t s) {
 int launch_plan_scores(const PlanArgs& a, cudaStream_t s) {
   const int64_t warps = (int64_t)a.nq * a.P;
   const int per = PA_THREADS / 32;
-  k_plan_scores_approx<<<(unsigned)((warps + per - 1) / per), PA_THREADS, 0, s>>>(a);
+  const unsigned grid = (unsigned)((warps + per - 1) / per);
+  if (a.direct) {
+    switch (f16_pitch(a.ix.d) / 32) {
+      case 1: k_plan_scores_direct<4><<<grid, PA_THREADS, 0, s>>>(a); break;
+      case 2: k_plan_scores_direct<8><<<grid, PA_THREADS, 0, s>>>(a); break;
+      case 3: k_plan_scores_direct<12><<<grid, PA_THREADS, 0, s>>>(a); break;
+      default: k_plan_scores_direct<16><<<grid, PA_THREADS, 0, s>>>(a); break;
+    }
+    return 1;
+  }
+  k_plan_scores_approx<<<grid, PA_THREADS, 0, s>>>(a);
   return 1;
 }
 

@@ -105,6 +105,10 @@ def default_mode_result():
     {"GIVF_SCAN_LUT": "plain"},                    # warp scan, [m][256] LUT (bank conflicts)
     {"GIVF_GEMM_SPLIT": "3"},                      # probe GEMM work units: 3 slices per m-block
     {"GIVF_RS_SPLIT": "5"},                        # K4b: 5 CTAs per query
+    {"GIVF_PROBE": "fused"},                       # fused probe, 2 x 128 queries x 128 centroids
+    {"GIVF_PROBE": "fused", "GIVF_FILTER_SHAPE": "4x64"},  # 4 x 128 queries x 64 centroids
+    {"GIVF_PROBE": "fused", "GIVF_FILTER_SHAPE": "1x128"},  # 128 queries, rows shared by 2 warps
+    {"GIVF_PROBE": "fused", "GIVF_FUSED_TARGET": "0"},  # threshold at ~128 survivors
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_execution_modes_agree(env_over, default_mode_result):
     """Every tuning knob changes how the work is scheduled, never the result:

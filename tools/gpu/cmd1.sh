@@ -1,0 +1,7 @@
+set -x
+for P in 64 512; do
+  timeout 300 python tools/probe_bench.py --nprobe $P 2>&1 | tail -2
+  GIVF_PROBE=dmat timeout 300 python tools/probe_bench.py --nprobe $P 2>&1 | tail -2
+done
+timeout 900 python -m pytest -q -x tests/test_gpu_fused.py tests/test_gpu_kernels.py -k "fused or modes" 2>&1 | tail -15
+timeout 900 python -m pytest -q -x tests/test_gpu_parity_scale.py -k "probe_lists or 512-0.5" 2>&1 | tail -15

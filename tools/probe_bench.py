@@ -55,7 +55,8 @@ def main():
     torch.cuda.synchronize()
     st = _native.profile_read()
     print(f"probe K={k} nq={args.nq} P={args.nprobe}: {a.elapsed_time(b) / args.reps:.3f} ms/call; "
-          + ", ".join(f"{n} {v[0] / args.reps:.3f}" for n, v in st.items() if v[1]))
+          + ", ".join(f"{n} {v[0] / args.reps:.3f}" for n, v in st.items() if v[1])
+          + f"; fallbacks {dev.fallback_counts()}")
 
 
 if __name__ == "__main__":
