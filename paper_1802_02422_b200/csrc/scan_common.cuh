@@ -124,6 +124,33 @@ GIVF_DEV float code_sum_xl(const CodeVec<M>& code, uint32_t lane_base, int x,
   return numpy_sum<M>(e);
 }
 
+// code_sum_xl with the per-step lane addresses precomputed: bs[s] =
+// lane_base ^ (s << 2), so each lookup is PRMT + LEA + LDS.
+template <int M>
+GIVF_DEV float code_sum_xlb(const CodeVec<M>& code, const uint32_t (&bs)[M], int x,
+                            const uint32_t (&xsel)[4]) {
+  CodeVec<M> p;  // words by k ^ (x >> 2)
+  const int xh = x >> 2;
+  if constexpr (M == 16) {
+    uint32_t t[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) t[k] = (xh & 1) ? code.w[k ^ 1] : code.w[k];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) p.w[k] = (xh & 2) ? t[k ^ 2] : t[k];
+  } else {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) p.w[k] = (xh & 1) ? code.w[k ^ 1] : code.w[k];
+  }
+  float e[M];
+#pragma unroll
+  for (int s = 0; s < M; ++s) {
+    const uint32_t byte = __byte_perm(p.w[s >> 2], 0, xsel[s & 3]);
+    const uint32_t addr = bs[s] + (byte << 7);
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(e[s]) : "r"(addr));
+  }
+  return numpy_sum<M>(e);
+}
+
 // LUT of one query (pq.py:147-169): optional rotation q' = R q, then
 // entry[m][i] = <q'_m, codeword[m][i]> accumulated in float64, rounded once;
 // plus (ctab != null) the dequantized constants as float64 (grouping.py:123-129).

@@ -401,6 +401,130 @@ __device__ __forceinline__ void warp_shrink(uint64_t* wb, int* cnt_io, uint32_t*
   if (lane == 0) atomicMin(s_thr64, (unsigned long long)*thr64);
 }
 
+// The end of a top-k scan: each warp's entries under the shared bound, ids
+// resolved, then exactly min(total, k) of them by (dist, id) across the
+// warps, written to the outputs.  Called by all threads after the warps'
+// final shrink and a block barrier.
+__device__ __forceinline__ void scan_final(const ScanArgs& a, int b, int k, uint64_t* wb, int cnt,
+                                        unsigned char* dsm, uint64_t* merge, uint32_t* bh,
+                                        unsigned long long* s_thr64_p, uint32_t* s_tw, int* s_wcnt,
+                                        uint32_t* s_sel, int* s_nout_p) {
+  const IndexView& ix = a.ix;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  unsigned long long& s_thr64 = *s_thr64_p;
+  int& s_nout = *s_nout_p;
+  uint64_t T = s_thr64;
+  {  // the quota bound (warp_cut) holds as well
+    uint32_t qb = 0;
+#pragma unroll
+    for (int w = 0; w < SW_WARPS; ++w) qb = max(qb, s_tw[w]);
+    const uint64_t tq = ((uint64_t)qb << 32) | 0xffffffffull;
+    T = T < tq ? T : tq;
+  }
+  {
+    // every id load of the warp in flight at once (cnt <= SW_WB)
+    constexpr int R = SW_WB / 32;
+    uint64_t vr[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int i = j * 32 + lane;
+      uint64_t v = i < cnt ? wb[i] : kKeyPad;
+      if (i < cnt && (v >> 32) <= (T >> 32))
+        v = (v & 0xffffffff00000000ull) | (uint32_t)__ldg(ix.pids + (uint32_t)v);
+      else
+        v = kKeyPad;
+      vr[j] = v;
+    }
+    int out = 0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const bool keep = vr[j] <= T;
+      const uint32_t bal = __ballot_sync(FULL, keep);
+      if (keep) wb[out + __popc(bal & lt_mask)] = vr[j];
+      out += __popc(bal);
+    }
+    if (lane == 0) s_wcnt[warp] = out;
+  }
+  __syncthreads();
+  uint64_t* const all = reinterpret_cast<uint64_t*>(dsm + SW_WBUF);
+  auto slot_key = [&](int i) -> uint64_t {  // slot i of the warps' buffers
+    return (i % SW_WB) < s_wcnt[i / SW_WB] ? all[i] : kKeyPad;
+  };
+  int nm = 0, myoff = 0;
+  for (int w = 0; w < SW_WARPS; ++w) {
+    if (w == warp) myoff = nm;
+    nm += s_wcnt[w];
+  }
+  // usually the survivors fit the merge area: gather them there so the
+  // selection below touches nm entries, not every buffer slot
+  const bool compact = nm <= SW_WARPS * SW_KMAX;
+  if (compact) {
+    for (int i = lane; i < s_wcnt[warp]; i += 32) merge[myoff + i] = wb[i];
+    __syncthreads();
+  }
+  auto key_at = [&](int i) -> uint64_t { return compact ? merge[i] : slot_key(i); };
+  const int n_in = compact ? nm : SW_WARPS * SW_WB;
+  uint64_t* fin = compact ? all : merge;
+  int nf = 0;
+  if (compact && nm <= 128) {  // few survivors: sort them all, keep the first k
+    if (warp == 0) warp_sort128(merge, nm);
+    __syncthreads();
+    fin = merge;
+    nf = min(nm, k);
+  } else {
+    uint64_t lim = kKeyPad;
+    if (nm > k) {
+      uint32_t need = (uint32_t)k, eq = 0;
+      const uint32_t kd = block_select(n_in, [&](int i) { return (uint32_t)(key_at(i) >> 32); },
+                                       bh, s_sel, &need, &eq);
+      uint32_t kp = 0xffffffffu;
+      if (eq != need) {
+        uint32_t eq2;
+        kp = block_select(n_in, [&](int i) {
+          const uint64_t v = key_at(i);
+          return (uint32_t)(v >> 32) == kd ? (uint32_t)v : 0xffffffffu;
+        }, bh, s_sel, &need, &eq2);
+      }
+      lim = ((uint64_t)kd << 32) | kp;
+    }
+    if (tid == 0) s_nout = 0;
+    __syncthreads();
+    for (int i0 = 0; i0 < n_in; i0 += SW_THREADS) {
+      const int i = i0 + tid;
+      const uint64_t v = i < n_in ? key_at(i) : kKeyPad;
+      const bool keep = v != kKeyPad && v <= lim;
+      const uint32_t bal = __ballot_sync(FULL, keep);
+      int base = 0;
+      if (lane == 0 && bal) base = atomicAdd(&s_nout, __popc(bal));
+      base = __shfl_sync(FULL, base, 0);
+      if (keep) fin[base + __popc(bal & lt_mask)] = v;
+    }
+    __syncthreads();
+    nf = s_nout;
+    if (nf <= 128) {  // k <= SW_KMAX: one warp sorts in registers, no block barriers
+      if (warp == 0) warp_sort128(fin, nf);
+      __syncthreads();
+    } else {
+      const uint32_t np2 = next_pow2((uint32_t)max(nf, 1));
+      for (uint32_t i = nf + tid; i < np2; i += SW_THREADS) fin[i] = kKeyPad;
+      __syncthreads();
+      bitonic_sort_keys(fin, np2);
+    }
+  }
+  for (int i = tid; i < k; i += SW_THREADS) {
+    int32_t id = -1;
+    float dv = __int_as_float(0x7f800000);
+    if (i < nf) {
+      const uint64_t key = fin[i];
+      id = (int32_t)(uint32_t)key;
+      dv = key_f32((uint32_t)(key >> 32));
+    }
+    a.out_ids[(int64_t)b * k + i] = id;
+    a.out_d[(int64_t)b * k + i] = dv;
+  }
+}
+
 // FULLK: every scanned key to full_keys (mode 1), else top-k (mode 0)
 template <int M, int U, bool CPA, bool XL, bool FULLK>
 __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
@@ -667,116 +791,226 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
   __syncthreads();
   // every warp's bound holds >= k entries: entries above the smallest bound
   // are out; ids are loaded only for the survivors
-  uint64_t T = s_thr64;
-  {  // the quota bound (warp_cut) holds as well
-    uint32_t qb = 0;
-#pragma unroll
-    for (int w = 0; w < SW_WARPS; ++w) qb = max(qb, s_tw[w]);
-    const uint64_t tq = ((uint64_t)qb << 32) | 0xffffffffull;
-    T = T < tq ? T : tq;
-  }
+  scan_final(a, b, k, wb, cnt, dsm, merge, reinterpret_cast<uint32_t*>(sstart), &s_thr64, s_tw,
+             s_wcnt, s_sel, &s_nout);
+}
+
+// ---------------------------------------------------------------- lean
+// k_scan_lean: the default top-k scan for M in {8, 16} (interleaved LUT,
+// prebuilt LUTs, local rows < 2^32).  Same arithmetic, candidate buffers,
+// bounds and final merge as k_scan_warp; what goes is the block-wide
+// segment window (staging + two block barriers per 256 segments, ~25 % of
+// the stall samples at configs[2]'s 15-row segments):
+//  * every warp sums the query's segment lengths itself (coalesced, from L2)
+//    and takes positions [tot w / 8, tot (w + 1) / 8);
+//  * the warp's segment window lives in registers: lane j holds segment
+//    ws + j (row offset and base); a batch maps lanes to segments with one
+//    ballot (segments ending at or before the batch) and one redux.or
+//    (segment ends inside it), then two shuffles fetch row and base;
+//  * the window re-anchors (one coalesced load of 32 work items and a warp
+//    scan) only when a batch runs past its last segment.
+template <int M, int D>
+__global__ void __launch_bounds__(SW_THREADS, 3) k_scan_lean(ScanArgs a) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const IndexView& ix = a.ix;
+  float* lut = reinterpret_cast<float*>(dsm + SW_LUT);
+  lut += ((128u - (smem_u32(lut) & 127u)) & 127u) / 4u;  // 128-byte aligned
+  float* ctab = reinterpret_cast<float*>(dsm + SW_CTAB);
+  uint64_t* merge = reinterpret_cast<uint64_t*>(dsm + SW_MERGE);
+  __shared__ unsigned long long s_thr64;
+  __shared__ int s_nout;
+  __shared__ int s_wcnt[SW_WARPS];
+  __shared__ uint32_t s_sel[4];
+  __shared__ __align__(16) uint32_t s_tw[SW_WARPS];
+  static_assert(M == 8 || M == 16, "interleaved LUT");
+
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  const int k = a.k;
   {
-    // every id load of the warp in flight at once (cnt <= SW_WB)
-    constexpr int R = SW_WB / 32;
-    uint64_t vr[R];
+    // prebuilt [m][256] -> interleaved copies (as in k_scan_warp)
+    constexpr int NC = 32 / M;
+    const float4* src = reinterpret_cast<const float4*>(a.luts + (int64_t)b * M * 256);
+    const int m = lane % M, sub = lane / M;
+    constexpr int IT = M * 64 / 32 / SW_WARPS;
+    float4 v[IT];
 #pragma unroll
-    for (int j = 0; j < R; ++j) {
-      const int i = j * 32 + lane;
-      uint64_t v = i < cnt ? wb[i] : kKeyPad;
-      if (i < cnt && (v >> 32) <= (T >> 32))
-        v = (v & 0xffffffff00000000ull) | (uint32_t)__ldg(ix.pids + (uint32_t)v);
-      else
-        v = kKeyPad;
-      vr[j] = v;
-    }
-    int out = 0;
+    for (int it = 0; it < IT; ++it) v[it] = __ldg(src + m * 64 + NC * (warp + it * SW_WARPS) + sub);
+    const float cv = ix.ctab[tid];
 #pragma unroll
-    for (int j = 0; j < R; ++j) {
-      const bool keep = vr[j] <= T;
-      const uint32_t bal = __ballot_sync(FULL, keep);
-      if (keep) wb[out + __popc(bal & lt_mask)] = vr[j];
-      out += __popc(bal);
-    }
-    if (lane == 0) s_wcnt[warp] = out;
-  }
-  __syncthreads();
-  uint64_t* const all = reinterpret_cast<uint64_t*>(dsm + SW_WBUF);
-  auto slot_key = [&](int i) -> uint64_t {  // slot i of the warps' buffers
-    return (i % SW_WB) < s_wcnt[i / SW_WB] ? all[i] : kKeyPad;
-  };
-  int nm = 0, myoff = 0;
-  for (int w = 0; w < SW_WARPS; ++w) {
-    if (w == warp) myoff = nm;
-    nm += s_wcnt[w];
-  }
-  // usually the survivors fit the merge area: gather them there so the
-  // selection below touches nm entries, not every buffer slot
-  const bool compact = nm <= SW_WARPS * SW_KMAX;
-  if (compact) {
-    for (int i = lane; i < s_wcnt[warp]; i += 32) merge[myoff + i] = wb[i];
-    __syncthreads();
-  }
-  auto key_at = [&](int i) -> uint64_t { return compact ? merge[i] : slot_key(i); };
-  const int n_in = compact ? nm : SW_WARPS * SW_WB;
-  uint64_t* fin = compact ? all : merge;
-  int nf = 0;
-  if (compact && nm <= 128) {  // few survivors: sort them all, keep the first k
-    if (warp == 0) warp_sort128(merge, nm);
-    __syncthreads();
-    fin = merge;
-    nf = min(nm, k);
-  } else {
-    uint64_t lim = kKeyPad;
-    if (nm > k) {
-      uint32_t* bh = reinterpret_cast<uint32_t*>(sstart);  // free after the sweeps
-      uint32_t need = (uint32_t)k, eq = 0;
-      const uint32_t kd = block_select(n_in, [&](int i) { return (uint32_t)(key_at(i) >> 32); },
-                                       bh, s_sel, &need, &eq);
-      uint32_t kp = 0xffffffffu;
-      if (eq != need) {
-        uint32_t eq2;
-        kp = block_select(n_in, [&](int i) {
-          const uint64_t v = key_at(i);
-          return (uint32_t)(v >> 32) == kd ? (uint32_t)v : 0xffffffffu;
-        }, bh, s_sel, &need, &eq2);
+    for (int it = 0; it < IT; ++it) {
+      const int chunk = NC * (warp + it * SW_WARPS) + sub;
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) {
+        float* dst = lut + (4 * chunk) * 32 + (cc ^ sub) * M + m;
+        dst[0] = v[it].x; dst[32] = v[it].y; dst[64] = v[it].z; dst[96] = v[it].w;
       }
-      lim = ((uint64_t)kd << 32) | kp;
     }
-    if (tid == 0) s_nout = 0;
-    __syncthreads();
-    for (int i0 = 0; i0 < n_in; i0 += SW_THREADS) {
-      const int i = i0 + tid;
-      const uint64_t v = i < n_in ? key_at(i) : kKeyPad;
-      const bool keep = v != kKeyPad && v <= lim;
-      const uint32_t bal = __ballot_sync(FULL, keep);
-      int base = 0;
-      if (lane == 0 && bal) base = atomicAdd(&s_nout, __popc(bal));
-      base = __shfl_sync(FULL, base, 0);
-      if (keep) fin[base + __popc(bal & lt_mask)] = v;
-    }
-    __syncthreads();
-    nf = s_nout;
-    if (nf <= 128) {  // k <= SW_KMAX: one warp sorts in registers, no block barriers
-      if (warp == 0) warp_sort128(fin, nf);
-      __syncthreads();
-    } else {
-      const uint32_t np2 = next_pow2((uint32_t)max(nf, 1));
-      for (uint32_t i = nf + tid; i < np2; i += SW_THREADS) fin[i] = kKeyPad;
-      __syncthreads();
-      bitonic_sort_keys(fin, np2);
-    }
+    ctab[tid] = cv;
   }
-  for (int i = tid; i < k; i += SW_THREADS) {
-    int32_t id = -1;
-    float dv = __int_as_float(0x7f800000);
-    if (i < nf) {
-      const uint64_t key = fin[i];
-      id = (int32_t)(uint32_t)key;
-      dv = key_f32((uint32_t)(key >> 32));
+  if (tid == 0) s_thr64 = kKeyPad;
+  if (tid < SW_WARPS) s_tw[tid] = 0xffffffffu;
+  const int k8 = (k + SW_WARPS - 1) / SW_WARPS;
+  uint64_t* wb = reinterpret_cast<uint64_t*>(dsm + SW_WBUF) + warp * SW_WB;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(merge) + warp * 256;
+  int cnt = 0;
+  uint32_t thr = 0xffffffffu;
+  uint64_t thr64 = kKeyPad;
+  auto f_of = [](uint32_t t) -> float {
+    const float f = key_f32(t);
+    return isnan(f) ? __int_as_float(0x7f800000) : f;
+  };
+  float thr_f = f_of(thr);
+  auto shrink = [&](int room) {
+    if (!warp_cut(wb, &cnt, &thr, &thr64, hist, k, room, &s_thr64, &s_tw[warp], k8))
+      warp_shrink(wb, &cnt, &thr, &thr64, hist, ix.pids, k, &s_thr64);
+  };
+  const WorkItem* W = a.work + (int64_t)b * a.cap_w;
+  const int nseg = a.nwork[b];
+  __syncthreads();  // LUT, constants and bounds ready
+
+  // ---- this warp's positions
+  int tot = 0;
+  for (int i = lane; i < nseg; i += 32) tot += __ldg(&W[i].len);
+  tot = __reduce_add_sync(FULL, tot);
+  const int pb = (int)((int64_t)tot * warp / SW_WARPS);
+  const int pe = (int)((int64_t)tot * (warp + 1) / SW_WARPS);
+  if (pb < pe) {
+    // register window: lane j = segment ws + j; wend = its end position,
+    // wadj = first row - first position (row of position p = wadj + p)
+    int ws = 0, wend = 0, wlast = 0;
+    uint32_t wadj = 0;
+    double wbase = 0.0;
+    auto fill = [&](int s0, int off0) {
+      const int i = s0 + lane;
+      int ln = 0;
+      uint32_t st = 0;
+      double bs = 0.0;
+      if (i < nseg) {
+        st = (uint32_t)__ldg(&W[i].start);
+        ln = __ldg(&W[i].len);
+        bs = __ldg(&W[i].base);
+      }
+      int incl = ln;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+      }
+      wend = off0 + incl;
+      wadj = st - (uint32_t)(wend - ln);
+      wbase = bs;
+      ws = s0;
+      wlast = __shfl_sync(FULL, wend, 31);
+    };
+    // the window starting at the segment that holds position p (inside or
+    // past the current window)
+    auto anchor = [&](int p) {
+      while (wlast <= p) fill(ws + 32, wlast);
+      const int sl = __popc(__ballot_sync(FULL, wend <= p));
+      if (sl > 0) fill(ws + sl, __shfl_sync(FULL, wend, sl - 1));
+    };
+    fill(0, 0);
+    anchor(pb);
+
+    struct Slot {
+      uint32_t row;
+      double base;
+      bool ok;
+    };
+    uint8_t* ring = dsm + sw_ring(M, true) + (size_t)warp * D * sw_slot(M);
+    const int xl_x = lane % M;
+    const uint32_t xl_base = smem_u32(lut) + (uint32_t)((lane / M) * M + xl_x) * 4u;
+    uint32_t xl_sel[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) xl_sel[j] = 0x4440u | (uint32_t)(j ^ (xl_x & 3));
+    uint32_t xl_bs[M];  // per-step lane addresses (code_sum_xlb)
+#pragma unroll
+    for (int s = 0; s < M; ++s) xl_bs[s] = xl_base ^ ((uint32_t)s << 2);
+
+    // batch p0 .. p0 + 31 -> (row, base) per lane; code row + constant-byte
+    // word issued by cp.async into ring slot `slot` (one commit group)
+    auto map = [&](int p0, Slot& sl, int slot) {
+      if (p0 < pe) {
+        if (wlast < min(p0 + 32, pe)) anchor(p0);
+        const int before = __popc(__ballot_sync(FULL, wend <= p0));
+        const int rel = wend - p0;
+        const uint32_t bit = (rel >= 1 && rel <= 31) ? (1u << rel) : 0u;
+        const uint32_t starts = __reduce_or_sync(FULL, bit);
+        const int p = p0 + lane;
+        sl.ok = p < pe;
+        // lanes past pe take the warp's last position (same row, no new sector)
+        const int pc = sl.ok ? p : pe - 1;
+        const int seg = before + __popc(starts & (FULL >> (31 - (pc - p0))));
+        sl.row = __shfl_sync(FULL, wadj, seg) + (uint32_t)pc;
+        sl.base = __shfl_sync(FULL, wbase, seg);
+        uint8_t* dst = ring + slot * sw_slot(M);
+        const uint8_t* src = ix.codes + (size_t)sl.row * M;
+        constexpr int CH = cp_chunk<M>();
+#pragma unroll
+        for (int c = 0; c < M / CH; ++c) cp_async<CH>(dst + lane * M + c * CH, src + c * CH);
+        cp_async<4>(dst + 32 * M + lane * 4, ix.cbytes + (sl.row & ~3u));
+      } else {
+        sl.ok = false;
+      }
+      cp_async_commit();
+    };
+    auto dist_of = [&](const Slot& cur, int slot) -> float {
+      const uint8_t* src = ring + slot * sw_slot(M);
+      const CodeVec<M> code = smem_code<M>(src + lane * M);
+      const uint32_t cw = reinterpret_cast<const uint32_t*>(src + 32 * M)[lane];
+      const uint32_t cb = __byte_perm(cw, 0, 0x4440u | (cur.row & 3u));
+      const float ip = code_sum_xlb<M>(code, xl_bs, xl_x, xl_sel);
+      return (float)dadd(dsub(cur.base, 2.0 * (double)ip), (double)ctab[cb]);
+    };
+    auto consider = [&](const Slot& cur, float dist) {
+      bool pass = cur.ok && dist <= thr_f;
+      if (pass && dist == thr_f && (uint32_t)thr64 != 0xffffffffu)
+        pass = (((uint64_t)f32_key(dist) << 32) | (uint32_t)__ldg(ix.pids + cur.row)) < thr64;
+      const uint32_t bal = __ballot_sync(FULL, pass);
+      if (bal) {
+        if (pass) wb[cnt + __popc(bal & lt_mask)] = ((uint64_t)f32_key(dist) << 32) | cur.row;
+        cnt += __popc(bal);
+      }
+    };
+    // D ring slots: D - 1 batches in flight while one is summed
+    Slot sl[D];
+#pragma unroll
+    for (int i = 0; i < D - 1; ++i) map(pb + 32 * i, sl[i], i);
+    for (int p0 = pb; p0 < pe; p0 += 32 * D) {
+      {  // adopt a tighter bound from the other warps
+        uint32_t q[8];
+        asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]) : "r"(smem_u32(&s_tw[0])));
+        asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(q[4]), "=r"(q[5]), "=r"(q[6]), "=r"(q[7]) : "r"(smem_u32(&s_tw[4])));
+        const uint32_t qb = max(max(max(q[0], q[1]), max(q[2], q[3])), max(max(q[4], q[5]), max(q[6], q[7])));
+        const uint64_t tq = ((uint64_t)qb << 32) | 0xffffffffull;
+        const uint64_t ts = *(volatile unsigned long long*)&s_thr64;
+        const uint64_t t = ts < tq ? ts : tq;
+        if (t < thr64) { thr64 = t; thr = (uint32_t)(t >> 32); thr_f = f_of(thr); }
+      }
+#pragma unroll
+      for (int h = 0; h < D; ++h) {
+        const int nx = (h + D - 1) % D;
+        map(p0 + 32 * (h + D - 1), sl[nx], nx);
+        cp_async_wait<D - 1>();  // this batch's group landed
+        const float dv = dist_of(sl[h], h);
+        consider(sl[h], dv);
+      }
+      if (cnt > SW_WB - 32 * D) {
+        __syncwarp();
+        shrink(SW_WB / 2);
+        thr_f = f_of(thr);
+      }
     }
-    a.out_ids[(int64_t)b * k + i] = id;
-    a.out_d[(int64_t)b * k + i] = dv;
+    cp_async_wait<0>();
   }
+  __syncwarp();
+  if (cnt > k) shrink(k + 32);
+  __syncthreads();
+  scan_final(a, b, k, wb, cnt, dsm, merge, reinterpret_cast<uint32_t*>(dsm + SW_SSTART), &s_thr64,
+             s_tw, s_wcnt, s_sel, &s_nout);
 }
 
 // LUTs of QB queries for one sub-quantizer m per CTA (grid (ceil(nq/QB), M)):
@@ -877,10 +1111,30 @@ static bool scan_xl() {
   return x;
 }
 
+// GIVF_SCAN=warp keeps k_scan_warp's block-wide segment windows
+static bool scan_lean() {
+  static bool x = [] {
+    const char* e = getenv("GIVF_SCAN");
+    return !(e && strcmp(e, "warp") == 0);
+  }();
+  return x;
+}
+
 template <int M, int U, bool CPA>
 static void launch_warp_md(const ScanArgs& a, cudaStream_t s) {
   if constexpr (M == 8 || M == 16) {
-    if (a.luts && a.mode == 0 && scan_xl()) { launch_warp_mdx<M, U, CPA, true>(a, s); return; }
+    if (a.luts && a.mode == 0 && scan_xl()) {
+      if (scan_lean()) {
+        // two ring slots: deeper rings (3, 4) cost a CTA per SM of shared
+        // memory and measured slower (configs[2] shape: 1.20 -> 1.60 / 1.85 ms)
+        const size_t bytes = sw_bytes(M, 2, true, true, a.ix.d);
+        ensure_max_smem((const void*)k_scan_lean<M, 2>, bytes);
+        k_scan_lean<M, 2><<<a.nq, SW_THREADS, bytes, s>>>(a);
+        return;
+      }
+      launch_warp_mdx<M, U, CPA, true>(a, s);
+      return;
+    }
   }
   launch_warp_mdx<M, U, CPA, false>(a, s);
 }

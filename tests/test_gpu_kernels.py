@@ -103,6 +103,7 @@ def default_mode_result():
     {"GIVF_PROBE": "simt"},                        # SIMT fp32 probe GEMM
     {"GIVF_CHUNK_QUERIES": "3"},                   # many small chunks (arena reuse)
     {"GIVF_SCAN_LUT": "plain"},                    # warp scan, [m][256] LUT (bank conflicts)
+    {"GIVF_SCAN": "warp"},                         # block-wide segment windows (k_scan_warp)
     {"GIVF_GEMM_SPLIT": "3"},                      # probe GEMM work units: 3 slices per m-block
     {"GIVF_RS_SPLIT": "5"},                        # K4b: 5 CTAs per query
     {"GIVF_PROBE": "fused"},                       # fused probe, 2 x 128 queries x 128 centroids
