@@ -22,6 +22,14 @@
  *                        ef_search == K, i.e. the exact region ranking.
  *   givf_merge_topk      no reference counterpart (single process): merge
  *                        of per-shard top-k lists, SURVEY §8e.
+ *   givf_plan            search.py:77-139 alone (probe, group scores,
+ *                        prune, budget walk) for a share of the queries,
+ *                        emitting each query's begun groups in their global
+ *                        form -- the query-sharded planning step of the
+ *                        list-sharded layout.
+ *   givf_search_planned  search.py:138-158 (scan + rerank, top-k) of plans
+ *                        made by givf_plan on any rank, over the rows this
+ *                        shard holds.
  *
  * Status codes: GIVF_OK, GIVF_EINVAL (bad argument: givf_last_error() holds
  * the reference's ValueError text, e.g. "need 1 <= nprobe <= 48, got 0"),
@@ -140,6 +148,35 @@ int givf_probe(givf_index_t index, const float* queries, int64_t nq, int32_t npr
 /* K7: merge shard lists ids/dists (shards, nq, k) -> (nq, k) by (dist, id). */
 int givf_merge_topk(const int32_t* ids, const float* dists, int32_t shards, int64_t nq,
                     int32_t k, int32_t* out_ids, float* out_dists, int device, void* stream);
+
+/* Query-sharded planning.  One record per begun group of a
+ * query's plan, in its global form: the group's index region * groups +
+ * group (replaces index.py:80-85 group_starts, which is per shard), the
+ * number of its rows to scan (search.py:131-139 lengths, global), and the
+ * float64 base (1 - a) qc2 + a qs2 (search.py:115-121). */
+typedef struct givf_plan_item {
+  int32_t group;
+  int32_t len;
+  double base;
+} givf_plan_item;
+
+/* Per-query capacity (records) givf_plan needs: min(ceil(tau P L), candidates). */
+int givf_plan_capacity(givf_index_t index, const givf_search_params* params, int64_t* cap);
+
+/* Plans of nq queries from this index's replicated tables (any shard of a
+ * sharded index gives the same plans): items (nq, cap) givf_plan_item,
+ * nitems (nq) records used, stats (nq) the global SearchStats. */
+int givf_plan(givf_index_t index, const float* queries, int64_t nq,
+              const givf_search_params* params, int64_t cap, void* items, int32_t* nitems,
+              givf_search_stats* stats, void* stream);
+
+/* Top-k of nq queries from their plans (CSR on the device: offsets (nq + 1)
+ * into items), scanning this shard's rows of every planned group:
+ * clip(len - lo, 0, cnt) rows of the slice this shard holds.  ids / dists
+ * (nq, k) as givf_search_topk; merge the shards' lists with givf_merge_topk. */
+int givf_search_planned(givf_index_t index, const float* queries, int64_t nq,
+                        const givf_search_params* params, const int64_t* offsets,
+                        const void* items, int32_t k, int32_t* ids, float* dists, void* stream);
 
 /* Count of kernels this library has launched in the calling process. */
 int64_t givf_kernel_launches(void);

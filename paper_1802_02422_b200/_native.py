@@ -27,6 +27,9 @@ EXPORTS = (
     "givf_probe_scores",
     "givf_probe",
     "givf_merge_topk",
+    "givf_plan_capacity",
+    "givf_plan",
+    "givf_search_planned",
     "givf_kernel_launches",
     "givf_profile_enable",
     "givf_profile_read",
@@ -114,6 +117,12 @@ class EncodeDesc(ctypes.Structure):
     ]
 
 
+class PlanItemC(ctypes.Structure):
+    """givf_plan_item: one begun group of a plan in its global form."""
+
+    _fields_ = [("group", ctypes.c_int32), ("len", ctypes.c_int32), ("base", ctypes.c_double)]
+
+
 _lib = None
 
 
@@ -141,6 +150,10 @@ def load(path: str = LIB_PATH):
     lib.givf_probe.argtypes = [vp, vp, i64, i32, vp, vp, vp]
     lib.givf_probe_scores.argtypes = [vp, vp, i64, vp, vp, vp]
     lib.givf_merge_topk.argtypes = [vp, vp, i32, i64, i32, vp, vp, ctypes.c_int, vp]
+    lib.givf_plan_capacity.argtypes = [vp, ctypes.POINTER(SearchParamsC), ctypes.POINTER(i64)]
+    lib.givf_plan.argtypes = [vp, vp, i64, ctypes.POINTER(SearchParamsC), i64, vp, vp, vp, vp]
+    lib.givf_search_planned.argtypes = [vp, vp, i64, ctypes.POINTER(SearchParamsC), vp, vp, i32,
+                                        vp, vp, vp]
     lib.givf_kernel_launches.restype = i64
     lib.givf_profile_enable.argtypes = [ctypes.c_int]
     lib.givf_profile_read.argtypes = [vp, vp, i32]

@@ -542,14 +542,23 @@ int build_plan(givf_index* ix, const givf_search_params* p, Plan* pl) {
   return GIVF_OK;
 }
 
-enum OutMode { OUT_TOPK = 0, OUT_FULL = 1 };
+enum OutMode { OUT_TOPK = 0, OUT_FULL = 1, OUT_PLAN = 2 };
+
+// OUT_PLAN (givf_plan): the planner's global work lists, no scan
+struct PlanOut {
+  PlanItem* items;  // (nq, cap)
+  int32_t* nitems;  // (nq)
+  int64_t cap;
+};
 
 int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_search_params* p,
                OutMode om, int64_t width, int32_t* ids, float* dists, givf_search_stats* stats,
-               void* stream) {
+               void* stream, const PlanOut* po = nullptr) {
   Plan pl;
   int rc = build_plan(ix, p, &pl);
   if (rc) return rc;
+  if (om == OUT_PLAN && (!po || !po->items || !po->nitems || po->cap < pl.cap_w))
+    return fail(GIVF_EINVAL, "plan output capacity must be >= givf_plan_capacity()");
   if (om == OUT_TOPK && (width < 1 || width > 4096))
     return fail(GIVF_EINVAL, "need 1 <= k <= 4096");
   if (om == OUT_FULL) {
@@ -559,7 +568,8 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
       return fail(GIVF_EINVAL, "capacity must be >= min(candidates, n)");
   }
   if (nq == 0) return GIVF_OK;
-  if (!queries || !ids || !dists || !stats) return fail(GIVF_EINVAL, "null output pointer");
+  if (!queries || !stats || (om != OUT_PLAN && (!ids || !dists)))
+    return fail(GIVF_EINVAL, "null output pointer");
 
   std::lock_guard<std::mutex> lock(ix->mu);
   CUDA_TRY(cudaSetDevice(ix->device));
@@ -570,10 +580,13 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
   int32_t* const ids_w = kernel_writable(ids);
   float* const dists_w = kernel_writable(dists);
   int64_t* const stats_w = reinterpret_cast<int64_t*>(kernel_writable(stats));
-  const bool out_dev = ids_w && dists_w;
+  const bool out_dev = om == OUT_PLAN || (ids_w && dists_w);
   const bool st_dev = stats_w != nullptr;
   // results in host memory: the call returns once they have landed
-  const bool host_out = !(is_device_ptr(ids) && is_device_ptr(dists) && is_device_ptr(stats));
+  const bool host_out = om == OUT_PLAN
+      ? !(is_device_ptr(po->items) && is_device_ptr(po->nitems) && is_device_ptr(stats))
+      : !(is_device_ptr(ids) && is_device_ptr(dists) && is_device_ptr(stats));
+  const bool plan_dev = om == OUT_PLAN && is_device_ptr(po->items) && is_device_ptr(po->nitems);
   const bool rerank = p->rerank != 0;
   const int64_t full_p2 = om == OUT_FULL ? (int64_t)next_pow2_host((uint32_t)std::max<int64_t>(width, 1)) : 0;
 
@@ -589,6 +602,7 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
   }
   if (om == OUT_FULL && rerank) per_q += (size_t)full_p2 * 8;
   if (!out_dev) per_q += (size_t)width * 8 + 512;
+  if (om == OUT_PLAN && !plan_dev) per_q += (size_t)po->cap * sizeof(PlanItem) + 64;
   per_q += aligned_bytes<float>((size_t)v.M * 256);  // prebuilt LUTs
   per_q += probe_q;
   const size_t fixed = probe_fixed_bytes(pl) + (1 << 16);
@@ -635,7 +649,7 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
       la.ix = v;
       la.mode = om == OUT_TOPK ? 0 : 1;
       la.k = (int)(om == OUT_TOPK ? width : 0);
-      if (om == OUT_TOPK && scan_warp_ok(la)) {
+      if (om == OUT_TOPK && scan_warp_ok(la)) {  // (OUT_PLAN: no LUTs)
         luts = ar.take<float>((size_t)bq * v.M * 256);
         CUDA_TRY(ix->ensure_side());
       }
@@ -678,6 +692,7 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
     pa.ldD = v.K;
     pa.cmax = v.cmax;
     pa.half_rel = (float)kHalfRel;
+    pa.global_items = om == OUT_PLAN ? 1 : 0;
     pa.only = ar.take<int>(bq);
     ARENA_CHECK(ar);
     // the approximate planner's keys alias the exact scratch, which the exact
@@ -721,6 +736,25 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
     staged(ST_PLAN, st, [&] { nk = launch_plan(pa, st); }, 0);
     g_launches += nk;
     KCHECK();
+
+    if (om == OUT_PLAN) {
+      PlanItem* pi = plan_dev ? po->items + q0 * po->cap : ar.take<PlanItem>((size_t)bq * po->cap);
+      int32_t* pn = plan_dev ? po->nitems + q0 : ar.take<int32_t>(bq);
+      ARENA_CHECK(ar);
+      staged(ST_FINISH, st, [&] {
+        launch_items_from_work(pa.work, pl.cap_w, pa.nwork, bq, pi, po->cap, pn, st);
+      });
+      KCHECK();
+      if (!plan_dev) {
+        CUDA_TRY(cudaMemcpyAsync(po->items + q0 * po->cap, pi, sizeof(PlanItem) * bq * po->cap,
+                                 cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(po->nitems + q0, pn, sizeof(int32_t) * bq, cudaMemcpyDeviceToHost, st));
+      }
+      if (!st_dev)
+        CUDA_TRY(cudaMemcpyAsync(stats + q0, dstats, sizeof(int64_t) * 4 * bq,
+                                 cudaMemcpyDeviceToHost, st));
+      continue;
+    }
 
     int32_t* oid;
     float* od;
@@ -1036,6 +1070,113 @@ int givf_search_full(givf_index_t ix, const float* queries, int64_t nq,
                      float* dists, givf_search_stats* stats, void* stream) {
   if (!ix || !params) return fail(GIVF_EINVAL, "null argument");
   return run_search(ix, queries, nq, params, OUT_FULL, capacity, ids, dists, stats, stream);
+}
+
+int givf_plan_capacity(givf_index_t ix, const givf_search_params* params, int64_t* cap) {
+  if (!ix || !params || !cap) return fail(GIVF_EINVAL, "null argument");
+  Plan pl;
+  int rc = build_plan(ix, params, &pl);
+  if (rc) return rc;
+  *cap = pl.cap_w;
+  return GIVF_OK;
+}
+
+int givf_plan(givf_index_t ix, const float* queries, int64_t nq, const givf_search_params* params,
+              int64_t cap, void* items, int32_t* nitems, givf_search_stats* stats, void* stream) {
+  if (!ix || !params) return fail(GIVF_EINVAL, "null argument");
+  static_assert(sizeof(PlanItem) == sizeof(givf_plan_item), "plan item layout");
+  PlanOut po{reinterpret_cast<PlanItem*>(items), nitems, cap};
+  return run_search(ix, queries, nq, params, OUT_PLAN, 0, nullptr, nullptr, stats, stream, &po);
+}
+
+int givf_search_planned(givf_index_t ix, const float* queries, int64_t nq,
+                        const givf_search_params* params, const int64_t* offsets, const void* items,
+                        int32_t k, int32_t* ids, float* dists, void* stream) {
+  if (!ix || !params) return fail(GIVF_EINVAL, "null argument");
+  Plan pl;
+  int rc = build_plan(ix, params, &pl);
+  if (rc) return rc;
+  if (k < 1 || k > 4096) return fail(GIVF_EINVAL, "need 1 <= k <= 4096");
+  if (nq == 0) return GIVF_OK;
+  if (!queries || !offsets || !items || !ids || !dists) return fail(GIVF_EINVAL, "null argument");
+  if (!is_device_ptr(offsets) || !is_device_ptr(items))
+    return fail(GIVF_EINVAL, "planned search expects device offsets / items");
+  std::lock_guard<std::mutex> lock(ix->mu);
+  CUDA_TRY(cudaSetDevice(ix->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const IndexView& v = ix->v;
+  const bool q_dev = is_device_ptr(queries);
+  int32_t* const ids_w = kernel_writable(ids);
+  float* const dists_w = kernel_writable(dists);
+  const bool out_dev = ids_w && dists_w;
+  const bool host_out = !(is_device_ptr(ids) && is_device_ptr(dists));
+  size_t per_q = aligned_bytes<float>(v.d) + aligned_bytes<WorkItem>(pl.cap_w) +
+                 aligned_bytes<int>(1) + aligned_bytes<float>((size_t)v.M * 256) + 256;
+  if (!out_dev) per_q += (size_t)k * 8 + 512;
+  const size_t budget = workspace_budget();
+  int64_t chunk = std::max<int64_t>(1, std::min<int64_t>({nq, 65535, (int64_t)(budget / per_q)}));
+  chunk = (nq + (nq + chunk - 1) / chunk - 1) / ((nq + chunk - 1) / chunk);
+  const size_t slice = ((per_q * (size_t)chunk + (1 << 20)) + 4095) & ~(size_t)4095;
+  CUDA_TRY(ix->arena.reserve(slice));
+  for (int64_t q0 = 0; q0 < nq; q0 += chunk) {
+    const int bq = (int)std::min<int64_t>(chunk, nq - q0);
+    Arena ar;
+    ar.base = ix->arena.base;
+    ar.cap = slice;
+    ar.reset();
+    const float* dQ;
+    if (q_dev) {
+      dQ = queries + q0 * v.d;
+    } else {
+      float* tmp = ar.take<float>((size_t)bq * v.d);
+      ARENA_CHECK(ar);
+      CUDA_TRY(cudaMemcpyAsync(tmp, queries + q0 * v.d, sizeof(float) * bq * v.d,
+                               cudaMemcpyHostToDevice, st));
+      dQ = tmp;
+    }
+    WorkItem* work = ar.take<WorkItem>((size_t)bq * pl.cap_w);
+    int* nwork = ar.take<int>(bq);
+    float* luts = ar.take<float>((size_t)bq * v.M * 256);
+    ARENA_CHECK(ar);
+    staged(ST_PLAN, st, [&] {
+      launch_localize(v, offsets + q0, reinterpret_cast<const PlanItem*>(items), bq, work, pl.cap_w,
+                      nwork, st);
+    });
+    staged(ST_LUT, st, [&] { launch_build_luts(v, dQ, bq, luts, st); });
+    KCHECK();
+    int32_t* oid;
+    float* od;
+    if (out_dev) {
+      oid = ids_w + q0 * k;
+      od = dists_w + q0 * k;
+    } else {
+      oid = ar.take<int32_t>((size_t)bq * k);
+      od = ar.take<float>((size_t)bq * k);
+      ARENA_CHECK(ar);
+    }
+    ScanArgs sa{};
+    sa.ix = v;
+    sa.Q = dQ;
+    sa.nq = bq;
+    sa.work = work;
+    sa.cap_w = pl.cap_w;
+    sa.nwork = nwork;
+    sa.mode = 0;
+    sa.k = k;
+    sa.out_ids = oid;
+    sa.out_d = od;
+    sa.luts = luts;
+    staged(ST_SCAN, st, [&] {
+      if (!launch_scan_warp(sa, st)) launch_scan(sa, st);
+    });
+    KCHECK();
+    if (!out_dev) {
+      CUDA_TRY(cudaMemcpyAsync(ids + q0 * k, oid, sizeof(int32_t) * bq * k, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaMemcpyAsync(dists + q0 * k, od, sizeof(float) * bq * k, cudaMemcpyDeviceToHost, st));
+    }
+  }
+  if (host_out || !q_dev) CUDA_TRY(cudaStreamSynchronize(st));
+  return GIVF_OK;
 }
 
 int givf_probe_scores(givf_index_t ix, const float* queries, int64_t nq, float* scores,

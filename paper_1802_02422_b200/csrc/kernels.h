@@ -159,6 +159,9 @@ struct PlanArgs {
   // relative storage error of the approximate qs2 (kHalfRel for D, 0 here)
   int direct;
   float half_rel;
+  // query-sharded planning: emit whole groups (start = global group index
+  // region * G + group, len = global length) instead of this shard's rows
+  int global_items;
   int approx;           // akey holds K3a's keys: run the approximate-first planner
 };
 // plan_approx.cu: K3a, the approximate group scores (needs D; may run per
@@ -170,6 +173,20 @@ int launch_plan_approx(const PlanArgs& a, cudaStream_t s);
 // run) followed by the exact planner for the queries it could not certify;
 // returns kernels launched.
 int launch_plan(const PlanArgs& a, cudaStream_t s);
+
+// plan_exchange.cu: plans made on another rank (query-sharded planning,
+// SURVEY §8e) as 16-byte records, localized to this shard's rows
+struct PlanItem {
+  int32_t group;  // region * G + group (global)
+  int32_t len;    // rows of the group to scan (global)
+  double base;    // (1 - a) qc2 + a qs2
+};
+// work items (start = global group) -> plan items; nq x cap, counts in nwork
+void launch_items_from_work(const WorkItem* work, int64_t cap_w, const int* nwork, int nq,
+                            PlanItem* items, int64_t cap, int* nitems, cudaStream_t s);
+// CSR plan items -> this shard's work items (empty slices dropped)
+void launch_localize(const IndexView& ix, const int64_t* offsets, const PlanItem* items, int nq,
+                     WorkItem* work, int64_t cap_w, int* nwork, cudaStream_t s);
 
 // scan.cu
 struct ScanArgs {

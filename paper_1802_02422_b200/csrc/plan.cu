@@ -294,14 +294,14 @@ __device__ void plan_select_one(const PlanArgs& a, const int b) {
   auto emit = [&](int64_t f, int64_t len_g) {
     int p = (int)(f / G), j = (int)(f % G);
     int64_t gi = (int64_t)reg[p] * G + j;
-    int64_t lo_ = ix.llo ? ix.llo[gi] : 0;
-    int64_t cnt_ = ix.lsize ? ix.lsize[gi] : ix.gsize[gi];
+    int64_t lo_ = (ix.llo && !a.global_items) ? ix.llo[gi] : 0;
+    int64_t cnt_ = a.global_items ? len_g : (ix.lsize ? ix.lsize[gi] : ix.gsize[gi]);
     int64_t ll = min(max(len_g - lo_, (int64_t)0), cnt_);
     if (ll <= 0) return;
     int pos = atomicAdd(&s_nemit, 1);
     if (pos >= a.cap_w) return;  // cannot happen: cap_w bounds the begun items
     WorkItem w;
-    w.start = ix.lstart[gi];
+    w.start = a.global_items ? gi : ix.lstart[gi];
     w.len = (int32_t)ll;
     w.flat = (int32_t)f;
     w.base = sbase[f];

@@ -624,9 +624,11 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
     float nrm = 0.f;
     if (valid) {  // independent loads, issued together
       const int64_t gi = GI(f);
-      const int64_t lo_ = ix.llo ? ix.llo[gi] : 0;
-      const int64_t cnt_ = ix.lsize ? ix.lsize[gi] : ix.gsize[gi];
-      start = ix.lstart[gi];
+      // global_items (query-sharded planning): the whole group,
+      // identified by its global index, for every shard to localize
+      const int64_t lo_ = (ix.llo && !a.global_items) ? ix.llo[gi] : 0;
+      const int64_t cnt_ = a.global_items ? len_g : (ix.lsize ? ix.lsize[gi] : ix.gsize[gi]);
+      start = a.global_items ? gi : ix.lstart[gi];
       if (ix.grouping) {
         row = ix.nbr[gi];
         nrm = ix.norm[gi];

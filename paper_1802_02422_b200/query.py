@@ -105,7 +105,7 @@ def search_batch(index, queries, params: SearchParams, k: int | None = None, dev
     b = q.shape[0]
     if k is not None and out is not None:
         ids, dists, stats = out
-        assert ids.shape == (b, k) and dists.shape == (b, k) and stats.shape == (b, 4)
+        _check_out(ids, dists, stats, b, int(k))
         _native.check(lib.givf_search_topk(dev.handle, _vp(q), b, ctypes.byref(cp), int(k),
                                            _vp(ids), _vp(dists), _vp(stats), None))
         return ids, dists, stats
@@ -132,6 +132,26 @@ def search_batch(index, queries, params: SearchParams, k: int | None = None, dev
     return out
 
 
+def _check_out(ids, dists, stats, b, k, device=None):
+    """Caller-owned outputs: right dtype, shape, C-contiguous, writable, and
+    (torch) on the index's device -- the kernels write them raw."""
+    want = ((ids, "ids", (b, k), "int32"), (dists, "dists", (b, k), "float32"),
+            (stats, "stats", (b, 4), "int64"))
+    for a, name, shape, dt in want:
+        if tuple(a.shape) != shape:
+            raise ValueError(f"out {name}: shape {tuple(a.shape)} != {shape}")
+        if str(a.dtype).replace("torch.", "") != dt:
+            raise ValueError(f"out {name}: dtype {a.dtype} != {dt}")
+        if hasattr(a, "is_contiguous"):
+            if not a.is_contiguous():
+                raise ValueError(f"out {name}: not contiguous")
+            if device is not None and a.is_cuda and a.device.index != device:
+                raise ValueError(f"out {name}: on cuda:{a.device.index}, index on cuda:{device}")
+        else:
+            if not a.flags.c_contiguous or not a.flags.writeable:
+                raise ValueError(f"out {name}: not C-contiguous and writable")
+
+
 def _is_torch_cuda(x) -> bool:
     mod = type(x).__module__
     return mod.startswith("torch") and getattr(x, "is_cuda", False)
@@ -148,8 +168,11 @@ def _search_batch_torch(dev, queries, cp, params, k, out=None):
     if q.shape[-1] != dev.dim:
         raise ValueError(f"query dim {q.shape[-1]} != index dim {dev.dim}")
     b = q.shape[0]
+    if q.device.index != dev.device:
+        raise ValueError(f"queries on cuda:{q.device.index}, index on cuda:{dev.device}")
     if out is not None:
         ids, dists, stats = out
+        _check_out(ids, dists, stats, b, int(k), dev.device)
     else:
         ids = torch.empty((b, int(k)), dtype=torch.int32, device=q.device)
         dists = torch.empty((b, int(k)), dtype=torch.float32, device=q.device)
@@ -209,6 +232,87 @@ def probe_scores(index, queries, device: int = 0):
     return out, float(eps.value)
 
 
+def plan_capacity(index, params: SearchParams, device: int = 0) -> int:
+    """Records per query givf_plan needs: min(ceil(tau * P * L), candidates)."""
+    dev = device_index(index, device)
+    cap = ctypes.c_int64(0)
+    _native.check(_native.load().givf_plan_capacity(dev.handle, ctypes.byref(_cparams(params)),
+                                                    ctypes.byref(cap)))
+    return int(cap.value)
+
+
+def plan_batch(index, queries, params: SearchParams, device: int = 0):
+    """The planning half of search() (search.py:77-139) for a share of the
+    queries, in the global form the list-sharded layout exchanges (SURVEY
+    §8e): CUDA tensors items (B, cap, 4) int32 = givf_plan_item records
+    (group, len, base as two words), nitems (B,) int32, stats (B, 4) int64."""
+    import torch
+
+    dev = device_index(index, device)
+    cp = _cparams(params)
+    cap = plan_capacity(dev, params)
+    if _is_torch_cuda(queries):
+        q = queries.contiguous().to(torch.float32)
+        qp = ctypes.c_void_p(q.data_ptr())
+    else:
+        q = np.ascontiguousarray(np.asarray(queries, dtype=np.float32))
+        qp = _vp(q)
+    if q.ndim == 1:
+        q = q[None, :]
+    if q.shape[-1] != dev.dim:
+        raise ValueError(f"query dim {q.shape[-1]} != index dim {dev.dim}")
+    b = q.shape[0]
+    cuda = torch.device("cuda", dev.device)
+    items = torch.empty((b, cap, 4), dtype=torch.int32, device=cuda)
+    nitems = torch.empty((b,), dtype=torch.int32, device=cuda)
+    stats = torch.empty((b, 4), dtype=torch.int64, device=cuda)
+    stream = torch.cuda.current_stream(cuda).cuda_stream
+    _native.check(_native.load().givf_plan(
+        dev.handle, qp, b, ctypes.byref(cp), cap, ctypes.c_void_p(items.data_ptr()),
+        ctypes.c_void_p(nitems.data_ptr()), ctypes.c_void_p(stats.data_ptr()),
+        ctypes.c_void_p(stream)))
+    return items, nitems, stats
+
+
+def compact_plans(items, nitems):
+    """(B, cap, 4) padded plans -> CSR: offsets (B + 1,) int64, flat (T, 4)."""
+    import torch
+
+    cap = items.shape[1]
+    mask = torch.arange(cap, device=items.device)[None, :] < nitems[:, None].to(torch.int64)
+    flat = items[mask].contiguous()
+    offsets = torch.zeros(items.shape[0] + 1, dtype=torch.int64, device=items.device)
+    offsets[1:] = torch.cumsum(nitems.to(torch.int64), 0)
+    return offsets, flat
+
+
+def search_planned(index, queries, params: SearchParams, offsets, items, k: int,
+                   device: int = 0):
+    """Top-k from plans made by plan_batch on any rank (search.py:138-158),
+    scanning the rows this (shard) index holds: CUDA tensors ids (B, k),
+    dists (B, k).  offsets / items: the CSR of compact_plans, on the device."""
+    import torch
+
+    dev = device_index(index, device)
+    cp = _cparams(params)
+    if _is_torch_cuda(queries):
+        q = queries.contiguous().to(torch.float32)
+        qp = ctypes.c_void_p(q.data_ptr())
+    else:
+        q = np.ascontiguousarray(np.asarray(queries, dtype=np.float32))
+        qp = _vp(q)
+    b = q.shape[0]
+    cuda = torch.device("cuda", dev.device)
+    ids = torch.empty((b, int(k)), dtype=torch.int32, device=cuda)
+    dists = torch.empty((b, int(k)), dtype=torch.float32, device=cuda)
+    stream = torch.cuda.current_stream(cuda).cuda_stream
+    _native.check(_native.load().givf_search_planned(
+        dev.handle, qp, b, ctypes.byref(cp), ctypes.c_void_p(offsets.data_ptr()),
+        ctypes.c_void_p(items.data_ptr()), int(k), ctypes.c_void_p(ids.data_ptr()),
+        ctypes.c_void_p(dists.data_ptr()), ctypes.c_void_p(stream)))
+    return ids, dists
+
+
 def decomposed_distance(query, centroid, neighbor, alpha, code, tables, const_term):
     """Scalar float64 evaluation of the expanded distance form for one point
     (search.py:166-183); `tables` is an inner-product lookup table object with
@@ -251,20 +355,36 @@ class SweepRow:
     codes_scanned: float
 
 
-def sweep(index, queries, truth, grid, r_values=(1, 10, 100), latency_runs=1):
-    """One SweepRow per (params, r) (search.py:215-249).  Each grid point runs
-    the whole query set as one batch; latency_ms is the batch wall time per
-    query (median over latency_runs; 0 when latency_runs == 0)."""
+def sweep(index, queries, truth, grid, r_values=(1, 10, 100), latency_runs=1, batched=False):
+    """One SweepRow per (params, r) (search.py:215-249).
+
+    Default (batched=False) keeps the reference's semantics: every query is
+    its own search() call, latency_ms is the mean over queries of each
+    query's median wall time over latency_runs repeats (0 when latency_runs
+    == 0, so runs compare byte for byte).  batched=True runs each grid point
+    as one batch on the device and reports the batch wall time per query
+    (a throughput figure, not the reference's per-query latency)."""
     queries = np.asarray(queries, dtype=np.float32)
     rows = []
     for params in grid:
         reps = max(1, latency_runs)
-        times = []
-        for _ in range(reps):
-            t0 = time.perf_counter()
-            results = search_batch(index, queries, params)
-            times.append((time.perf_counter() - t0) / max(len(queries), 1))
-        latency_ms = float(np.median(times)) * 1e3 if latency_runs > 0 else 0.0
+        if batched:
+            times = []
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                results = search_batch(index, queries, params)
+                times.append((time.perf_counter() - t0) / max(len(queries), 1))
+            latency_ms = float(np.median(times)) * 1e3 if latency_runs > 0 else 0.0
+        else:
+            results, lat = [], []
+            for qi in range(queries.shape[0]):
+                t = np.empty(reps, dtype=np.float64)
+                for j in range(reps):
+                    res = search(index, queries[qi], params)
+                    t[j] = res.stats.wall_time_s
+                results.append(res)
+                lat.append(float(np.median(t)))
+            latency_ms = float(np.mean(lat)) * 1e3 if latency_runs > 0 else 0.0
         codes = float(np.mean([r.stats.codes_scanned for r in results])) if results else 0.0
         for r in r_values:
             rows.append(SweepRow(nprobe=params.nprobe, tau=params.tau,

@@ -190,7 +190,7 @@ def load_index(path, verify: bool = True) -> IndexArrays:
     return arr
 
 
-def _graph_bytes(index, k) -> bytes:
+def _graph_bytes(index, k, allow_no_graph=False) -> bytes:
     meta = getattr(index, "meta", None)
     if isinstance(meta, FileMeta):
         return meta.graph
@@ -207,13 +207,23 @@ def _graph_bytes(index, k) -> bytes:
                 parts.append(struct.pack("<I", row.size))
                 parts.append(row.astype("<u4").tobytes())
         return b"".join(parts)
-    # GPU-built index (no graph): a valid one-layer graph without edges
+    # GPU-built index (no graph): a valid one-layer graph without edges.  The
+    # reference's search_graph would then return only the entry point (one
+    # probed region whatever nprobe says), so it is written only on request.
+    if not allow_no_graph:
+        raise ValueError("index has no proximity graph: the reference could load the file but "
+                         "its graph probe would visit one region; pass allow_no_graph=True to "
+                         "write an edgeless graph (for this package's loader)")
     return struct.pack("<II", 0, 2) + struct.pack("<II", 1, 0) * k
 
 
-def save_index(index, path, *, l=None, dataset_hash=0, build_seed=0) -> int:
+def save_index(index, path, *, l=None, dataset_hash=0, build_seed=0,
+               allow_no_graph=False) -> int:
     """Write `index` (IndexArrays from load_index / the builder, or a
-    reference GroupedIndex) as a .givf file; returns the bytes written."""
+    reference GroupedIndex) as a .givf file; returns the bytes written.
+    An index without a proximity graph (GPU-built) needs allow_no_graph=True:
+    the file then carries an edgeless graph that the reference's own search
+    cannot probe with (see _graph_bytes)."""
     arr = IndexArrays.from_any(index)
     meta = getattr(index, "meta", None)
     params = getattr(index, "params", None)
@@ -241,7 +251,7 @@ def save_index(index, path, *, l=None, dataset_hash=0, build_seed=0) -> int:
         if arr.rotation is not None:
             w(np.ascontiguousarray(arr.rotation, "<f4").tobytes())
         w(np.ascontiguousarray(arr.codewords, "<f4").tobytes())
-        w(_graph_bytes(index, k))
+        w(_graph_bytes(index, k, allow_no_graph))
         recs = np.zeros(arr.n, _record_dtype(m))
         recs["id"] = arr.point_ids
         recs["code"] = arr.codes

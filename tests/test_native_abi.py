@@ -50,6 +50,7 @@ def test_struct_layouts_match_header(tmp_path):
         "givf_search_params": _native.SearchParamsC,
         "givf_search_stats": _native.SearchStatsC,
         "givf_encode_desc": _native.EncodeDesc,
+        "givf_plan_item": _native.PlanItemC,
     }
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "givf_b200.h"',
              '#include "givf_build.h"', "int main(void){"]

@@ -53,7 +53,9 @@ def test_roundtrip_without_graph(tmp_path):
         "point_ids", "codes", "const_bytes", "codewords", "rotation", "const_lo", "const_hi",
         "grouping")})
     out = tmp_path / "bare.givf"
-    save_index(bare, out)
+    with pytest.raises(ValueError, match="allow_no_graph"):
+        save_index(bare, out)
+    save_index(bare, out, allow_no_graph=True)
     back = load_index(out)
     for f in ("centroids", "alphas", "neighbor_ids", "norm_terms", "group_sizes",
               "region_offsets", "point_ids", "codes", "const_bytes", "codewords"):
