@@ -576,12 +576,7 @@ def run_ours(args, w):
             "kernel_ms_per_step": scan_ms_step,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
         },
-        "roofline_probe": {
-            "kernel": "probe_gemm (K1a: bf16x3 tcgen05 GEMM + split kernel); 2*K*d flops per query",
-            "achieved_tflops": (probe_flops / (gemm_ms / prof_steps / 1e3) / 1e12) if gemm_n else None,
-            "tensor_flops_per_step_bf16x3": probe_flops * 3 * (288 + 32) / 288,
-            "unit": "TFLOP/s",
-        },
+        "roofline_probe": probe_roofline(w, nq, gemm_ms / prof_steps if gemm_n else None, peaks),
         "stage_ms_per_step": step_stage_ms,
         "gpu_launches": int(launches),
         "fallback_queries_per_step": fallbacks,
@@ -603,6 +598,29 @@ def run_ours(args, w):
                                 "sample": f"{done} of the {nq} step queries in {wall:.1f}s "
                                           f"(oracle port of search.py, exact probe, fork x{cpu.cores})"}
     return line
+
+
+def probe_roofline(w, nq, gemm_ms, peaks):
+    """The probe GEMM stage against its bounds.  K >= 2^17 runs the fused
+    probe (probe_fused.cu: one fp16 tcgen05 product per term, 2 K d flops per
+    query; the epilogue reads every fp32 accumulator from TMEM once, K x 4
+    bytes per query -- the measured bound of that kernel); smaller K the
+    bf16x3 GEMM with fp16 score stores (probe_tc.cu)."""
+    if not gemm_ms:
+        return None
+    flops = 2.0 * w["k"] * w["d"] * nq
+    fused = w["k"] >= (1 << 17)
+    peak = float(peaks.get("bf16_tflops", 1590.0))
+    out = {"kernel": ("k_probe_filter (fused fp16 tcgen05 GEMM, threshold epilogue, no score store)"
+                      if fused else "k_probe_gemm_tc (bf16x3 tcgen05 GEMM, fp16 score store)"),
+           "unit": "TFLOP/s", "kernel_ms_per_step": gemm_ms,
+           "achieved_tflops": flops / (gemm_ms / 1e3) / 1e12,
+           "mma_tflops": (flops if fused else flops * 10.0 / 3.0) / (gemm_ms / 1e3) / 1e12,
+           "peak_tflops_dense_bf16": peak}
+    out["frac_of_tensor_peak"] = out["mma_tflops"] / peak
+    if fused:
+        out["tmem_read_GBps"] = 4.0 * w["k"] * nq / (gemm_ms / 1e3) / 1e9
+    return out
 
 
 def reference_recall(workload, noise):

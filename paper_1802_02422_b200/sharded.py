@@ -90,6 +90,10 @@ class ShardedIndex:
 
         from .query import compact_plans, plan_batch, search_planned
 
+        if self.world == 1 and self._local_plan is None:  # nothing to exchange
+            from .query import search_batch
+
+            return search_batch(self.dev, queries, params, k=k)
         b = int(queries.shape[0])
         share = -(-b // self.world)  # ceil
         lo, hi = min(b, self.rank * share), min(b, (self.rank + 1) * share)
