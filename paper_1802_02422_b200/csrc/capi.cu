@@ -990,8 +990,11 @@ int givf_index_create(const givf_index_desc* ds, int device, givf_index_t* out) 
     v.c16e = ec;
     v.c16x = std::ldexp(1.0f, ec);
     const int dp = f16_pitch(d);
-    // sample: every centroid up to 8192, else K/8 (at most 2^17)
-    const int Ks = K <= 8192 ? K : std::min(1 << 17, std::max(8192, K / 8));
+    // sample: every centroid up to 8192, else K/16 (at most 2^16); its
+    // j-th smallest chunk minimum aims the threshold at ~3P + 128 survivors
+    // (j >= 20 at nprobe 64: a sample that lands below the P-th smallest
+    // score of all K is a > 5 sigma event, and costs only a fallback)
+    const int Ks = K <= 8192 ? K : std::min(1 << 16, std::max(8192, K / 16));
     std::vector<int32_t> ids((size_t)K);
     for (int i = 0; i < K; ++i) ids[i] = i;
     if (Ks < K) {
@@ -1008,7 +1011,7 @@ int givf_index_create(const givf_index_desc* ds, int device, givf_index_t* out) 
     const size_t cb = (size_t)K * dp * 2, sb = (size_t)Ks * dp * 2;
     e = cudaMalloc(&c16, cb);
     if (e == cudaSuccess) { ix->allocs.push_back(c16); ix->dev_bytes += (int64_t)cb; e = cudaMalloc(&s16, sb); }
-    if (e == cudaSuccess) { ix->allocs.push_back(s16); ix->dev_bytes += (int64_t)sb; e = cudaMalloc(&sc2, (size_t)Ks * 4); }
+    if (e == cudaSuccess) { ix->allocs.push_back(s16); ix->dev_bytes += (int64_t)sb; e = cudaMalloc(&sc2, (size_t)Ks * 4 + 16); }
     if (e == cudaSuccess) { ix->allocs.push_back(sc2); e = upload(ix, ids.data(), (size_t)Ks, &dids); }
     if (e == cudaSuccess) {
       launch_rows_f16(v.centroids, nullptr, K, d, ec, c16, nullptr, nullptr, 0);

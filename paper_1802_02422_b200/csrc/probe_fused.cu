@@ -286,6 +286,7 @@ k_probe_filter(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
         __syncwarp();
         const uint32_t tq = tmem + ((uint32_t)(quarter * 32) << 16) + acc * TC;
         uint32_t ra[32], rb[32];
+        float mq[4];  // MODE 0: the tile's chunk minima (one row)
         tmem_ld32_async(tq + ((pair * CW) / CPM) * BN + ((pair * CW) % CPM) * 32, ra);
         tmem_wait_ld(ra);
 #pragma unroll
@@ -319,8 +320,20 @@ k_probe_filter(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
           const float u2 = fmin3(tt[6], tt[7], tt[8]), u3 = fmin3(tt[9], tt[10], tt[11]);
           const float m = fminf(fmin3(u0, u1, u2), u3);
           if constexpr (MODE == 0) {
-            if (row[rs] < a.nq && col0 + cc * 32 < a.K)
+            if constexpr (CW == 4 && CPM == 4) {
+              // the warp's four chunks are one row's whole tile: one 16-byte store
+              mq[c] = m;
+              if (c == 3 && row[0] < a.nq) {
+                float* dst = a.cmin + (int64_t)row[0] * a.nch + (col0 >> 5);
+                if ((a.nch & 3) == 0 && col0 + BN <= a.K)
+                  *reinterpret_cast<float4*>(dst) = make_float4(mq[0], mq[1], mq[2], mq[3]);
+                else
+                  for (int i = 0; i < 4; ++i)
+                    if (col0 + i * 32 < a.K) dst[i] = mq[i];
+              }
+            } else if (row[rs] < a.nq && col0 + cc * 32 < a.K) {
               a.cmin[(int64_t)row[rs] * a.nch + ((col0 + cc * 32) >> 5)] = m;
+            }
           } else {
             if (m < thr[rs]) {  // rare: stage the chunk, walk the triples below thr
               uint32_t tm = 0;
