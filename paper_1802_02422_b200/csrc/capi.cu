@@ -446,12 +446,71 @@ int run_probe(givf_index* ix, const Plan& pl, const float* dQ, int nq, int* regi
     if (fused_out) *fused_out = true;
     staged(ST_RECHECK, st, [&] {
       launch_probe_recheck(dQ, v.centroids, nq, K, d, P, cand, cand_n, ps.fcap2, theta, v.cmax,
-                           eps, 0.f, regions, qc2, failf, v.counters, st);
+                           eps, 0.f, regions, qc2, failf, nullptr, st);
     });
-    staged(ST_FULL, st, [&] {
-      launch_probe_full(dQ, v.centroids, nq, K, d, P, 1, failf, slots, sk, sv, sk2, sv2, sdv,
-                        regions, qc2, st);
-    });
+    // Retry pass for the queries the sampled threshold missed (too few
+    // survivors, an overflowing segment, or no certificate): the P-th
+    // smallest sample chunk minimum bounds the P-th smallest score of all K
+    // from above, so the second threshold always admits the true top-P;
+    // only what still fails takes the exhaustive float64 probe (K2').
+    int* fidx = ar.take<int>(nq);
+    int* fcnt = ar.take<int>(1);
+    ARENA_CHECK(ar);
+    launch_collect_failed(failf, nq, fidx, fcnt, st);
+    int nfail = 0;
+    CUDA_TRY(cudaMemcpyAsync(&nfail, fcnt, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    g_launches += 1;
+    if (nfail > 0) {
+      launch_add_counter(v.counters + 8, fcnt, st);  // retried queries
+      // up to 64k survivors per retried query, in groups that fit the first
+      // pass's survivor buffers (nq x nseg counters, nq x nseg x cap_u records)
+      const int64_t room = (int64_t)nq * nseg * cap_u;
+      const int fcap_r = (int)std::min<int64_t>(65536, (int64_t)K);
+      int g = (int)std::max<int64_t>(1, std::min<int64_t>(nfail, room / fcap_r));
+      int nseg_r = 0, cap_u_r = 0;
+      for (;;) {  // shrink the group until its segment counters fit
+        filter_segments(g, K, fcap_r, &nseg_r, &cap_u_r);
+        cap_u_r = (int)std::min<int64_t>(cap_u_r, room / ((int64_t)g * nseg_r));
+        if ((int64_t)g * nseg_r <= (int64_t)nq * nseg || g == 1) break;
+        g = std::max(1, g / 2);
+      }
+      float* qr = ar.take<float>((size_t)std::min(nfail, g) * d);
+      ARENA_CHECK(ar);
+      if ((int64_t)g * nseg_r > (int64_t)nq * nseg || cap_u_r < 8) {
+        launch_add_counter(v.counters, fcnt, st);  // no room: straight to K2'
+      } else {
+        for (int f0 = 0; f0 < nfail; f0 += g) {
+          const int gn = std::min(g, nfail - f0);
+          const int* gidx = fidx + f0;
+          staged(ST_SAMPLE, st, [&] {
+            launch_gather_rows(dQ, gidx, gn, d, qr, st);
+            launch_query_f16(qr, gn, d, v.c16x, q16, ms, q2f, st);
+            launch_probe_thresh(cmin, nch, P, q2f, v.cmax, eps, gn, thr, st, gidx);
+          }, 3);
+          staged(ST_GEMM, st, [&] {
+            ce = launch_probe_filter(q16, v.c16, v.c2f, gn, K, d, ms, thr, nseg_r, cap_u_r, cnt,
+                                     cid, cval, st);
+          });
+          if (ce != cudaSuccess)
+            return fail(GIVF_ECUDA, std::string("probe retry: ") + cudaGetErrorString(ce));
+          staged(ST_SELECT, st, [&] {
+            launch_probe_pick(cnt, cid, cval, nseg_r, cap_u_r, nseg_r * cap_u_r, thr, q2f, v.cmax,
+                              eps, P, ps.fcap2, gn, cand, cand_n, theta, st);
+          });
+          staged(ST_RECHECK, st, [&] {
+            launch_probe_recheck(dQ, v.centroids, gn, K, d, P, cand, cand_n, ps.fcap2, theta,
+                                 v.cmax, eps, 0.f, regions, qc2, failf, v.counters, st, gidx);
+          });
+        }
+      }
+    }
+    if (nfail > 0) {
+      staged(ST_FULL, st, [&] {
+        launch_probe_full(dQ, v.centroids, nq, K, d, P, 1, failf, slots, sk, sv, sk2, sv2, sdv,
+                          regions, qc2, st);
+      });
+    }
     KCHECK();
     return GIVF_OK;
   }
@@ -510,7 +569,7 @@ size_t probe_bytes_per_query(const Plan& pl) {
   if (!pl.ps.exhaustive && pl.fused)
     b += (size_t)f16_pitch(pl.d) * 2 + 8 * aligned_bytes<float>(1) +
          (size_t)((pl.Ks + 31) / 32) * 4 + (size_t)pl.ps.fcap * 8 + 2048 * 4 +
-         (size_t)pl.ps.fcap2 * 4 + 512;
+         (size_t)pl.ps.fcap2 * 4 + (size_t)pl.d * 4 + 512;  // + the retry's gathered rows
   else if (!pl.ps.exhaustive)
     b += (size_t)pl.K * 2 + 4 * aligned_bytes<float>(1) + (size_t)pl.ps.cap * 4 +
          aligned_bytes<float>(probe_tiles(pl.K)) +
@@ -692,6 +751,7 @@ int run_search(givf_index* ix, const float* queries, int64_t nq, const givf_sear
     pa.ldD = v.K;
     pa.cmax = v.cmax;
     pa.half_rel = (float)kHalfRel;
+    pa.n_overflow = ar.take<int>(1);
     pa.global_items = om == OUT_PLAN ? 1 : 0;
     pa.only = ar.take<int>(bq);
     ARENA_CHECK(ar);

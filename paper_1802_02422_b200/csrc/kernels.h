@@ -103,7 +103,13 @@ cudaError_t launch_probe_filter(const void* q16, const void* c16, const float* c
                                 int d, const float* ms, const float* thr, int nseg, int cap_u,
                                 int* cnt, int* cid, float* cval, cudaStream_t s);
 void launch_probe_thresh(const float* cmin, int nch, int j, const float* q2, float cmax,
-                         float eps_scale, int nq, float* thr, cudaStream_t s);
+                         float eps_scale, int nq, float* thr, cudaStream_t s,
+                         const int* qmap = nullptr);
+// retry pass of the fused probe: indices of the queries flagged in fail
+// (any order) and their count; rows of Q gathered by idx
+void launch_collect_failed(const int* fail, int nq, int* idx, int* n, cudaStream_t s);
+void launch_gather_rows(const float* Q, const int* idx, int n, int d, float* out, cudaStream_t s);
+void launch_add_counter(unsigned long long* c, const int* n, cudaStream_t s);
 void launch_probe_pick(const int* cnt, const int* cid, const float* cval, int nseg, int cap_u,
                        int fcap, const float* thr, const float* q2, float cmax, float eps_scale,
                        int P, int cap2, int nq, int* cand, int* cand_n, float* theta,
@@ -122,7 +128,8 @@ size_t probe_recheck_smem(int d, int P, int cap);
 void launch_probe_recheck(const float* Q, const float* C, int nq, int K, int d, int P,
                           const int* cand, const int* cand_n, int cap, const float* theta,
                           float cmax, float eps_scale, float half_rel, int* regions, double* qc2,
-                          int* fail, unsigned long long* fail_count, cudaStream_t s);
+                          int* fail, unsigned long long* fail_count, cudaStream_t s,
+                          const int* qmap = nullptr);
 void launch_probe_full(const float* Q, const float* C, int nq, int K, int d, int P, int mode,
                        const int* fail, int nslots, uint64_t* sk, uint32_t* sv, uint64_t* sk2,
                        uint32_t* sv2, double* sdv, int* regions, double* qc2, cudaStream_t s);
@@ -162,6 +169,11 @@ struct PlanArgs {
   // query-sharded planning: emit whole groups (start = global group index
   // region * G + group, len = global length) instead of this shard's rows
   int global_items;
+  // K4 window capacity: first pass (0 = the default by staging) and the
+  // retry pass for the queries whose certified window overflowed
+  int wcap_override;
+  int retry;            // 1: only the queries flagged for window overflow
+  int* n_overflow;      // (1) device counter of first-pass window overflows
   int approx;           // akey holds K3a's keys: run the approximate-first planner
 };
 // plan_approx.cu: K3a, the approximate group scores (needs D; may run per

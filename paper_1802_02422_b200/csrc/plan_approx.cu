@@ -44,6 +44,7 @@ constexpr int PA_SORT = 1024;     // boundary-bucket sort capacity
 constexpr int PA_SMALL = 128;     // refine further while the bucket is larger
 constexpr int PA_WCAP = 256;      // window capacity (items staged in shared memory)
 constexpr int PA_WCAP_BIG = 1024; // window capacity when the items are not staged
+constexpr int PA_WCAP_RETRY = 2048;  // retry pass for the queries whose window overflowed
 constexpr int PA_CAND = 1536;     // begun groups (else the exact planner)
 constexpr int PA_PSTAGE = 512;    // probed regions staged in shared memory
 constexpr int PA_U = 4;           // centroid rows in flight per 8-lane group
@@ -162,14 +163,14 @@ struct PaSmem {
   size_t skey, ssz, pool, wkey, wval, wlen, wrow, wnorm, qd, preg, pqc, pal, bytes;
   int wcap;  // window capacity: larger when the items' staging space is free
   // small: every group size < 2^16, so the staged sizes are 16-bit
-  __host__ __device__ PaSmem(int d, int P, int64_t total, bool small) {
+  __host__ __device__ PaSmem(int d, int P, int64_t total, bool small, int wcap_override = 0) {
     const bool staged = total <= PA_ITEMS;
     const bool pst = P <= PA_PSTAGE;
     size_t o = 0;
     auto take = [&](size_t n) { size_t r = o; o = (o + n + 15) & ~(size_t)15; return r; };
     pool = take((size_t)3 * PA_CAND * 4 > (size_t)(PA_BUCKETS + PA_SORT) * 8
                     ? (size_t)3 * PA_CAND * 4 : (size_t)(PA_BUCKETS + PA_SORT) * 8);
-    wcap = staged ? PA_WCAP : PA_WCAP_BIG;
+    wcap = wcap_override > 0 ? wcap_override : (staged ? PA_WCAP : PA_WCAP_BIG);
     wkey = take((size_t)wcap * 8);
     qd = take((size_t)d * 8);
     pqc = take(pst ? (size_t)P * 8 : 0);
@@ -197,7 +198,9 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
   const bool staged = total <= PA_ITEMS;
   const bool pst = P <= PA_PSTAGE;
   const bool small = ix.max_gsize < 65536;
-  const PaSmem L(d, P, total, small);
+  // retry pass: only the queries whose window overflowed in the first pass
+  if (a.retry && a.only[b] != 2) return;
+  const PaSmem L(d, P, total, small, a.wcap_override);
 
   // histogram: separate 32-bit counts and weights (a 64-bit shared atomic
   // is a CAS loop); bucket weights are sums of group sizes < 2^32
@@ -604,10 +607,17 @@ __global__ void __launch_bounds__(PA_THREADS, INLINE ? 3 : 4) k_plan_approx(Plan
 #endif
   if (flag) {
     if (tid == 0) {
-      a.only[b] = 1;
-      if (ix.counters) {
-        atomicAdd(&ix.counters[1], 1ull);
-        atomicAdd(&ix.counters[2 + why], 1ull);
+      if (why == 1 && !a.retry && a.n_overflow) {
+        // window overflow: a second pass with a larger window (only = 2)
+        a.only[b] = 2;
+        atomicAdd(a.n_overflow, 1);
+        if (ix.counters) atomicAdd(&ix.counters[9], 1ull);
+      } else {
+        a.only[b] = 1;
+        if (ix.counters) {
+          atomicAdd(&ix.counters[1], 1ull);
+          atomicAdd(&ix.counters[2 + why], 1ull);
+        }
       }
     }
     return;
@@ -830,17 +840,38 @@ int launch_plan_approx(const PlanArgs& a0, cudaStream_t s) {
   PlanArgs a = a0;
   // the scan-order sort (rerank=False) needs the scores inside k_plan_approx
   a.defer_rescore = (a.ix.grouping && !a.sort_work) ? 1 : 0;
-  const PaSmem L(a.ix.d, a.P, (int64_t)a.P * a.ix.G, a.ix.max_gsize < 65536);
+  static const int wcap_env = getenv("GIVF_PLAN_WCAP") ? atoi(getenv("GIVF_PLAN_WCAP")) : 0;
+  a.wcap_override = wcap_env > 0 ? std::min(wcap_env, PA_WCAP_RETRY) : 0;
+  a.retry = 0;
+  const PaSmem L(a.ix.d, a.P, (int64_t)a.P * a.ix.G, a.ix.max_gsize < 65536, a.wcap_override);
   auto kern = a.defer_rescore ? k_plan_approx<false> : k_plan_approx<true>;
   ensure_max_smem((const void*)kern, L.bytes);
+  if (a.n_overflow) cudaMemsetAsync(a.n_overflow, 0, sizeof(int), s);
   kern<<<a.nq, PA_THREADS, L.bytes, s>>>(a);
-  if (!a.defer_rescore) return 1;
+  int n = 1;
+  if (a.n_overflow) {
+    // queries whose certified window overflowed: one more pass with a
+    // 2048-entry window before the exact planner takes what is left
+    int nov = 0;
+    cudaMemcpyAsync(&nov, a.n_overflow, sizeof(int), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    if (nov > 0) {
+      PlanArgs r = a;
+      r.retry = 1;
+      r.wcap_override = PA_WCAP_RETRY;
+      const PaSmem LR(r.ix.d, r.P, (int64_t)r.P * r.ix.G, r.ix.max_gsize < 65536, PA_WCAP_RETRY);
+      ensure_max_smem((const void*)kern, LR.bytes);
+      kern<<<r.nq, PA_THREADS, LR.bytes, s>>>(r);
+      ++n;
+    }
+  }
+  if (!a.defer_rescore) return n;
   static const int split = [] {  // CTAs per query (GIVF_RS_SPLIT)
     const char* e = getenv("GIVF_RS_SPLIT");
     return e ? std::max(1, std::min(64, atoi(e))) : RS_SPLIT;
   }();
   k_plan_rescore<<<dim3(a.nq, split), RS_THREADS, (size_t)a.ix.d * 8, s>>>(a);
-  return 2;
+  return n + 1;
 }
 
 int launch_plan_scores(const PlanArgs& a, cudaStream_t s) {

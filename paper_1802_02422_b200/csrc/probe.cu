@@ -468,7 +468,8 @@ k_probe_recheck(const float* __restrict__ Q, const float* __restrict__ C, int K,
                 int P, const int* __restrict__ cand, const int* __restrict__ cand_n,
                 int cap, const float* __restrict__ theta, float cmax, float eps_scale,
                 float half_rel, int* __restrict__ regions, double* __restrict__ qc2,
-                int* __restrict__ fail, unsigned long long* fail_count) {
+                int* __restrict__ fail, unsigned long long* fail_count,
+                const int* __restrict__ qmap) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int capp2 = (int)next_pow2((uint32_t)cap);
   const int pp2 = (int)next_pow2((uint32_t)P);
@@ -481,8 +482,11 @@ k_probe_recheck(const float* __restrict__ Q, const float* __restrict__ C, int K,
   float* qf = reinterpret_cast<float*>(v2 + pp2);
   __shared__ double red[40];
 
+  // b indexes the candidate lists; qb the query (qmap: a re-check of some
+  // queries of the chunk, e.g. the fused probe's retry pass)
   const int b = blockIdx.x;
-  const float* q = Q + (int64_t)b * d;
+  const int qb = qmap ? qmap[b] : b;
+  const float* q = Q + (int64_t)qb * d;
   double q2p = 0.0;
   for (int j = threadIdx.x; j < d; j += blockDim.x) {
     qf[j] = q[j];
@@ -552,14 +556,14 @@ k_probe_recheck(const float* __restrict__ Q, const float* __restrict__ C, int K,
     bool ok = (n >= P) && (dp - q2 < th - eps);
     if (!ok) {
       if (threadIdx.x == 0) {
-        fail[b] = 1;
+        fail[qb] = 1;
         if (fail_count) atomicAdd(fail_count, 1ull);
       }
       return;
     }
   }
-  if (threadIdx.x == 0) fail[b] = 0;
-  emit_probe(key, val, P, true, k2, v2, dv, regions + (int64_t)b * P, qc2 + (int64_t)b * P);
+  if (threadIdx.x == 0) fail[qb] = 0;
+  emit_probe(key, val, P, true, k2, v2, dv, regions + (int64_t)qb * P, qc2 + (int64_t)qb * P);
 }
 
 // Exhaustive exact ranking of all K regions for one query per loop step:
@@ -656,11 +660,12 @@ size_t probe_recheck_smem(int d, int P, int cap) {
 void launch_probe_recheck(const float* Q, const float* C, int nq, int K, int d, int P,
                           const int* cand, const int* cand_n, int cap, const float* theta,
                           float cmax, float eps_scale, float half_rel, int* regions, double* qc2,
-                          int* fail, unsigned long long* fail_count, cudaStream_t s) {
+                          int* fail, unsigned long long* fail_count, cudaStream_t s,
+                          const int* qmap) {
   size_t sm = probe_recheck_smem(d, P, cap);
   ensure_max_smem((const void*)k_probe_recheck, 200 * 1024);
   k_probe_recheck<<<nq, 256, sm, s>>>(Q, C, K, d, P, cand, cand_n, cap, theta, cmax, eps_scale,
-                                      half_rel, regions, qc2, fail, fail_count);
+                                      half_rel, regions, qc2, fail, fail_count, qmap);
 }
 
 void launch_probe_full(const float* Q, const float* C, int nq, int K, int d, int P, int mode,

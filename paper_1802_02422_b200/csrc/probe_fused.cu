@@ -461,13 +461,14 @@ __device__ uint32_t block_kth_key(const uint32_t* keys, int n, int k, uint32_t* 
 // thr = (j-th smallest sample chunk minimum) + 2 eps (+ float slack).
 __global__ void __launch_bounds__(256)
 k_probe_thresh(const float* __restrict__ cmin, int nch, int j, const float* __restrict__ q2,
-               float cmax, float eps_scale, float* __restrict__ thr) {
+               float cmax, float eps_scale, float* __restrict__ thr, const int* __restrict__ qmap) {
   extern __shared__ uint32_t keys[];
   __shared__ uint32_t hist[256];
   __shared__ uint32_t red[40];
   const int b = blockIdx.x;
+  const int64_t row = qmap ? qmap[b] : b;  // the sample minima of the chunk's query qmap[b]
   for (int i = threadIdx.x; i < nch; i += blockDim.x)
-    keys[i] = f32_key(cmin[(int64_t)b * nch + i]);
+    keys[i] = f32_key(cmin[row * nch + i]);
   __syncthreads();
   const uint32_t kk = block_kth_key(keys, nch, min(j, nch), hist, red);
   if (threadIdx.x == 0) {
@@ -728,10 +729,49 @@ cudaError_t launch_probe_filter(const void* q16, const void* c16, const float* c
 }
 
 void launch_probe_thresh(const float* cmin, int nch, int j, const float* q2, float cmax,
-                         float eps_scale, int nq, float* thr, cudaStream_t s) {
+                         float eps_scale, int nq, float* thr, cudaStream_t s, const int* qmap) {
   const size_t sm = (size_t)nch * 4;
   ensure_max_smem((const void*)k_probe_thresh, sm);
-  k_probe_thresh<<<nq, 256, sm, s>>>(cmin, nch, j, q2, cmax, eps_scale, thr);
+  k_probe_thresh<<<nq, 256, sm, s>>>(cmin, nch, j, q2, cmax, eps_scale, thr, qmap);
+}
+
+__global__ void k_collect_failed(const int* __restrict__ fail, int nq, int* __restrict__ idx,
+                                 int* __restrict__ n) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool f = b < nq && fail[b] != 0;
+  const unsigned bal = __ballot_sync(0xffffffffu, f);
+  if (!bal) return;
+  int base = 0;
+  if ((threadIdx.x & 31) == 0) base = atomicAdd(n, __popc(bal));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (f) idx[base + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u))] = b;
+}
+
+__global__ void k_gather_rows(const float* __restrict__ Q, const int* __restrict__ idx, int n, int d,
+                              float* __restrict__ out) {
+  const int64_t total = (int64_t)n * d;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x)
+    out[e] = Q[(int64_t)idx[e / d] * d + e % d];
+}
+
+__global__ void k_add_counter(unsigned long long* c, const int* n) {
+  if (threadIdx.x == 0 && *n) atomicAdd(c, (unsigned long long)*n);
+}
+
+void launch_collect_failed(const int* fail, int nq, int* idx, int* n, cudaStream_t s) {
+  cudaMemsetAsync(n, 0, sizeof(int), s);
+  k_collect_failed<<<(nq + 255) / 256, 256, 0, s>>>(fail, nq, idx, n);
+}
+
+void launch_gather_rows(const float* Q, const int* idx, int n, int d, float* out, cudaStream_t s) {
+  const int64_t total = (int64_t)n * d;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms_cur() * 8);
+  if (blocks > 0) k_gather_rows<<<blocks, 256, 0, s>>>(Q, idx, n, d, out);
+}
+
+void launch_add_counter(unsigned long long* c, const int* n, cudaStream_t s) {
+  k_add_counter<<<1, 32, 0, s>>>(c, n);
 }
 
 void launch_probe_pick(const int* cnt, const int* cid, const float* cval, int nseg, int cap_u,

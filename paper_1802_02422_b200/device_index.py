@@ -230,9 +230,23 @@ class DeviceIndex:
 
     def fallback_counts(self) -> dict:
         """Queries that left the fast path so far (probe re-check / planner)."""
-        out = np.zeros(8, np.int64)
-        _native.check(_native.load().givf_index_counters(self._h, out.ctypes.data, 8))
+        out = np.zeros(16, np.int64)
+        _native.check(_native.load().givf_index_counters(self._h, out.ctypes.data, 16))
         return {"probe": int(out[0]), "plan": int(out[1])}
+
+    def probe_retries(self) -> int:
+        """Queries the fused probe re-ran with its guaranteed threshold (their
+        sampled threshold missed; the retry keeps them off the exhaustive path)."""
+        out = np.zeros(16, np.int64)
+        _native.check(_native.load().givf_index_counters(self._h, out.ctypes.data, 16))
+        return int(out[8])
+
+    def plan_retries(self) -> int:
+        """Queries the approximate planner re-ran with a 2048-entry certified
+        window (their first window overflowed)."""
+        out = np.zeros(16, np.int64)
+        _native.check(_native.load().givf_index_counters(self._h, out.ctypes.data, 16))
+        return int(out[9])
 
     def plan_fallback_reasons(self) -> dict:
         """Approximate-planner fallbacks split by the check that failed."""

@@ -106,6 +106,7 @@ def default_mode_result():
     {"GIVF_SCAN": "warp"},                         # block-wide segment windows (k_scan_warp)
     {"GIVF_GEMM_SPLIT": "3"},                      # probe GEMM work units: 3 slices per m-block
     {"GIVF_RS_SPLIT": "5"},                        # K4b: 5 CTAs per query
+    {"GIVF_PLAN_WCAP": "8"},                       # K4 windows overflow: the 2048-entry retry pass
     {"GIVF_PROBE": "fused"},                       # fused probe, 2 x 128 queries x 128 centroids
     {"GIVF_PROBE": "fused", "GIVF_FILTER_SHAPE": "4x64"},  # 4 x 128 queries x 64 centroids
     {"GIVF_PROBE": "fused", "GIVF_FILTER_SHAPE": "1x128"},  # 128 queries, rows shared by 2 warps

@@ -20,8 +20,8 @@ from parity import assert_ranked_equal, assert_topk_equal
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def k20():
+def _k20_arrays():
+    """The K = 2^20 index and 100 queries (deterministic)."""
     import torch
 
     from paper_1802_02422_b200.builder import neighbor_centroids, norm_terms
@@ -52,7 +52,52 @@ def k20():
         codewords=cw.cpu().numpy(), rotation=None, const_lo=-0.5, const_hi=0.5, grouping=True)
     del key, order, codes, cbytes
     torch.cuda.empty_cache()
-    return arr, DeviceIndex(arr), q.cpu().numpy()
+    return arr, q.cpu().numpy()
+
+
+@pytest.fixture(scope="module")
+def k20():
+    from paper_1802_02422_b200.device_index import DeviceIndex
+
+    arr, q = _k20_arrays()
+    return arr, DeviceIndex(arr), q
+
+
+_RETRY_CODE = """
+import sys, json, numpy as np
+sys.path.insert(0, %(root)r); sys.path.insert(0, %(tests)r)
+import test_gpu_parity_scale as t
+from paper_1802_02422_b200 import SearchParams, search_batch
+from paper_1802_02422_b200.device_index import DeviceIndex
+arr, q = t._k20_arrays()
+dev = DeviceIndex(arr)
+ids, d, st = search_batch(dev, q, SearchParams(nprobe=512, tau=0.5, candidates=10_000), k=100)
+np.savez(%(out)r, ids=ids, d=d, st=st, fb=dev.fallback_counts()["probe"], retry=dev.probe_retries())
+"""
+
+
+def test_k20_fused_retry_pass(tmp_path):
+    """A sampled threshold aimed at 128 survivors (GIVF_FUSED_TARGET=0) is
+    below the 512th score for every query: all of them take the fused
+    probe's retry pass (guaranteed threshold) instead of the exhaustive
+    float64 probe, with results identical to the default run."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    outs = {}
+    for name, env in (("default", {}), ("retry", {"GIVF_FUSED_TARGET": "0"})):
+        out = str(tmp_path / f"{name}.npz")
+        code = _RETRY_CODE % dict(root=os.path.dirname(here), tests=here, out=out)
+        subprocess.check_call([sys.executable, "-c", code], env=dict(os.environ, **env))
+        outs[name] = np.load(out)
+    a, b = outs["default"], outs["retry"]
+    assert int(a["retry"]) == 0 and int(a["fb"]) == 0
+    assert int(b["retry"]) == b["ids"].shape[0] and int(b["fb"]) == 0
+    np.testing.assert_array_equal(a["ids"], b["ids"])
+    np.testing.assert_array_equal(a["d"], b["d"])
+    np.testing.assert_array_equal(a["st"], b["st"])
 
 
 @pytest.mark.parametrize("nprobe,tau", [(32, 0.5), (32, 0.25), (128, 0.5), (128, 0.25),
