@@ -1256,7 +1256,8 @@ int givf_probe_scores(givf_index_t ix, const float* queries, int64_t nq, float* 
   int nseg = 0, cap_u = 0;
   if (fz) {  // every centroid survives thr = +inf: segments sized for a whole slice
     filter_segments((int)nq, K, K, &nseg, &cap_u);
-    cap_u = (K + nseg / 2 - 1) / (nseg / 2) + 256;
+    const int ns = nseg / filter_slots();
+    cap_u = (K + ns - 1) / ns + 256;
   }
   const size_t bytes = (size_t)nq * (d * 4 + (size_t)K * 4 + (size_t)nseg * cap_u * 8 + nseg * 4 +
                                      tc_kpad(d) * 2 + probe_tiles(K) * 4 + f16_pitch(d) * 2 + 64) +

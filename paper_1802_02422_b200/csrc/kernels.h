@@ -99,6 +99,7 @@ void launch_query_f16(const float* Q, int nq, int d, float cexp, void* q16, floa
 cudaError_t launch_probe_sample(const void* q16, const void* s16, const float* sc2, int nq, int Ks,
                                 int d, const float* ms, float* cmin, cudaStream_t s);
 void filter_segments(int nq, int K, int fcap, int* nseg, int* cap_u);
+int filter_slots();  // survivor segments per (query, work unit)
 cudaError_t launch_probe_filter(const void* q16, const void* c16, const float* c2, int nq, int K,
                                 int d, const float* ms, const float* thr, int nseg, int cap_u,
                                 int* cnt, int* cid, float* cval, cudaStream_t s);

@@ -58,9 +58,10 @@ namespace givf {
 namespace pf {
 constexpr int BM = 128, BK = 32;  // BK fp16 = 64 B = one SWIZZLE_64B row
 constexpr int NS_MAX = 4;         // centroid-tile ring depth
-constexpr int STG = 36;           // per-lane staging row (floats, 16-byte aligned)
-constexpr int EPI_WARPS = 8;      // two per TMEM lane quarter
-constexpr int THREADS = 64 + 32 * EPI_WARPS;
+// Epilogue warps: EW = 8, two per TMEM lane quarter (a template parameter;
+// 16 measured slower, see filter_warps).
+constexpr int EW_MAX = 16;
+__host__ __device__ constexpr int threads_of(int ew) { return 64 + 32 * ew; }
 constexpr uint32_t A_CHUNK = BM * BK * 2;  // 8 KB
 constexpr int TMEM_COLS = 512;             // 512 / (MB * BN) accumulator buffers
 constexpr int NBUF_MAX = 4;
@@ -82,10 +83,10 @@ __host__ __device__ constexpr int ring(int mb, int bn, int kc) {
        : (size_t)mb * kc * A_CHUNK + (size_t)3 * kc * b_chunk(bn) <= 180 * 1024       ? 3
                                                                                        : 2;
 }
-// [A block][B ring][|c|^2 per warp][survivor staging per warp][barriers]
-__host__ __device__ constexpr size_t smem_bytes(int mb, int bn, int kc) {
+// [A block][B ring][|c|^2 per warp][barriers]
+__host__ __device__ constexpr size_t smem_bytes(int mb, int bn, int kc, int ew) {
   return 1024 + (size_t)mb * kc * A_CHUNK + (size_t)ring(mb, bn, kc) * kc * b_chunk(bn) +
-         (size_t)EPI_WARPS * 256 * 4 + (size_t)EPI_WARPS * 32 * STG * 4 + sizeof(Smem) + 64;
+         (size_t)ew * 256 * 4 + sizeof(Smem) + 64;
 }
 }  // namespace pf
 
@@ -96,10 +97,10 @@ struct FilterArgs {
   // MODE 0: chunk minima
   float* cmin;       // (nq, nch)
   int nch;
-  // MODE 1: survivors below thr, in per-(query, unit, epilogue warp pair)
+  // MODE 1: survivors below thr, in per-(query, unit, epilogue slot)
   // segments of cap_u entries -- no atomics: each segment has one writer
   const float* thr;  // (nq)
-  int nseg, cap_u;   // nseg = 2 * nsplit
+  int nseg, cap_u;   // nseg = (EW / 4) * nsplit
   int* cnt;          // (nq, nseg) survivors found (may exceed cap_u)
   int* cid;          // (nq, nseg, cap_u)
   float* cval;       // (nq, nseg, cap_u)
@@ -122,8 +123,8 @@ GIVF_DEV float fmin3(float a, float b, float c) {
 // Work unit = (MB m-blocks of 128 queries, slice of the BN-centroid tiles).
 // The tile's accumulators take MB * BN TMEM columns: 512 / (MB * BN)
 // buffers let the MMA run that many tiles ahead of the epilogue.
-template <int MB, int BN, int MODE>
-__global__ void __launch_bounds__(pf::THREADS, 1)
+template <int MB, int BN, int MODE, int EW>
+__global__ void __launch_bounds__(pf::threads_of(EW), 1)
 k_probe_filter(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                FilterArgs a) {
   using namespace pf;
@@ -132,7 +133,8 @@ k_probe_filter(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
   constexpr int TC = MB * BN;           // TMEM columns per tile
   constexpr int NBUF = TMEM_COLS / TC;  // accumulator buffers
   constexpr int CPM = BN / 32;          // 32-column chunks per m-block
-  constexpr int CW = TC / 64;           // chunks per epilogue warp per tile
+  constexpr int SLOTS = EW / 4;         // epilogue warps per TMEM lane quarter
+  constexpr int CW = TC / (32 * SLOTS);  // chunks per epilogue warp per tile
   constexpr int NR = CW >= CPM ? CW / CPM : 1;  // query rows per thread
   constexpr uint32_t IDESC = idesc_f16(BM, BN);
   static_assert(NBUF >= 2 && NBUF <= NBUF_MAX && CW >= 1, "tile shape");
@@ -144,8 +146,7 @@ k_probe_filter(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
   unsigned char* smA = base;
   unsigned char* smB = base + (size_t)MB * KC * A_CHUNK;
   float* c2all = reinterpret_cast<float*>(smB + (size_t)NS * KC * B_CHUNK);
-  float* stg_all = c2all + EPI_WARPS * 256;
-  Smem* sm = reinterpret_cast<Smem*>(stg_all + EPI_WARPS * 32 * STG);
+  Smem* sm = reinterpret_cast<Smem*>(c2all + EW * 256);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int groups = (a.nq + MB * BM - 1) / (MB * BM);
@@ -159,7 +160,7 @@ k_probe_filter(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
     mbar_init(&sm->a_empty, 1);
     for (int i = 0; i < NBUF; ++i) {
       mbar_init(&sm->tm_full[i], 1);
-      mbar_init(&sm->tm_empty[i], EPI_WARPS);
+      mbar_init(&sm->tm_empty[i], EW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -224,13 +225,16 @@ k_probe_filter(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
         if (lane == 0) {
           const uint32_t b0 = smem_u32(smB + (size_t)stage * KC * B_CHUNK);
 #pragma unroll
-          for (int mb = 0; mb < MB; ++mb) {
-            const uint32_t dcol = tmem + acc * TC + mb * BN;
-            const uint32_t a0 = smem_u32(smA + (size_t)mb * KC * A_CHUNK);
-            for (int ks = 0; ks < ksteps; ++ks) {
-              const int kc = ks >> 1, k = ks & 1;
-              mma_bf16(dcol, sw64_desc(a0 + kc * A_CHUNK + k * 32),
-                       sw64_desc(b0 + kc * B_CHUNK + k * 32), IDESC, ks != 0 ? 1u : 0u);
+          // k-steps outer, m-blocks inner: consecutive MMAs go to different
+          // accumulators, so no MMA waits on the one before it
+          for (int ks = 0; ks < ksteps; ++ks) {
+            const int kc = ks >> 1, k = ks & 1;
+            const uint64_t bd = sw64_desc(b0 + kc * B_CHUNK + k * 32);
+#pragma unroll
+            for (int mb = 0; mb < MB; ++mb) {
+              const uint32_t a0 = smem_u32(smA + (size_t)mb * KC * A_CHUNK);
+              mma_bf16(tmem + acc * TC + mb * BN, sw64_desc(a0 + kc * A_CHUNK + k * 32), bd, IDESC,
+                       ks != 0 ? 1u : 0u);
             }
           }
           mma_commit(&sm->empty[stage]);  // the tile's stage is free once these retire
@@ -244,14 +248,13 @@ k_probe_filter(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
       __syncwarp();
     }
   } else {
-    // ------------------------------------------------ epilogue (warps 2..9)
+    // ------------------------------------------------ epilogue (warps 2..)
     // Warp e owns lane quarter (warp & 3) and CW 32-column chunks of the
-    // tile: flat chunk f = pair * CW + c over (m-block, column chunk).
+    // tile: flat chunk f = slot * CW + c over (m-block, column chunk).
     const int e = warp - 2;
     const int quarter = warp & 3;
-    const int pair = e >> 2;
+    const int slot = e >> 2;
     float* c2w = c2all + e * 256;
-    float* stg = stg_all + (e * 32 + lane) * STG;
     uint32_t acc = 0, acc_phase = 0;
     const float kInf = __int_as_float(0x7f800000);
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -262,7 +265,7 @@ k_probe_filter(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
       float msr[NR], thr[NR];
 #pragma unroll
       for (int r = 0; r < NR; ++r) {
-        const int mb = (pair * CW + r * CPM) / CPM;
+        const int mb = (slot * CW + r * CPM) / CPM;
         row[r] = (g * MB + mb) * BM + quarter * 32 + lane;
         const bool ok = row[r] < a.nq;
         msr[r] = ok ? a.ms[row[r]] : 0.f;
@@ -285,22 +288,15 @@ k_probe_filter(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
         for (int i = 0; i < CPM; ++i) c2w[i * 32 + lane] = cr[i];
         __syncwarp();
         const uint32_t tq = tmem + ((uint32_t)(quarter * 32) << 16) + acc * TC;
-        uint32_t ra[32], rb[32];
-        float mq[4];  // MODE 0: the tile's chunk minima (one row)
-        tmem_ld32_async(tq + ((pair * CW) / CPM) * BN + ((pair * CW) % CPM) * 32, ra);
-        tmem_wait_ld(ra);
-#pragma unroll
-        for (int c = 0; c < CW; ++c) {
-          uint32_t* r = (c & 1) ? rb : ra;
-          uint32_t* rn = (c & 1) ? ra : rb;
-          const int f = pair * CW + c, cc = f % CPM, rs = NR > 1 ? c / CPM : 0;
-          if (c + 1 < CW) {  // next chunk in flight while this one is reduced
-            const int fn = f + 1;
-            tmem_ld32_async(tq + (fn / CPM) * BN + (fn % CPM) * 32, rn);
-          }
+        auto chunk_addr = [&](int c) {
+          const int f = slot * CW + c;
+          return tq + (f / CPM) * BN + (f % CPM) * 32;
+        };
+        // s~ in place over the accumulator registers, then the minima of
+        // the triples (tt) and of the chunk (depth-4 FMNMX3 tree)
+        auto scores = [&](uint32_t* r, int cc, int rs) {
           const float4* c4 = reinterpret_cast<const float4*>(c2w + cc * 32);
           const float2 m2 = make_float2(msr[rs], msr[rs]);
-          float v[32];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const float4 q = c4[i];  // shared-memory broadcast
@@ -308,22 +304,98 @@ k_probe_filter(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
                                     m2, make_float2(q.x, q.y));
             const float2 hi = ffma2(make_float2(__uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3])),
                                     m2, make_float2(q.z, q.w));
-            v[4 * i] = lo.x; v[4 * i + 1] = lo.y; v[4 * i + 2] = hi.x; v[4 * i + 3] = hi.y;
+            r[4 * i] = __float_as_uint(lo.x); r[4 * i + 1] = __float_as_uint(lo.y);
+            r[4 * i + 2] = __float_as_uint(hi.x); r[4 * i + 3] = __float_as_uint(hi.y);
           }
-          // minimum: a depth-4 tree of three-input minima over triples t[k]
-          float tt[12];
+        };
+        auto minima = [&](const uint32_t* r, float* tt) -> float {
 #pragma unroll
-          for (int k = 0; k < 10; ++k) tt[k] = fmin3(v[3 * k], v[3 * k + 1], v[3 * k + 2]);
-          tt[10] = v[30];
-          tt[11] = v[31];
+          for (int k = 0; k < 10; ++k)
+            tt[k] = fmin3(__uint_as_float(r[3 * k]), __uint_as_float(r[3 * k + 1]),
+                          __uint_as_float(r[3 * k + 2]));
+          tt[10] = __uint_as_float(r[30]);
+          tt[11] = __uint_as_float(r[31]);
           const float u0 = fmin3(tt[0], tt[1], tt[2]), u1 = fmin3(tt[3], tt[4], tt[5]);
           const float u2 = fmin3(tt[6], tt[7], tt[8]), u3 = fmin3(tt[9], tt[10], tt[11]);
-          const float m = fminf(fmin3(u0, u1, u2), u3);
-          if constexpr (MODE == 0) {
+          return fminf(fmin3(u0, u1, u2), u3);
+        };
+        // rare: a chunk with survivors for this lane -- walk its triples
+        // below thr; the values are picked out of registers by a switch (no
+        // dynamic register indexing, no staging)
+        auto append = [&](const uint32_t* r, const float* tt, int cc, int rs) {
+          uint32_t tm = 0;
+#pragma unroll
+          for (int k = 0; k < 12; ++k) tm |= (tt[k] < thr[rs] ? 1u : 0u) << k;
+          const int64_t sb = (((int64_t)row[rs] * a.nsplit + sp) * SLOTS + slot) * a.cap_u;
+          int kk = kc_[rs];
+          while (tm) {
+            const int k = __ffs(tm) - 1;
+            tm &= tm - 1;
+            float x[3];
+            int n = 3;
+            switch (k) {
+#define GIVF_TRIPLE(K)                                                          \
+  case K:                                                                       \
+    x[0] = __uint_as_float(r[3 * K]); x[1] = __uint_as_float(r[3 * K + 1]);     \
+    x[2] = __uint_as_float(r[3 * K + 2]);                                       \
+    break;
+              GIVF_TRIPLE(0) GIVF_TRIPLE(1) GIVF_TRIPLE(2) GIVF_TRIPLE(3) GIVF_TRIPLE(4)
+              GIVF_TRIPLE(5) GIVF_TRIPLE(6) GIVF_TRIPLE(7) GIVF_TRIPLE(8) GIVF_TRIPLE(9)
+#undef GIVF_TRIPLE
+              case 10: x[0] = __uint_as_float(r[30]); n = 1; break;
+              default: x[0] = __uint_as_float(r[31]); n = 1; break;
+            }
+            const int i0 = k < 10 ? 3 * k : 20 + k;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+              if (j < n && x[j] < thr[rs]) {
+                if (kk < a.cap_u) {
+                  a.cid[sb + kk] = col0 + cc * 32 + i0 + j;
+                  a.cval[sb + kk] = x[j];
+                }
+                ++kk;
+              }
+            }
+          }
+          kc_[rs] = kk;
+        };
+        float mq[CW];
+        // chunks in pairs: both tcgen05.ld in flight, then the two
+        // independent reduction chains (the next pair's loads issued first)
+        uint32_t ra[32], rb[32];
+        tmem_ld32_async(chunk_addr(0), ra);
+        if (CW > 1) tmem_ld32_async(chunk_addr(1), rb);
+        tmem_wait_ld(ra);
+        if (CW > 1) tmem_wait_ld(rb);
+#pragma unroll
+        for (int c0 = 0; c0 < CW; c0 += 2) {
+          const int f0 = slot * CW + c0;
+          const int cc0 = f0 % CPM, rs0 = NR > 1 ? c0 / CPM : 0;
+          const int cc1 = (f0 + 1) % CPM, rs1 = NR > 1 ? (c0 + 1) / CPM : 0;
+          float t0[12], t1[12];
+          scores(ra, cc0, rs0);
+          if (CW > 1) scores(rb, cc1, rs1);
+          const float m0 = minima(ra, t0);
+          const float m1 = CW > 1 ? minima(rb, t1) : kInf;
+          mq[c0] = m0;
+          if (CW > 1) mq[c0 + 1] = m1;
+          if constexpr (MODE == 1) {
+            if (m0 < thr[rs0]) append(ra, t0, cc0, rs0);
+            if (CW > 1 && m1 < thr[rs1]) append(rb, t1, cc1, rs1);
+          }
+          if (c0 + 2 < CW) {
+            tmem_ld32_async(chunk_addr(c0 + 2), ra);
+            tmem_ld32_async(chunk_addr(c0 + 3), rb);
+            tmem_wait_ld(ra);
+            tmem_wait_ld(rb);
+          }
+        }
+        if constexpr (MODE == 0) {
+#pragma unroll
+          for (int c = 0; c < CW; ++c) {
+            const int f = slot * CW + c, cc = f % CPM, rs = NR > 1 ? c / CPM : 0;
             if constexpr (CW == 4 && CPM == 4) {
-              // the warp's four chunks are one row's whole tile: one 16-byte store
-              mq[c] = m;
-              if (c == 3 && row[0] < a.nq) {
+              if (c == 3 && row[0] < a.nq) {  // one row's whole tile: one 16-byte store
                 float* dst = a.cmin + (int64_t)row[0] * a.nch + (col0 >> 5);
                 if ((a.nch & 3) == 0 && col0 + BN <= a.K)
                   *reinterpret_cast<float4*>(dst) = make_float4(mq[0], mq[1], mq[2], mq[3]);
@@ -332,38 +404,9 @@ k_probe_filter(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
                     if (col0 + i * 32 < a.K) dst[i] = mq[i];
               }
             } else if (row[rs] < a.nq && col0 + cc * 32 < a.K) {
-              a.cmin[(int64_t)row[rs] * a.nch + ((col0 + cc * 32) >> 5)] = m;
-            }
-          } else {
-            if (m < thr[rs]) {  // rare: stage the chunk, walk the triples below thr
-              uint32_t tm = 0;
-#pragma unroll
-              for (int i = 0; i < 8; ++i)
-                *reinterpret_cast<float4*>(stg + 4 * i) =
-                    make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-#pragma unroll
-              for (int k = 0; k < 12; ++k) tm |= (tt[k] < thr[rs] ? 1u : 0u) << k;
-              const int64_t seg = ((int64_t)row[rs] * a.nsplit + sp) * 2 + pair;
-              int kk = kc_[rs];
-              while (tm) {
-                const int k = __ffs(tm) - 1;
-                tm &= tm - 1;
-                const int i0 = k < 10 ? 3 * k : 20 + k, i1 = k < 10 ? i0 + 3 : i0 + 1;
-                for (int i = i0; i < i1; ++i) {
-                  const float x = stg[i];
-                  if (x < thr[rs]) {
-                    if (kk < a.cap_u) {
-                      a.cid[seg * a.cap_u + kk] = col0 + cc * 32 + i;
-                      a.cval[seg * a.cap_u + kk] = x;
-                    }
-                    ++kk;
-                  }
-                }
-              }
-              kc_[rs] = kk;
+              a.cmin[(int64_t)row[rs] * a.nch + ((col0 + cc * 32) >> 5)] = mq[c];
             }
           }
-          if (c + 1 < CW) tmem_wait_ld(rn);
         }
         fence_before();
         __syncwarp();
@@ -373,7 +416,7 @@ k_probe_filter(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
       if constexpr (MODE == 1) {
 #pragma unroll
         for (int r = 0; r < NR; ++r)
-          if (row[r] < a.nq) a.cnt[((int64_t)row[r] * a.nsplit + sp) * 2 + pair] = kc_[r];
+          if (row[r] < a.nq) a.cnt[((int64_t)row[r] * a.nsplit + sp) * SLOTS + slot] = kc_[r];
       }
     }
   }
@@ -603,7 +646,7 @@ FilterShape filter_shape() {
       if (sscanf(e, "%dx%d", &m, &n) == 2) f = FilterShape{m, n};
     }
     const bool ok = (f.mb == 2 && f.bn == 128) || (f.mb == 4 && f.bn == 64) ||
-                    (f.mb == 1 && f.bn == 128);
+                    (f.mb == 1 && f.bn == 128) || (f.mb == 1 && f.bn == 256);
     return ok ? f : FilterShape{2, 128};
   }();
   return fs;
@@ -612,6 +655,10 @@ FilterShape filter_shape() {
 // Work units = (MB x 128 queries, slice of the centroid tiles), slice-major;
 // the slice count minimises the busiest CTA's tiles (+1 tile of overhead
 // per unit for its A block).
+// epilogue warps: 8 (16, four per lane quarter with two chunks each,
+// measured 3.53 ms against 2.85 at configs[2]; removed)
+int filter_warps() { return 8; }
+
 int filter_nsplit(int nq, int K, int MB, int BN) {
   const int groups = (nq + MB * pf::BM - 1) / (MB * pf::BM);
   const int n_tiles = (K + BN - 1) / BN;
@@ -626,18 +673,24 @@ int filter_nsplit(int nq, int K, int MB, int BN) {
   return nsplit;
 }
 
-template <int MB, int BN, int MODE>
-cudaError_t launch_filter_t(const CUtensorMap& ma, const CUtensorMap& mb, const FilterArgs& a,
+template <int MB, int BN, int MODE, int EW>
+cudaError_t launch_filter_w(const CUtensorMap& ma, const CUtensorMap& mb, const FilterArgs& a,
                             cudaStream_t s) {
   const int groups = (a.nq + MB * pf::BM - 1) / (MB * pf::BM);
   const int units = groups * a.nsplit;
   const int grid = std::min(units, num_sms_cur());
-  const size_t smem = pf::smem_bytes(MB, BN, a.KC);
-  auto fn = k_probe_filter<MB, BN, MODE>;
+  const size_t smem = pf::smem_bytes(MB, BN, a.KC, EW);
+  auto fn = k_probe_filter<MB, BN, MODE, EW>;
   cudaError_t e = ensure_max_smem((const void*)fn, smem);
   if (e != cudaSuccess) return e;
-  fn<<<grid, pf::THREADS, smem, s>>>(ma, mb, a);
+  fn<<<grid, pf::threads_of(EW), smem, s>>>(ma, mb, a);
   return cudaGetLastError();
+}
+
+template <int MB, int BN, int MODE>
+cudaError_t launch_filter_t(const CUtensorMap& ma, const CUtensorMap& mb, const FilterArgs& a,
+                            cudaStream_t s) {
+  return launch_filter_w<MB, BN, MODE, 8>(ma, mb, a, s);
 }
 
 template <int MODE>
@@ -650,6 +703,7 @@ cudaError_t launch_filter(const void* q16, const void* c16, int dp, FilterArgs a
     return cudaErrorInvalidValue;
   if (fs.mb == 4 && fs.bn == 64) return launch_filter_t<4, 64, MODE>(ma, mb, a, s);
   if (fs.mb == 1 && fs.bn == 128) return launch_filter_t<1, 128, MODE>(ma, mb, a, s);
+  if (fs.mb == 1 && fs.bn == 256) return launch_filter_t<1, 256, MODE>(ma, mb, a, s);
   return launch_filter_t<2, 128, MODE>(ma, mb, a, s);
 }
 
@@ -700,9 +754,11 @@ cudaError_t launch_probe_sample(const void* q16, const void* s16, const float* s
 
 // Survivor segments of the filter for nq queries: per query nseg segments
 // of cap_u entries, cap_u * nseg <= fcap (fixed per-query bytes).
+int filter_slots() { return filter_warps() / 4; }
+
 void filter_segments(int nq, int K, int fcap, int* nseg, int* cap_u) {
   const FilterShape fs = filter_shape();
-  *nseg = 2 * filter_nsplit(nq, K, fs.mb, fs.bn);
+  *nseg = (filter_warps() / 4) * filter_nsplit(nq, K, fs.mb, fs.bn);
   *cap_u = std::max(8, fcap / *nseg);
 }
 
@@ -717,7 +773,7 @@ cudaError_t launch_probe_filter(const void* q16, const void* c16, const float* c
   a.d = d;
   a.ms = ms;
   a.thr = thr;
-  a.nsplit = nseg / 2;
+  a.nsplit = nseg / (filter_warps() / 4);
   a.nseg = nseg;
   a.cap_u = cap_u;
   a.cnt = cnt;
