@@ -428,13 +428,13 @@ int run_probe(givf_index* ix, const Plan& pl, const float* dQ, int nq, int* regi
     const float eps = probe_f16_eps(d);
     cudaError_t ce = cudaSuccess;
     staged(ST_SAMPLE, st, [&] {
-      launch_query_f16(dQ, nq, d, v.c16x, q16, ms, q2f, st);
-      ce = launch_probe_sample(q16, v.s16, v.sc2, nq, v.Ks, d, ms, cmin, st);
+      launch_query_f16(dQ, nq, d, v.c16e, v.c16T, q16, ms, q2f, st);
+      ce = launch_probe_sample(q16, v.s16, nq, v.Ks, d, ms, cmin, st);
       launch_probe_thresh(cmin, nch, ps.fj, q2f, v.cmax, eps, nq, thr, st);
     }, 3);
     if (ce != cudaSuccess) return fail(GIVF_ECUDA, std::string("probe sample: ") + cudaGetErrorString(ce));
     staged(ST_GEMM, st, [&] {
-      ce = launch_probe_filter(q16, v.c16, v.c2f, nq, K, d, ms, thr, nseg, cap_u, cnt, cid, cval,
+      ce = launch_probe_filter(q16, v.c16, nq, K, d, ms, thr, nseg, cap_u, cnt, cid, cval,
                                st);
     });
     if (ce != cudaSuccess) return fail(GIVF_ECUDA, std::string("probe filter: ") + cudaGetErrorString(ce));
@@ -485,11 +485,11 @@ int run_probe(givf_index* ix, const Plan& pl, const float* dQ, int nq, int* regi
           const int* gidx = fidx + f0;
           staged(ST_SAMPLE, st, [&] {
             launch_gather_rows(dQ, gidx, gn, d, qr, st);
-            launch_query_f16(qr, gn, d, v.c16x, q16, ms, q2f, st);
+            launch_query_f16(qr, gn, d, v.c16e, v.c16T, q16, ms, q2f, st);
             launch_probe_thresh(cmin, nch, P, q2f, v.cmax, eps, gn, thr, st, gidx);
           }, 3);
           staged(ST_GEMM, st, [&] {
-            ce = launch_probe_filter(q16, v.c16, v.c2f, gn, K, d, ms, thr, nseg_r, cap_u_r, cnt,
+            ce = launch_probe_filter(q16, v.c16, gn, K, d, ms, thr, nseg_r, cap_u_r, cnt,
                                      cid, cval, st);
           });
           if (ce != cudaSuccess)
@@ -1043,12 +1043,19 @@ int givf_index_create(const givf_index_desc* ds, int device, givf_index_t* out) 
   }
   if (e == cudaSuccess && fused_supported(d)) {
     // fused probe (probe_fused.cu): fp16 centroids scaled by 2^-ec (max
-    // |c_ij| in [2^13, 2^14)), and a seeded random sample of them
+    // |c_ij| in [2^7, 2^8)) with the |c|^2 columns scaled by 2^-T so that
+    // the largest b = |c|^2 2^-(1 + ec + T) is below 2^14, and a seeded
+    // random sample of the rows
     float amax = 0.f;
+    double c2max = 0.0;
     for (size_t i = 0; i < (size_t)K * d; ++i) amax = std::max(amax, std::fabs(ds->centroids[i]));
-    const int ec = amax > 0.f ? std::ilogb(amax) - 13 : 0;
+    for (int r = 0; r < K; ++r) c2max = std::max(c2max, (double)c2f[r]);
+    const int ec = amax > 0.f ? std::ilogb(amax) - 7 : 0;
+    const double bmax = std::ldexp(c2max, -(1 + ec));
+    const int T = bmax > 0.0 ? std::ilogb(bmax) + 1 - 14 : 0;
     v.c16e = ec;
     v.c16x = std::ldexp(1.0f, ec);
+    v.c16T = T;
     const int dp = f16_pitch(d);
     // sample: every centroid up to 8192, else K/16 (at most 2^16); its
     // j-th smallest chunk minimum aims the threshold at ~3P + 128 survivors
@@ -1065,21 +1072,26 @@ int givf_index_create(const givf_index_desc* ds, int device, givf_index_t* out) 
       }
       std::sort(ids.begin(), ids.begin() + Ks);
     }
-    void *c16 = nullptr, *s16 = nullptr;
+    void *c16 = nullptr, *s16 = nullptr, *c16r = nullptr;
     float* sc2 = nullptr;
     const int32_t* dids = nullptr;
     const size_t cb = (size_t)K * dp * 2, sb = (size_t)Ks * dp * 2;
-    e = cudaMalloc(&c16, cb);
+    const size_t rb = (size_t)K * f16_row_pitch(d) * 2;
+    e = cudaMalloc(&c16r, rb);
+    if (e == cudaSuccess) { ix->allocs.push_back(c16r); ix->dev_bytes += (int64_t)rb; }
+    if (e == cudaSuccess) e = cudaMalloc(&c16, cb);
     if (e == cudaSuccess) { ix->allocs.push_back(c16); ix->dev_bytes += (int64_t)cb; e = cudaMalloc(&s16, sb); }
     if (e == cudaSuccess) { ix->allocs.push_back(s16); ix->dev_bytes += (int64_t)sb; e = cudaMalloc(&sc2, (size_t)Ks * 4 + 16); }
     if (e == cudaSuccess) { ix->allocs.push_back(sc2); e = upload(ix, ids.data(), (size_t)Ks, &dids); }
     if (e == cudaSuccess) {
-      launch_rows_f16(v.centroids, nullptr, K, d, ec, c16, nullptr, nullptr, 0);
-      launch_rows_f16(v.centroids, dids, Ks, d, ec, s16, v.c2f, sc2, 0);
+      launch_rows_f16(v.centroids, nullptr, K, d, ec, T, v.c2f, c16, nullptr, 0);
+      launch_rows_f16(v.centroids, nullptr, K, d, ec, T, v.c2f, c16r, nullptr, 0, f16_row_pitch(d));
+      launch_rows_f16(v.centroids, dids, Ks, d, ec, T, v.c2f, s16, sc2, 0);
       e = cudaDeviceSynchronize();
     }
     if (e == cudaSuccess) {
       v.c16 = c16;
+      v.c16r = c16r;
       v.s16 = s16;
       v.sc2 = sc2;
       v.Ks = Ks;
@@ -1283,8 +1295,8 @@ int givf_probe_scores(givf_index_t ix, const float* queries, int64_t nq, float* 
     ARENA_CHECK(ar);
     std::vector<float> inf((size_t)nq, INFINITY);
     CUDA_TRY(cudaMemcpyAsync(thr, inf.data(), sizeof(float) * nq, cudaMemcpyHostToDevice, st));
-    launch_query_f16(dQ, (int)nq, d, v.c16x, q16, ms, nullptr, st);
-    cudaError_t ce = launch_probe_filter(q16, v.c16, v.c2f, (int)nq, K, d, ms, thr, nseg, cap_u,
+    launch_query_f16(dQ, (int)nq, d, v.c16e, v.c16T, q16, ms, nullptr, st);
+    cudaError_t ce = launch_probe_filter(q16, v.c16, (int)nq, K, d, ms, thr, nseg, cap_u,
                                          cnt, cid, cval, st);
     if (ce != cudaSuccess) return fail(GIVF_ECUDA, std::string("probe filter: ") + cudaGetErrorString(ce));
     g_launches += 2;

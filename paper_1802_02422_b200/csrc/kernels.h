@@ -50,10 +50,13 @@ struct IndexView {
   const float* rotation;      // (d, d) or null
   const float* ctab;          // (256) dequantized constants, f32
   const void* csplit;         // (K, tc_kpad_b(d)) bf16 [c_hi | c_lo] or null
-  // fused probe (probe_fused.cu): fp16 centroids c 2^-c16e, pitch f16_pitch(d)
+  // fused probe (probe_fused.cu): fp16 centroids c 2^-c16e, pitch f16_pitch(d),
+  // columns d, d+1: -|c|^2 2^-(1 + ec + T) as an fp16 hi + lo pair
   const void* c16;            // (K, dp) or null
   int c16e;                   // scale exponent ec
   float c16x;                 // 2^ec
+  int c16T;                   // T
+  const void* c16r;           // (K, f16_row_pitch(d)) the same fp16 coordinates, K3a's rows
   const void* s16;            // (Ks, dp) fp16 rows of a random centroid sample
   const float* sc2;           // (Ks) their f32 |c|^2
   int Ks;
@@ -92,17 +95,20 @@ int f16_pitch(int d);
 bool fused_supported(int d);
 float probe_f16_eps(int d);   // GEMM bound, units of cmax^2 + 2 |q| cmax
 float direct_f16_eps(int d);  // K3a-from-fp16-rows bound, same units
-void launch_rows_f16(const float* x, const int32_t* ids, int64_t rows, int d, int e, void* out,
-                     const float* c2in, float* c2out, cudaStream_t s);
-void launch_query_f16(const float* Q, int nq, int d, float cexp, void* q16, float* ms, float* q2,
-                      cudaStream_t s);
-cudaError_t launch_probe_sample(const void* q16, const void* s16, const float* sc2, int nq, int Ks,
-                                int d, const float* ms, float* cmin, cudaStream_t s);
+// dp = row pitch (0: f16_pitch(d), with the |c|^2 columns; d rounded up
+// to 32: the coordinates only, for K3a's row reads)
+void launch_rows_f16(const float* x, const int32_t* ids, int64_t rows, int d, int e, int T,
+                     const float* c2, void* out, float* c2out, cudaStream_t s, int dp = 0);
+__host__ __device__ inline int f16_row_pitch(int d) { return ((d + 31) / 32) * 32; }
+void launch_query_f16(const float* Q, int nq, int d, int ec, int T, void* q16, float* ms,
+                      float* q2, cudaStream_t s);
+cudaError_t launch_probe_sample(const void* q16, const void* s16, int nq, int Ks, int d,
+                                const float* ms, float* cmin, cudaStream_t s);
 void filter_segments(int nq, int K, int fcap, int* nseg, int* cap_u);
 int filter_slots();  // survivor segments per (query, work unit)
-cudaError_t launch_probe_filter(const void* q16, const void* c16, const float* c2, int nq, int K,
-                                int d, const float* ms, const float* thr, int nseg, int cap_u,
-                                int* cnt, int* cid, float* cval, cudaStream_t s);
+cudaError_t launch_probe_filter(const void* q16, const void* c16, int nq, int K, int d,
+                                const float* ms, const float* thr, int nseg, int cap_u, int* cnt,
+                                int* cid, float* cval, cudaStream_t s);
 void launch_probe_thresh(const float* cmin, int nch, int j, const float* q2, float cmax,
                          float eps_scale, int nq, float* thr, cudaStream_t s,
                          const int* qmap = nullptr);

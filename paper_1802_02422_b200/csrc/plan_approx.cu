@@ -95,6 +95,8 @@ __global__ void __launch_bounds__(PA_THREADS) k_plan_scores_approx(PlanArgs a) {
 // d = 96) and the float32 query, float32 dot product; error bound
 // direct_f16_eps (units of cmax^2 + 2 |q| cmax), no storage term (half_rel 0).
 // One warp per (query, probed region) as above, a lane per group.
+// DP8: 16-byte chunks read per row (d coordinates, zero-padded in the
+// query's shared copy); rows from ix.c16r (pitch f16_row_pitch(d))
 template <int DP8>
 __global__ void __launch_bounds__(PA_THREADS) k_plan_scores_direct(PlanArgs a) {
   __shared__ __align__(16) float qsm[PA_THREADS / 32][DP8 * 8];
@@ -125,13 +127,14 @@ __global__ void __launch_bounds__(PA_THREADS) k_plan_scores_direct(PlanArgs a) {
   const double al = (double)ix.alphas[r];
   const double oma_qc = dmul(dsub(1.0, al), qc);
   const double cx2 = 2.0 * (double)ix.c16x;
-  const uint4* C16 = reinterpret_cast<const uint4*>(ix.c16);
+  const uint4* C16 = reinterpret_cast<const uint4*>(ix.c16r);
+  const int64_t rstride = f16_row_pitch(d) / 8;  // row pitch in 16-byte chunks
   const float4* q4 = reinterpret_cast<const float4*>(qs);
   for (int j = lane; j < G; j += 32) {
     const int64_t g = (int64_t)r * G + j;
     const int n = __ldg(ix.nbr + g);
     const float m = __ldg(ix.norm + g);
-    const uint4* row = C16 + (int64_t)n * DP8;
+    const uint4* row = C16 + (int64_t)n * rstride;
     uint4 u[DP8];
 #pragma unroll
     for (int c = 0; c < DP8; ++c) u[c] = __ldg(row + c);
@@ -879,7 +882,7 @@ int launch_plan_scores(const PlanArgs& a, cudaStream_t s) {
   const int per = PA_THREADS / 32;
   const unsigned grid = (unsigned)((warps + per - 1) / per);
   if (a.direct) {
-    switch (f16_pitch(a.ix.d) / 32) {
+    switch ((a.ix.d + 31) / 32) {  // 32-coordinate chunks of a row
       case 1: k_plan_scores_direct<4><<<grid, PA_THREADS, 0, s>>>(a); break;
       case 2: k_plan_scores_direct<8><<<grid, PA_THREADS, 0, s>>>(a); break;
       case 3: k_plan_scores_direct<12><<<grid, PA_THREADS, 0, s>>>(a); break;

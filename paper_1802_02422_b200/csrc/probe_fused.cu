@@ -60,12 +60,11 @@ constexpr int BM = 128, BK = 32;  // BK fp16 = 64 B = one SWIZZLE_64B row
 constexpr int NS_MAX = 4;         // centroid-tile ring depth
 // Epilogue warps: EW = 8, two per TMEM lane quarter (a template parameter;
 // 16 measured slower, see filter_warps).
-constexpr int EW_MAX = 16;
 __host__ __device__ constexpr int threads_of(int ew) { return 64 + 32 * ew; }
 constexpr uint32_t A_CHUNK = BM * BK * 2;  // 8 KB
 constexpr int TMEM_COLS = 512;             // 512 / (MB * BN) accumulator buffers
 constexpr int NBUF_MAX = 4;
-constexpr int KC_MAX = 4;                  // d <= 128
+constexpr int KC_MAX = 5;                  // d + 2 <= 160 (the |c|^2 columns)
 // kind::f16 instruction descriptor, fp16 x fp16 -> f32, both K-major
 constexpr uint32_t idesc_f16(int m, int n) {
   return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
@@ -83,17 +82,16 @@ __host__ __device__ constexpr int ring(int mb, int bn, int kc) {
        : (size_t)mb * kc * A_CHUNK + (size_t)3 * kc * b_chunk(bn) <= 180 * 1024       ? 3
                                                                                        : 2;
 }
-// [A block][B ring][|c|^2 per warp][barriers]
+// [A block][B ring][barriers]
 __host__ __device__ constexpr size_t smem_bytes(int mb, int bn, int kc, int ew) {
   return 1024 + (size_t)mb * kc * A_CHUNK + (size_t)ring(mb, bn, kc) * kc * b_chunk(bn) +
-         (size_t)ew * 256 * 4 + sizeof(Smem) + 64;
+         sizeof(Smem) + 64 + 0 * ew;
 }
 }  // namespace pf
 
 struct FilterArgs {
-  const float* c2;   // (K) f32 |c|^2 of the B rows
-  int nq, K, KC, d, nsplit;
-  const float* ms;   // (nq) -2^(1 + eq + ec): s~ = fma(acc, ms, c2)
+  int nq, K, KC, d, nsplit;  // d: MMA depth = dim + 2 (the |c|^2 columns)
+  const float* ms;   // (nq) -2^(1 + eq + ec): s~ = ms * acc (exact, a power of two)
   // MODE 0: chunk minima
   float* cmin;       // (nq, nch)
   int nch;
@@ -114,6 +112,11 @@ GIVF_DEV float2 ffma2(float2 a, float2 b, float2 c) {
         "l"(*reinterpret_cast<unsigned long long*>(&b)),
         "l"(*reinterpret_cast<unsigned long long*>(&c)));
   return *reinterpret_cast<float2*>(&r);
+}
+GIVF_DEV float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
 }
 GIVF_DEV float fmin3(float a, float b, float c) {
   float r;
@@ -145,8 +148,7 @@ k_probe_filter(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
   const int NS = ring(MB, BN, KC);
   unsigned char* smA = base;
   unsigned char* smB = base + (size_t)MB * KC * A_CHUNK;
-  float* c2all = reinterpret_cast<float*>(smB + (size_t)NS * KC * B_CHUNK);
-  Smem* sm = reinterpret_cast<Smem*>(c2all + EW * 256);
+  Smem* sm = reinterpret_cast<Smem*>(smB + (size_t)NS * KC * B_CHUNK);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int groups = (a.nq + MB * BM - 1) / (MB * BM);
@@ -254,78 +256,62 @@ k_probe_filter(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
     const int e = warp - 2;
     const int quarter = warp & 3;
     const int slot = e >> 2;
-    float* c2w = c2all + e * 256;
     uint32_t acc = 0, acc_phase = 0;
     const float kInf = __int_as_float(0x7f800000);
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int g = u % groups, sp = u / groups;
       const int t0 = sp * per_split, t1 = min(n_tiles, t0 + per_split);
       if (t0 >= t1) continue;
+      // s~ = ms * acc with ms = -2^k: s~ < thr  <=>  acc > thr / ms (exact)
       int row[NR], kc_[NR];
-      float msr[NR], thr[NR];
+      float msr[NR], tr[NR];
 #pragma unroll
       for (int r = 0; r < NR; ++r) {
         const int mb = (slot * CW + r * CPM) / CPM;
         row[r] = (g * MB + mb) * BM + quarter * 32 + lane;
         const bool ok = row[r] < a.nq;
-        msr[r] = ok ? a.ms[row[r]] : 0.f;
-        if constexpr (MODE == 1) thr[r] = ok ? a.thr[row[r]] : -kInf;
-        else thr[r] = 0.f;
+        msr[r] = ok ? a.ms[row[r]] : -1.f;
+        if constexpr (MODE == 1) tr[r] = ok ? a.thr[row[r]] / msr[r] : kInf;
+        else tr[r] = 0.f;
         kc_[r] = 0;
       }
       for (int t = t0; t < t1; ++t) {
         const int col0 = t * BN;
-        // the tile's |c|^2 terms, fetched before the accumulator wait
-        float cr[CPM];
-#pragma unroll
-        for (int i = 0; i < CPM; ++i) {
-          const int col = col0 + i * 32 + lane;
-          cr[i] = col < a.K ? __ldg(a.c2 + col) : kInf;
-        }
         mbar_wait(&sm->tm_full[acc], acc_phase);
         fence_after();
-#pragma unroll
-        for (int i = 0; i < CPM; ++i) c2w[i * 32 + lane] = cr[i];
-        __syncwarp();
         const uint32_t tq = tmem + ((uint32_t)(quarter * 32) << 16) + acc * TC;
         auto chunk_addr = [&](int c) {
           const int f = slot * CW + c;
           return tq + (f / CPM) * BN + (f % CPM) * 32;
         };
-        // s~ in place over the accumulator registers, then the minima of
-        // the triples (tt) and of the chunk (depth-4 FMNMX3 tree)
-        auto scores = [&](uint32_t* r, int cc, int rs) {
-          const float4* c4 = reinterpret_cast<const float4*>(c2w + cc * 32);
-          const float2 m2 = make_float2(msr[rs], msr[rs]);
+        // columns past K (the last tile): -inf, never a maximum or a survivor
+        auto clip = [&](uint32_t* r, int cc) {
+          const int c0 = col0 + cc * 32;
+          if (c0 + 32 > a.K) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float4 q = c4[i];  // shared-memory broadcast
-            const float2 lo = ffma2(make_float2(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1])),
-                                    m2, make_float2(q.x, q.y));
-            const float2 hi = ffma2(make_float2(__uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3])),
-                                    m2, make_float2(q.z, q.w));
-            r[4 * i] = __float_as_uint(lo.x); r[4 * i + 1] = __float_as_uint(lo.y);
-            r[4 * i + 2] = __float_as_uint(hi.x); r[4 * i + 3] = __float_as_uint(hi.y);
+            for (int i = 0; i < 32; ++i)
+              if (c0 + i >= a.K) r[i] = __float_as_uint(-kInf);
           }
         };
-        auto minima = [&](const uint32_t* r, float* tt) -> float {
+        // maxima of the triples (tt) and of the chunk: depth-4 FMNMX3 tree
+        auto maxima = [&](const uint32_t* r, float* tt) -> float {
 #pragma unroll
           for (int k = 0; k < 10; ++k)
-            tt[k] = fmin3(__uint_as_float(r[3 * k]), __uint_as_float(r[3 * k + 1]),
+            tt[k] = fmax3(__uint_as_float(r[3 * k]), __uint_as_float(r[3 * k + 1]),
                           __uint_as_float(r[3 * k + 2]));
           tt[10] = __uint_as_float(r[30]);
           tt[11] = __uint_as_float(r[31]);
-          const float u0 = fmin3(tt[0], tt[1], tt[2]), u1 = fmin3(tt[3], tt[4], tt[5]);
-          const float u2 = fmin3(tt[6], tt[7], tt[8]), u3 = fmin3(tt[9], tt[10], tt[11]);
-          return fminf(fmin3(u0, u1, u2), u3);
+          const float u0 = fmax3(tt[0], tt[1], tt[2]), u1 = fmax3(tt[3], tt[4], tt[5]);
+          const float u2 = fmax3(tt[6], tt[7], tt[8]), u3 = fmax3(tt[9], tt[10], tt[11]);
+          return fmaxf(fmax3(u0, u1, u2), u3);
         };
         // rare: a chunk with survivors for this lane -- walk its triples
-        // below thr; the values are picked out of registers by a switch (no
-        // dynamic register indexing, no staging)
+        // above tr; values picked out of registers by a switch (no dynamic
+        // register indexing, no staging)
         auto append = [&](const uint32_t* r, const float* tt, int cc, int rs) {
           uint32_t tm = 0;
 #pragma unroll
-          for (int k = 0; k < 12; ++k) tm |= (tt[k] < thr[rs] ? 1u : 0u) << k;
+          for (int k = 0; k < 12; ++k) tm |= (tt[k] > tr[rs] ? 1u : 0u) << k;
           const int64_t sb = (((int64_t)row[rs] * a.nsplit + sp) * SLOTS + slot) * a.cap_u;
           int kk = kc_[rs];
           while (tm) {
@@ -348,10 +334,10 @@ k_probe_filter(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
             const int i0 = k < 10 ? 3 * k : 20 + k;
 #pragma unroll
             for (int j = 0; j < 3; ++j) {
-              if (j < n && x[j] < thr[rs]) {
+              if (j < n && x[j] > tr[rs]) {
                 if (kk < a.cap_u) {
                   a.cid[sb + kk] = col0 + cc * 32 + i0 + j;
-                  a.cval[sb + kk] = x[j];
+                  a.cval[sb + kk] = x[j] * msr[rs];  // exact: ms is a power of two
                 }
                 ++kk;
               }
@@ -360,34 +346,27 @@ k_probe_filter(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
           kc_[rs] = kk;
         };
         float mq[CW];
-        // chunks in pairs: both tcgen05.ld in flight, then the two
-        // independent reduction chains (the next pair's loads issued first)
-        uint32_t ra[32], rb[32];
-        tmem_ld32_async(chunk_addr(0), ra);
-        if (CW > 1) tmem_ld32_async(chunk_addr(1), rb);
-        tmem_wait_ld(ra);
-        if (CW > 1) tmem_wait_ld(rb);
+        // every chunk of this warp into registers, the accumulator buffer
+        // released at once (the MMA refills it while the chunks are reduced),
+        // then independent max trees; nothing else per score (|c|^2 came
+        // through the MMA)
+        uint32_t rr[CW][32];
 #pragma unroll
-        for (int c0 = 0; c0 < CW; c0 += 2) {
-          const int f0 = slot * CW + c0;
-          const int cc0 = f0 % CPM, rs0 = NR > 1 ? c0 / CPM : 0;
-          const int cc1 = (f0 + 1) % CPM, rs1 = NR > 1 ? (c0 + 1) / CPM : 0;
-          float t0[12], t1[12];
-          scores(ra, cc0, rs0);
-          if (CW > 1) scores(rb, cc1, rs1);
-          const float m0 = minima(ra, t0);
-          const float m1 = CW > 1 ? minima(rb, t1) : kInf;
-          mq[c0] = m0;
-          if (CW > 1) mq[c0 + 1] = m1;
+        for (int c = 0; c < CW; ++c) tmem_ld32_async(chunk_addr(c), rr[c]);
+#pragma unroll
+        for (int c = 0; c < CW; ++c) tmem_wait_ld(rr[c]);
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm->tm_empty[acc]);
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+          const int f = slot * CW + c, cc = f % CPM, rs = NR > 1 ? c / CPM : 0;
+          float tt[12];
+          clip(rr[c], cc);
+          const float m = maxima(rr[c], tt);
+          mq[c] = m * msr[rs];  // the chunk's smallest s~
           if constexpr (MODE == 1) {
-            if (m0 < thr[rs0]) append(ra, t0, cc0, rs0);
-            if (CW > 1 && m1 < thr[rs1]) append(rb, t1, cc1, rs1);
-          }
-          if (c0 + 2 < CW) {
-            tmem_ld32_async(chunk_addr(c0 + 2), ra);
-            tmem_ld32_async(chunk_addr(c0 + 3), rb);
-            tmem_wait_ld(ra);
-            tmem_wait_ld(rb);
+            if (m > tr[rs]) append(rr[c], tt, cc, rs);
           }
         }
         if constexpr (MODE == 0) {
@@ -408,9 +387,6 @@ k_probe_filter(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
             }
           }
         }
-        fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm->tm_empty[acc]);
         if (++acc == NBUF) { acc = 0; acc_phase ^= 1; }
       }
       if constexpr (MODE == 1) {
@@ -430,8 +406,13 @@ k_probe_filter(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
 }
 
 // ------------------------------------------------------------------ F0
-// One warp per query.
-__global__ void k_query_f16(const float* __restrict__ Q, int nq, int d, int dp, float cexp,
+// One warp per query: q' = q 2^-eq (max |q'_i| in [2^7, 2^8)), then in the
+// two |c|^2 columns a = 2^(T - eq); the centroid rows hold there b_hi + b_lo
+// = -|c|^2 2^-(1 + ec + T), so the MMA accumulates q'.c' - |c|^2 2^-(1+eq+ec)
+// and s~ = ms * acc with ms = -2^(1 + eq + ec).  A query whose a falls
+// outside fp16's normal range gets ms = NaN: no survivors, it takes the
+// exhaustive probe.
+__global__ void k_query_f16(const float* __restrict__ Q, int nq, int d, int dp, int ec, int T,
                             __half* __restrict__ q16, float* __restrict__ ms,
                             float* __restrict__ q2o) {
   const int lane = threadIdx.x & 31;
@@ -447,28 +428,43 @@ __global__ void k_query_f16(const float* __restrict__ Q, int nq, int d, int dp, 
   }
   mx = warp_max(mx);
   s = warp_sum(s);
-  const int eq = mx > 0.f ? ilogbf(mx) - 13 : 0;
-  for (int j = lane; j < dp; j += 32)
-    q16[(int64_t)b * dp + j] = __float2half_rn(j < d ? ldexpf(q[j], -eq) : 0.f);
+  const int eq = mx > 0.f ? ilogbf(mx) - 7 : 0;
+  const int ae = T - eq;
+  const bool ok = ae >= -14 && ae <= 15;
+  for (int j = lane; j < dp; j += 32) {
+    float x = 0.f;
+    if (j < d) x = ldexpf(q[j], -eq);
+    else if (j < d + 2) x = ok ? ldexpf(1.f, ae) : 0.f;
+    q16[(int64_t)b * dp + j] = __float2half_rn(x);
+  }
   if (lane == 0) {
-    ms[b] = -ldexpf(cexp, eq + 1);  // -2^(1 + eq) * 2^ec
+    ms[b] = ok ? -ldexpf(1.f, eq + ec + 1) : __int_as_float(0x7fc00000);
     if (q2o) q2o[b] = (float)s;
   }
 }
 
-// fp16 copy of rows (scaled by 2^-e, zero-padded to dp columns), optionally
-// of a subset of rows (ids) with their |c|^2.
+// fp16 copy of rows c 2^-ec (zero-padded to dp columns) with the |c|^2
+// columns b_hi, b_lo (b = -|c|^2 2^-(1 + ec + T)), optionally of a subset of
+// rows (ids) with their |c|^2.
 __global__ void k_rows_f16(const float* __restrict__ x, const int32_t* __restrict__ ids,
-                           int64_t rows, int d, int dp, int e, __half* __restrict__ out,
-                           const float* __restrict__ c2in, float* __restrict__ c2out) {
+                           int64_t rows, int d, int dp, int e, int T, const float* __restrict__ c2,
+                           __half* __restrict__ out, float* __restrict__ c2out) {
   const int64_t n = rows * dp;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / dp;
     const int c = (int)(i % dp);
     const int64_t src = ids ? (int64_t)ids[r] : r;
-    out[i] = __float2half_rn(c < d ? ldexpf(x[src * d + c], -e) : 0.f);
-    if (c == 0 && c2out) c2out[r] = c2in[src];
+    __half h = __float2half_rn(0.f);
+    if (c < d) {
+      h = __float2half_rn(ldexpf(x[src * d + c], -e));
+    } else if (c < d + 2 && dp >= d + 2) {
+      const double bv = -ldexp((double)c2[src], -(1 + e + T));
+      const __half hi = __double2half(bv);
+      h = c == d ? hi : __double2half(bv - (double)__half2float(hi));
+    }
+    out[i] = h;
+    if (c == 0 && c2out) c2out[r] = c2[src];
   }
 }
 
@@ -709,11 +705,13 @@ cudaError_t launch_filter(const void* q16, const void* c16, int dp, FilterArgs a
 
 }  // namespace
 
-int f16_pitch(int d) { return ((d + 31) / 32) * 32; }
-bool fused_supported(int d) { return d >= 1 && d <= 32 * pf::KC_MAX; }
+int f16_pitch(int d) { return ((d + 2 + 31) / 32) * 32; }  // + the two |c|^2 columns
+bool fused_supported(int d) { return d >= 1 && d + 2 <= 32 * pf::KC_MAX; }
 float probe_f16_eps(int d) {
   const double u2 = std::ldexp(1.0, -10);  // 2u, u = 2^-11
-  const double acc = (double)((d + 15) / 16 + 16) * std::ldexp(1.0, -22) * 1.001;
+  // fp32 tensor-core accumulation over the d + 2 terms; the b_hi + b_lo
+  // split carries |c|^2 to 2^-22 (the separate 2^-22 term below)
+  const double acc = (double)((d + 2 + 15) / 16 + 16) * std::ldexp(1.0, -22) * 1.001;
   return (float)(1.25 * (u2 + std::ldexp(1.0, -22) + acc + std::ldexp(1.0, -23)));
 }
 // K3a from fp16 centroid rows and f32 queries: |qs2~ - qs2| <= eps U with
@@ -722,30 +720,29 @@ float direct_f16_eps(int d) {
   return (float)(1.25 * (std::ldexp(1.0, -11) + (double)(d + 4) * std::ldexp(1.0, -24)));
 }
 
-void launch_rows_f16(const float* x, const int32_t* ids, int64_t rows, int d, int e, void* out,
-                     const float* c2in, float* c2out, cudaStream_t s) {
-  const int dp = f16_pitch(d);
+void launch_rows_f16(const float* x, const int32_t* ids, int64_t rows, int d, int e, int T,
+                     const float* c2, void* out, float* c2out, cudaStream_t s, int dp) {
+  if (dp <= 0) dp = f16_pitch(d);
   const int64_t n = rows * dp;
   const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms_cur() * 16);
-  k_rows_f16<<<std::max(blocks, 1), 256, 0, s>>>(x, ids, rows, d, dp, e,
-                                                  reinterpret_cast<__half*>(out), c2in, c2out);
+  k_rows_f16<<<std::max(blocks, 1), 256, 0, s>>>(x, ids, rows, d, dp, e, T, c2,
+                                                  reinterpret_cast<__half*>(out), c2out);
 }
 
-void launch_query_f16(const float* Q, int nq, int d, float cexp, void* q16, float* ms, float* q2,
-                      cudaStream_t s) {
+void launch_query_f16(const float* Q, int nq, int d, int ec, int T, void* q16, float* ms,
+                      float* q2, cudaStream_t s) {
   const int per = 8;
   k_query_f16<<<(nq + per - 1) / per, per * 32, 0, s>>>(
-      Q, nq, d, f16_pitch(d), cexp, reinterpret_cast<__half*>(q16), ms, q2);
+      Q, nq, d, f16_pitch(d), ec, T, reinterpret_cast<__half*>(q16), ms, q2);
 }
 
-cudaError_t launch_probe_sample(const void* q16, const void* s16, const float* sc2, int nq, int Ks,
-                                int d, const float* ms, float* cmin, cudaStream_t s) {
+cudaError_t launch_probe_sample(const void* q16, const void* s16, int nq, int Ks, int d,
+                                const float* ms, float* cmin, cudaStream_t s) {
   FilterArgs a{};
-  a.c2 = sc2;
   a.nq = nq;
   a.K = Ks;
   a.KC = f16_pitch(d) / 32;
-  a.d = d;
+  a.d = d + 2;
   a.ms = ms;
   a.cmin = cmin;
   a.nch = (Ks + 31) / 32;
@@ -762,15 +759,14 @@ void filter_segments(int nq, int K, int fcap, int* nseg, int* cap_u) {
   *cap_u = std::max(8, fcap / *nseg);
 }
 
-cudaError_t launch_probe_filter(const void* q16, const void* c16, const float* c2, int nq, int K,
-                                int d, const float* ms, const float* thr, int nseg, int cap_u,
-                                int* cnt, int* cid, float* cval, cudaStream_t s) {
+cudaError_t launch_probe_filter(const void* q16, const void* c16, int nq, int K, int d,
+                                const float* ms, const float* thr, int nseg, int cap_u, int* cnt,
+                                int* cid, float* cval, cudaStream_t s) {
   FilterArgs a{};
-  a.c2 = c2;
   a.nq = nq;
   a.K = K;
   a.KC = f16_pitch(d) / 32;
-  a.d = d;
+  a.d = d + 2;
   a.ms = ms;
   a.thr = thr;
   a.nsplit = nseg / (filter_warps() / 4);
