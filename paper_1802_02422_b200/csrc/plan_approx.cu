@@ -846,6 +846,10 @@ int launch_plan_approx(const PlanArgs& a0, cudaStream_t s) {
   static const int wcap_env = getenv("GIVF_PLAN_WCAP") ? atoi(getenv("GIVF_PLAN_WCAP")) : 0;
   a.wcap_override = wcap_env > 0 ? std::min(wcap_env, PA_WCAP_RETRY) : 0;
   a.retry = 0;
+  // GIVF_PLAN_RETRY=0 (read per call; tests use it) sends overflowed
+  // windows straight to the exact planner
+  const char* re = getenv("GIVF_PLAN_RETRY");
+  if (re && atoi(re) == 0) a.n_overflow = nullptr;
   const PaSmem L(a.ix.d, a.P, (int64_t)a.P * a.ix.G, a.ix.max_gsize < 65536, a.wcap_override);
   auto kern = a.defer_rescore ? k_plan_approx<false> : k_plan_approx<true>;
   ensure_max_smem((const void*)kern, L.bytes);

@@ -636,14 +636,14 @@ struct FilterShape {
 };
 FilterShape filter_shape() {
   static const FilterShape fs = [] {
-    FilterShape f{2, 128};
+    FilterShape f{1, 256};
     if (const char* e = getenv("GIVF_FILTER_SHAPE")) {
       int m = 0, n = 0;
       if (sscanf(e, "%dx%d", &m, &n) == 2) f = FilterShape{m, n};
     }
     const bool ok = (f.mb == 2 && f.bn == 128) || (f.mb == 4 && f.bn == 64) ||
                     (f.mb == 1 && f.bn == 128) || (f.mb == 1 && f.bn == 256);
-    return ok ? f : FilterShape{2, 128};
+    return ok ? f : FilterShape{1, 256};
   }();
   return fs;
 }
@@ -699,8 +699,8 @@ cudaError_t launch_filter(const void* q16, const void* c16, int dp, FilterArgs a
     return cudaErrorInvalidValue;
   if (fs.mb == 4 && fs.bn == 64) return launch_filter_t<4, 64, MODE>(ma, mb, a, s);
   if (fs.mb == 1 && fs.bn == 128) return launch_filter_t<1, 128, MODE>(ma, mb, a, s);
-  if (fs.mb == 1 && fs.bn == 256) return launch_filter_t<1, 256, MODE>(ma, mb, a, s);
-  return launch_filter_t<2, 128, MODE>(ma, mb, a, s);
+  if (fs.mb == 2 && fs.bn == 128) return launch_filter_t<2, 128, MODE>(ma, mb, a, s);
+  return launch_filter_t<1, 256, MODE>(ma, mb, a, s);
 }
 
 }  // namespace

@@ -107,7 +107,8 @@ def default_mode_result():
     {"GIVF_GEMM_SPLIT": "3"},                      # probe GEMM work units: 3 slices per m-block
     {"GIVF_RS_SPLIT": "5"},                        # K4b: 5 CTAs per query
     {"GIVF_PLAN_WCAP": "8"},                       # K4 windows overflow: the 2048-entry retry pass
-    {"GIVF_PROBE": "fused"},                       # fused probe, 2 x 128 queries x 128 centroids
+    {"GIVF_PROBE": "fused"},                       # fused probe, 128 queries x 256 centroids
+    {"GIVF_PROBE": "fused", "GIVF_FILTER_SHAPE": "2x128"},  # 2 x 128 queries x 128 centroids
     {"GIVF_PROBE": "fused", "GIVF_FILTER_SHAPE": "4x64"},  # 4 x 128 queries x 64 centroids
     {"GIVF_PROBE": "fused", "GIVF_FILTER_SHAPE": "1x128"},  # 128 queries, rows shared by 2 warps
     {"GIVF_PROBE": "fused", "GIVF_FUSED_TARGET": "0"},  # threshold at ~128 survivors
@@ -177,7 +178,12 @@ def _sphere_index(seed=0, k=4096, d=96, g=8, m=16, on_sphere=1024):
         rotation=None, const_lo=-0.5, const_hi=0.5, grouping=True)
 
 
-def test_equidistant_regions_force_both_fallbacks():
+@pytest.mark.parametrize("retry", [True, False])
+def test_equidistant_regions_force_both_fallbacks(retry, monkeypatch):
+    """Tied group scores overflow the planner's certified window: with the
+    retry pass its 2048-entry window takes them; without it (GIVF_PLAN_RETRY=0)
+    the queries go to the exact planner."""
+    monkeypatch.setenv("GIVF_PLAN_RETRY", "1" if retry else "0")
     from oracle import search_oracle as so
     from paper_1802_02422_b200 import SearchParams, search_batch
     from paper_1802_02422_b200.device_index import DeviceIndex
@@ -193,8 +199,12 @@ def test_equidistant_regions_force_both_fallbacks():
     for i in range(q.shape[0]):
         assert_topk_equal(ids[i], d[i], wi[i], wd[i])
     counts = dev.fallback_counts()
-    print("fallbacks", counts)
-    assert counts["probe"] > 0 and counts["plan"] > 0
+    print("fallbacks", counts, "plan retries", dev.plan_retries())
+    assert counts["probe"] > 0
+    if retry:
+        assert dev.plan_retries() > 0
+    else:
+        assert dev.plan_retries() == 0 and counts["plan"] > 0
 
 
 @pytest.fixture(scope="module")
