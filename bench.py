@@ -604,8 +604,9 @@ def probe_roofline(w, nq, gemm_ms, peaks):
     """The probe GEMM stage against its bounds.  K >= 2^17 runs the fused
     probe (probe_fused.cu: one fp16 tcgen05 product per term, 2 K d flops per
     query; the epilogue reads every fp32 accumulator from TMEM once, K x 4
-    bytes per query -- the measured bound of that kernel); smaller K the
-    bf16x3 GEMM with fp16 score stores (probe_tc.cu)."""
+    bytes per query -- the measured bound of that kernel; the MMA runs over
+    round_up(d + 2, 32) columns: q.c plus the folded |c|^2 term, zero padded);
+    smaller K the bf16x3 GEMM with fp16 score stores (probe_tc.cu)."""
     if not gemm_ms:
         return None
     flops = 2.0 * w["k"] * w["d"] * nq
@@ -615,8 +616,10 @@ def probe_roofline(w, nq, gemm_ms, peaks):
                       if fused else "k_probe_gemm_tc (bf16x3 tcgen05 GEMM, fp16 score store)"),
            "unit": "TFLOP/s", "kernel_ms_per_step": gemm_ms,
            "achieved_tflops": flops / (gemm_ms / 1e3) / 1e12,
-           "mma_tflops": (flops if fused else flops * 10.0 / 3.0) / (gemm_ms / 1e3) / 1e12,
+           "mma_tflops": (flops * (-(-(w["d"] + 2) // 32) * 32) / w["d"] if fused
+                          else flops * 10.0 / 3.0) / (gemm_ms / 1e3) / 1e12,
            "peak_tflops_dense_bf16": peak}
+    out["frac_algorithmic"] = out["achieved_tflops"] / peak
     out["frac_of_tensor_peak"] = out["mma_tflops"] / peak
     if fused:
         out["tmem_read_GBps"] = 4.0 * w["k"] * nq / (gemm_ms / 1e3) / 1e9
