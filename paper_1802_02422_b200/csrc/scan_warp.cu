@@ -869,10 +869,31 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_lean(ScanArgs a) {
   const int nseg = a.nwork[b];
   __syncthreads();  // LUT, constants and bounds ready
 
-  // ---- this warp's positions
-  int tot = 0;
-  for (int i = lane; i < nseg; i += 32) tot += __ldg(&W[i].len);
-  tot = __reduce_add_sync(FULL, tot);
+  // ---- this warp's positions.  The lengths are summed window by window
+  // (32 segments, one coalesced load); lane l keeps the total of windows
+  // [l wpl, (l + 1) wpl), so the window holding the warp's first position is
+  // found by one scan instead of a walk from segment 0 (a chain of dependent
+  // loads: 11 % of the stall samples at configs[2]'s ~670 segments per query)
+  const int nwin = (nseg + 31) >> 5;
+  const int wpl = (nwin + 31) >> 5;  // windows per lane: 1 up to 1024 segments
+  int csum = 0;
+  {
+    int owner = 0, left = wpl;
+#pragma unroll 4
+    for (int t = 0; t < nwin; ++t) {
+      const int i = t * 32 + lane;
+      const int ws_t = __reduce_add_sync(FULL, i < nseg ? __ldg(&W[i].len) : 0);
+      if (lane == owner) csum += ws_t;
+      if (--left == 0) { ++owner; left = wpl; }
+    }
+  }
+  int cend = csum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULL, cend, o);
+    if (lane >= o) cend += y;
+  }
+  const int tot = __shfl_sync(FULL, cend, 31);
   const int pb = (int)((int64_t)tot * warp / SW_WARPS);
   const int pe = (int)((int64_t)tot * (warp + 1) / SW_WARPS);
   if (pb < pe) {
@@ -910,7 +931,10 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_lean(ScanArgs a) {
       const int sl = __popc(__ballot_sync(FULL, wend <= p));
       if (sl > 0) fill(ws + sl, __shfl_sync(FULL, wend, sl - 1));
     };
-    fill(0, 0);
+    {
+      const int src = __popc(__ballot_sync(FULL, cend <= pb));  // the lane whose windows hold pb
+      fill(src * wpl * 32, __shfl_sync(FULL, cend - csum, src));
+    }
     anchor(pb);
 
     struct Slot {

@@ -107,6 +107,7 @@ def test_k20_topk_and_stats(k20, nprobe, tau):
     from paper_1802_02422_b200 import SearchParams, search_batch
 
     arr, dev, q = k20
+    q = q[:40]  # the CPU oracle takes ~0.5 s per query at K = 2^20
     p = SearchParams(nprobe=nprobe, tau=tau, candidates=10_000)
     fb0 = dev.fallback_counts()
     ids, d, st = search_batch(dev, q, p, k=100)
@@ -131,8 +132,8 @@ def test_k20_probe_lists_bit_exact(k20):
 
     arr, dev, q = k20
     for nprobe in (32, 512):
-        regions, qc2 = probe(dev, q[:40], nprobe)
-        for i in range(40):
+        regions, qc2 = probe(dev, q[:16], nprobe)
+        for i in range(16):
             want_r, want_c = so.probe_exact(arr.centroids, q[i], nprobe)
             np.testing.assert_array_equal(regions[i], want_r)
             # float64 sums of 96 terms in another order: a few ulps
