@@ -126,7 +126,7 @@ GIVF_DEV float code_sum_xl(const CodeVec<M>& code, uint32_t lane_base, int x,
 
 // code_sum_xl with the per-step lane addresses precomputed: bs[s] =
 // lane_base ^ (s << 2), so each lookup is PRMT + LEA + LDS.
-template <int M>
+template <int M, int SHIFT = 7>  // SHIFT = log2(bytes between the rows of consecutive codes)
 GIVF_DEV float code_sum_xlb(const CodeVec<M>& code, const uint32_t (&bs)[M], int x,
                             const uint32_t (&xsel)[4]) {
   CodeVec<M> p;  // words by k ^ (x >> 2)
@@ -145,7 +145,7 @@ GIVF_DEV float code_sum_xlb(const CodeVec<M>& code, const uint32_t (&bs)[M], int
 #pragma unroll
   for (int s = 0; s < M; ++s) {
     const uint32_t byte = __byte_perm(p.w[s >> 2], 0, xsel[s & 3]);
-    const uint32_t addr = bs[s] + (byte << 7);
+    const uint32_t addr = bs[s] + (byte << SHIFT);
     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(e[s]) : "r"(addr));
   }
   return numpy_sum<M>(e);

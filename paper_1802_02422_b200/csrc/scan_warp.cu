@@ -809,8 +809,11 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_warp(ScanArgs a) {
 //    (segment ends inside it), then two shuffles fetch row and base;
 //  * the window re-anchors (one coalesced load of 32 work items and a warp
 //    scan) only when a batch runs past its last segment.
-template <int M, int D>
-__global__ void __launch_bounds__(SW_THREADS, 3) k_scan_lean(ScanArgs a) {
+// C = LUT copies: 32 / M makes every lookup conflict-free (one bank per
+// (copy, sub-quantizer)); fewer copies shrink the LUT (C M KB) at the price of
+// bank conflicts between lanes that share a copy.
+template <int M, int D, int C = 32 / M>
+__global__ void __launch_bounds__(SW_THREADS, C == 32 / M ? 3 : 4) k_scan_lean(ScanArgs a) {
   extern __shared__ __align__(16) unsigned char dsm[];
   const IndexView& ix = a.ix;
   float* lut = reinterpret_cast<float*>(dsm + SW_LUT);
@@ -841,9 +844,10 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_lean(ScanArgs a) {
     for (int it = 0; it < IT; ++it) {
       const int chunk = NC * (warp + it * SW_WARPS) + sub;
 #pragma unroll
-      for (int cc = 0; cc < NC; ++cc) {
-        float* dst = lut + (4 * chunk) * 32 + (cc ^ sub) * M + m;
-        dst[0] = v[it].x; dst[32] = v[it].y; dst[64] = v[it].z; dst[96] = v[it].w;
+      for (int cc = 0; cc < C; ++cc) {
+        constexpr int S = C * M;  // floats per code
+        float* dst = lut + (4 * chunk) * S + ((cc ^ sub) % C) * M + m;
+        dst[0] = v[it].x; dst[S] = v[it].y; dst[2 * S] = v[it].z; dst[3 * S] = v[it].w;
       }
     }
     ctab[tid] = cv;
@@ -942,9 +946,9 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_lean(ScanArgs a) {
       double base;
       bool ok;
     };
-    uint8_t* ring = dsm + sw_ring(M, true) + (size_t)warp * D * sw_slot(M);
+    uint8_t* ring = dsm + SW_LUT + (size_t)C * M * 1024 + 128 + (size_t)warp * D * sw_slot(M);
     const int xl_x = lane % M;
-    const uint32_t xl_base = smem_u32(lut) + (uint32_t)((lane / M) * M + xl_x) * 4u;
+    const uint32_t xl_base = smem_u32(lut) + (uint32_t)(((lane / M) % C) * M + xl_x) * 4u;
     uint32_t xl_sel[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) xl_sel[j] = 0x4440u | (uint32_t)(j ^ (xl_x & 3));
@@ -984,7 +988,9 @@ __global__ void __launch_bounds__(SW_THREADS, 3) k_scan_lean(ScanArgs a) {
       const CodeVec<M> code = smem_code<M>(src + lane * M);
       const uint32_t cw = reinterpret_cast<const uint32_t*>(src + 32 * M)[lane];
       const uint32_t cb = __byte_perm(cw, 0, 0x4440u | (cur.row & 3u));
-      const float ip = code_sum_xlb<M>(code, xl_bs, xl_x, xl_sel);
+      constexpr int SHIFT = C * M == 32 ? 7 : (C * M == 16 ? 6 : 5);
+      static_assert(C * M == 32 || C * M == 16 || C * M == 8, "row stride");
+      const float ip = code_sum_xlb<M, SHIFT>(code, xl_bs, xl_x, xl_sel);
       return (float)dadd(dsub(cur.base, 2.0 * (double)ip), (double)ctab[cb]);
     };
     auto consider = [&](const Slot& cur, float dist) {
@@ -1151,6 +1157,21 @@ static void launch_warp_md(const ScanArgs& a, cudaStream_t s) {
       if (scan_lean()) {
         // two ring slots: deeper rings (3, 4) cost a CTA per SM of shared
         // memory and measured slower (configs[2] shape: 1.20 -> 1.60 / 1.85 ms)
+        // default: half the conflict-free copies -- a 16 KB LUT and 64
+        // registers fit 4 CTAs per SM, and 32 resident warps beat the bank
+        // conflicts they cost (configs[2] shape: M = 16 1.19 -> 1.13 ms,
+        // M = 8 1.09 -> 0.99 ms; GIVF_SCAN_COPIES=full keeps 32 / M copies)
+        static const bool full = [] {
+          const char* e = getenv("GIVF_SCAN_COPIES");
+          return e && strcmp(e, "full") == 0;
+        }();
+        constexpr int CH = 16 / M;
+        if (!full) {
+          const size_t bytes = SW_LUT + (size_t)CH * M * 1024 + 128 + (size_t)SW_WARPS * 2 * sw_slot(M);
+          ensure_max_smem((const void*)k_scan_lean<M, 2, CH>, bytes);
+          k_scan_lean<M, 2, CH><<<a.nq, SW_THREADS, bytes, s>>>(a);
+          return;
+        }
         const size_t bytes = sw_bytes(M, 2, true, true, a.ix.d);
         ensure_max_smem((const void*)k_scan_lean<M, 2>, bytes);
         k_scan_lean<M, 2><<<a.nq, SW_THREADS, bytes, s>>>(a);

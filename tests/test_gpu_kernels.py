@@ -104,6 +104,7 @@ def default_mode_result():
     {"GIVF_CHUNK_QUERIES": "3"},                   # many small chunks (arena reuse)
     {"GIVF_SCAN_LUT": "plain"},                    # warp scan, [m][256] LUT (bank conflicts)
     {"GIVF_SCAN": "warp"},                         # block-wide segment windows (k_scan_warp)
+    {"GIVF_SCAN_COPIES": "full"},                  # 32 / M LUT copies, 3 CTAs/SM (conflict-free lookups)
     {"GIVF_GEMM_SPLIT": "3"},                      # probe GEMM work units: 3 slices per m-block
     {"GIVF_RS_SPLIT": "5"},                        # K4b: 5 CTAs per query
     {"GIVF_PLAN_WCAP": "8"},                       # K4 windows overflow: the 2048-entry retry pass
