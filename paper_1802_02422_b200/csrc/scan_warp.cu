@@ -830,28 +830,17 @@ __global__ void __launch_bounds__(SW_THREADS, C == 32 / M ? 3 : 4) k_scan_lean(S
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t lt_mask = (1u << lane) - 1u;
   const int k = a.k;
-  {
-    // prebuilt [m][256] -> interleaved copies (as in k_scan_warp)
-    constexpr int NC = 32 / M;
-    const float4* src = reinterpret_cast<const float4*>(a.luts + (int64_t)b * M * 256);
-    const int m = lane % M, sub = lane / M;
-    constexpr int IT = M * 64 / 32 / SW_WARPS;
-    float4 v[IT];
+  // prebuilt [m][256] -> interleaved copies (as in k_scan_warp).  The global
+  // loads are issued first and stored to shared memory only after the window
+  // setup below, whose own global loads then overlap them.
+  constexpr int NC = 32 / M;
+  const float4* src = reinterpret_cast<const float4*>(a.luts + (int64_t)b * M * 256);
+  const int m = lane % M, sub = lane / M;
+  constexpr int IT = M * 64 / 32 / SW_WARPS;
+  float4 v[IT];
 #pragma unroll
-    for (int it = 0; it < IT; ++it) v[it] = __ldg(src + m * 64 + NC * (warp + it * SW_WARPS) + sub);
-    const float cv = ix.ctab[tid];
-#pragma unroll
-    for (int it = 0; it < IT; ++it) {
-      const int chunk = NC * (warp + it * SW_WARPS) + sub;
-#pragma unroll
-      for (int cc = 0; cc < C; ++cc) {
-        constexpr int S = C * M;  // floats per code
-        float* dst = lut + (4 * chunk) * S + ((cc ^ sub) % C) * M + m;
-        dst[0] = v[it].x; dst[S] = v[it].y; dst[2 * S] = v[it].z; dst[3 * S] = v[it].w;
-      }
-    }
-    ctab[tid] = cv;
-  }
+  for (int it = 0; it < IT; ++it) v[it] = __ldg(src + m * 64 + NC * (warp + it * SW_WARPS) + sub);
+  const float cv = ix.ctab[tid];
   if (tid == 0) s_thr64 = kKeyPad;
   if (tid < SW_WARPS) s_tw[tid] = 0xffffffffu;
   const int k8 = (k + SW_WARPS - 1) / SW_WARPS;
@@ -871,7 +860,6 @@ __global__ void __launch_bounds__(SW_THREADS, C == 32 / M ? 3 : 4) k_scan_lean(S
   };
   const WorkItem* W = a.work + (int64_t)b * a.cap_w;
   const int nseg = a.nwork[b];
-  __syncthreads();  // LUT, constants and bounds ready
 
   // ---- this warp's positions.  The lengths are summed window by window
   // (32 segments, one coalesced load); lane l keeps the total of windows
@@ -900,7 +888,8 @@ __global__ void __launch_bounds__(SW_THREADS, C == 32 / M ? 3 : 4) k_scan_lean(S
   const int tot = __shfl_sync(FULL, cend, 31);
   const int pb = (int)((int64_t)tot * warp / SW_WARPS);
   const int pe = (int)((int64_t)tot * (warp + 1) / SW_WARPS);
-  if (pb < pe) {
+  const bool active = pb < pe;
+  {
     // register window: lane j = segment ws + j; wend = its end position,
     // wadj = first row - first position (row of position p = wadj + p)
     int ws = 0, wend = 0, wlast = 0;
@@ -935,11 +924,11 @@ __global__ void __launch_bounds__(SW_THREADS, C == 32 / M ? 3 : 4) k_scan_lean(S
       const int sl = __popc(__ballot_sync(FULL, wend <= p));
       if (sl > 0) fill(ws + sl, __shfl_sync(FULL, wend, sl - 1));
     };
-    {
+    if (active) {
       const int src = __popc(__ballot_sync(FULL, cend <= pb));  // the lane whose windows hold pb
       fill(src * wpl * 32, __shfl_sync(FULL, cend - csum, src));
+      anchor(pb);
     }
-    anchor(pb);
 
     struct Slot {
       uint32_t row;
@@ -1005,8 +994,22 @@ __global__ void __launch_bounds__(SW_THREADS, C == 32 / M ? 3 : 4) k_scan_lean(S
     };
     // D ring slots: D - 1 batches in flight while one is summed
     Slot sl[D];
+    if (active) {
 #pragma unroll
-    for (int i = 0; i < D - 1; ++i) map(pb + 32 * i, sl[i], i);
+      for (int i = 0; i < D - 1; ++i) map(pb + 32 * i, sl[i], i);
+    }
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int chunk = NC * (warp + it * SW_WARPS) + sub;
+#pragma unroll
+      for (int cc = 0; cc < C; ++cc) {
+        constexpr int S = C * M;  // floats per code
+        float* dst = lut + (4 * chunk) * S + ((cc ^ sub) % C) * M + m;
+        dst[0] = v[it].x; dst[S] = v[it].y; dst[2 * S] = v[it].z; dst[3 * S] = v[it].w;
+      }
+    }
+    ctab[tid] = cv;
+    __syncthreads();  // LUT, constants and bounds ready
     for (int p0 = pb; p0 < pe; p0 += 32 * D) {
       {  // adopt a tighter bound from the other warps
         uint32_t q[8];
