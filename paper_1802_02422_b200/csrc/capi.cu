@@ -1096,6 +1096,37 @@ int givf_index_create(const givf_index_desc* ds, int device, givf_index_t* out) 
       v.sc2 = sc2;
       v.Ks = Ks;
     }
+    // K3a's per-region packed neighbour rows (K G row bytes: 12.9 GB at
+    // configs[2]): taken when the fused probe will run (K >= 2^17 or forced)
+    // and the device keeps >= 32 GB free after it (workspace, caller's
+    // tensors); GIVF_PACK_NEIGHBORS=0 / 1 overrides
+    if (e == cudaSuccess && v.grouping && v.nbr) {
+      const char* pk = getenv("GIVF_PACK_NEIGHBORS");
+      const size_t pb = (size_t)K * v.G * f16_row_pitch(d) * 2, p2 = (size_t)K * v.G * 4;
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      const bool want = pk ? atoi(pk) != 0 : (use_fused(v) && fr > pb + p2 + ((size_t)32 << 30));
+      if (want) {
+        void* c16p = nullptr;
+        float* c2p = nullptr;
+        if (cudaMalloc(&c16p, pb) == cudaSuccess) {
+          if (cudaMalloc(&c2p, p2) == cudaSuccess) {
+            launch_pack_neighbor_rows(c16r, v.c2f, v.nbr, K, v.G, d, c16p, c2p, 0);
+            e = cudaDeviceSynchronize();
+            ix->allocs.push_back(c16p);
+            ix->allocs.push_back(c2p);
+            ix->dev_bytes += (int64_t)(pb + p2);
+            v.c16p = c16p;
+            v.c2p = c2p;
+          } else {
+            cudaFree(c16p);
+            cudaGetLastError();
+          }
+        } else {
+          cudaGetLastError();
+        }
+      }
+    }
   }
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ix->stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) {

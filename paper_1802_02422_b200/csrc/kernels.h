@@ -57,6 +57,12 @@ struct IndexView {
   float c16x;                 // 2^ec
   int c16T;                   // T
   const void* c16r;           // (K, f16_row_pitch(d)) the same fp16 coordinates, K3a's rows
+  // K3a's rows again, packed per region: chunk c (16 bytes) of neighbour j of
+  // region r at ((r DP8 + c) G + j) 16 bytes, DP8 = f16_row_pitch(d) / 8, so a
+  // warp reads a region's 64 rows as contiguous 512-byte lines instead of 64
+  // random rows; c2p = the neighbours' f32 |c|^2, (K, G).  Null: gather c16r.
+  const void* c16p;
+  const float* c2p;
   const void* s16;            // (Ks, dp) fp16 rows of a random centroid sample
   const float* sc2;           // (Ks) their f32 |c|^2
   int Ks;
@@ -97,6 +103,9 @@ float probe_f16_eps(int d);   // GEMM bound, units of cmax^2 + 2 |q| cmax
 float direct_f16_eps(int d);  // K3a-from-fp16-rows bound, same units
 // dp = row pitch (0: f16_pitch(d), with the |c|^2 columns; d rounded up
 // to 32: the coordinates only, for K3a's row reads)
+// c16p / c2p of IndexView from c16r, c2f and the neighbour ids
+void launch_pack_neighbor_rows(const void* c16r, const float* c2f, const int32_t* nbr, int K, int G,
+                               int d, void* c16p, float* c2p, cudaStream_t s);
 void launch_rows_f16(const float* x, const int32_t* ids, int64_t rows, int d, int e, int T,
                      const float* c2, void* out, float* c2out, cudaStream_t s, int dp = 0);
 __host__ __device__ inline int f16_row_pitch(int d) { return ((d + 31) / 32) * 32; }

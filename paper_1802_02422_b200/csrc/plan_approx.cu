@@ -97,7 +97,9 @@ __global__ void __launch_bounds__(PA_THREADS) k_plan_scores_approx(PlanArgs a) {
 // One warp per (query, probed region) as above, a lane per group.
 // DP8: 16-byte chunks read per row (d coordinates, zero-padded in the
 // query's shared copy); rows from ix.c16r (pitch f16_row_pitch(d))
-template <int DP8>
+// PK: rows from the per-region packed copy ix.c16p (contiguous 512-byte
+// lines per warp load) instead of gathered from ix.c16r
+template <int DP8, bool PK>
 __global__ void __launch_bounds__(PA_THREADS) k_plan_scores_direct(PlanArgs a) {
   __shared__ __align__(16) float qsm[PA_THREADS / 32][DP8 * 8];
   const IndexView& ix = a.ix;
@@ -128,16 +130,26 @@ __global__ void __launch_bounds__(PA_THREADS) k_plan_scores_direct(PlanArgs a) {
   const double oma_qc = dmul(dsub(1.0, al), qc);
   const double cx2 = 2.0 * (double)ix.c16x;
   const uint4* C16 = reinterpret_cast<const uint4*>(ix.c16r);
+  const uint4* P16 = reinterpret_cast<const uint4*>(ix.c16p);
   const int64_t rstride = f16_row_pitch(d) / 8;  // row pitch in 16-byte chunks
   const float4* q4 = reinterpret_cast<const float4*>(qs);
   for (int j = lane; j < G; j += 32) {
     const int64_t g = (int64_t)r * G + j;
-    const int n = __ldg(ix.nbr + g);
     const float m = __ldg(ix.norm + g);
-    const uint4* row = C16 + (int64_t)n * rstride;
     uint4 u[DP8];
+    float c2n;
+    if constexpr (PK) {  // the region's packed copy: lanes read consecutive 16-byte chunks
+      const uint4* row = P16 + (int64_t)r * DP8 * G + j;
 #pragma unroll
-    for (int c = 0; c < DP8; ++c) u[c] = __ldg(row + c);
+      for (int c = 0; c < DP8; ++c) u[c] = __ldg(row + (int64_t)c * G);
+      c2n = __ldg(ix.c2p + g);
+    } else {
+      const int n = __ldg(ix.nbr + g);
+      const uint4* row = C16 + (int64_t)n * rstride;
+#pragma unroll
+      for (int c = 0; c < DP8; ++c) u[c] = __ldg(row + c);
+      c2n = __ldg(ix.c2f + n);
+    }
     float acc0 = 0.f, acc1 = 0.f;
 #pragma unroll
     for (int c = 0; c < DP8; ++c) {
@@ -155,7 +167,7 @@ __global__ void __launch_bounds__(PA_THREADS) k_plan_scores_direct(PlanArgs a) {
       acc0 = fmaf(qb.z, h3.x, acc0);
       acc1 = fmaf(qb.w, h3.y, acc1);
     }
-    const double qs2 = dsub(dadd(q2, (double)__ldg(ix.c2f + n)), dmul(cx2, (double)(acc0 + acc1)));
+    const double qs2 = dsub(dadd(q2, (double)c2n), dmul(cx2, (double)(acc0 + acc1)));
     akey[j] = f32_key((float)dadd(dadd(oma_qc, dmul(al, qs2)), (double)m));
   }
 }
@@ -881,16 +893,46 @@ int launch_plan_approx(const PlanArgs& a0, cudaStream_t s) {
   return n + 1;
 }
 
+// (K, G) rows of c16r gathered into the per-region chunk-major layout
+__global__ void __launch_bounds__(256) k_pack_neighbor_rows(const uint4* __restrict__ c16r,
+                                                            const float* __restrict__ c2f,
+                                                            const int32_t* __restrict__ nbr, int64_t total,
+                                                            int G, int dp8, uint4* __restrict__ out,
+                                                            float* __restrict__ c2p) {
+  // one thread per (region, chunk, neighbour): out index == thread index
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const int j = (int)(i % G);
+  const int64_t rc = i / G;
+  const int c = (int)(rc % dp8);
+  const int64_t r = rc / dp8;
+  const int n = __ldg(nbr + r * G + j);
+  out[i] = __ldg(c16r + (int64_t)n * dp8 + c);
+  if (c == 0) c2p[r * G + j] = __ldg(c2f + n);
+}
+
+void launch_pack_neighbor_rows(const void* c16r, const float* c2f, const int32_t* nbr, int K, int G,
+                               int d, void* c16p, float* c2p, cudaStream_t s) {
+  const int dp8 = f16_row_pitch(d) / 8;
+  const int64_t total = (int64_t)K * dp8 * G;
+  k_pack_neighbor_rows<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(
+      reinterpret_cast<const uint4*>(c16r), c2f, nbr, total, G, dp8, reinterpret_cast<uint4*>(c16p), c2p);
+}
+
 int launch_plan_scores(const PlanArgs& a, cudaStream_t s) {
   const int64_t warps = (int64_t)a.nq * a.P;
   const int per = PA_THREADS / 32;
   const unsigned grid = (unsigned)((warps + per - 1) / per);
   if (a.direct) {
     switch ((a.ix.d + 31) / 32) {  // 32-coordinate chunks of a row
-      case 1: k_plan_scores_direct<4><<<grid, PA_THREADS, 0, s>>>(a); break;
-      case 2: k_plan_scores_direct<8><<<grid, PA_THREADS, 0, s>>>(a); break;
-      case 3: k_plan_scores_direct<12><<<grid, PA_THREADS, 0, s>>>(a); break;
-      default: k_plan_scores_direct<16><<<grid, PA_THREADS, 0, s>>>(a); break;
+      case 1: a.ix.c16p ? k_plan_scores_direct<4, true><<<grid, PA_THREADS, 0, s>>>(a)
+                        : k_plan_scores_direct<4, false><<<grid, PA_THREADS, 0, s>>>(a); break;
+      case 2: a.ix.c16p ? k_plan_scores_direct<8, true><<<grid, PA_THREADS, 0, s>>>(a)
+                        : k_plan_scores_direct<8, false><<<grid, PA_THREADS, 0, s>>>(a); break;
+      case 3: a.ix.c16p ? k_plan_scores_direct<12, true><<<grid, PA_THREADS, 0, s>>>(a)
+                        : k_plan_scores_direct<12, false><<<grid, PA_THREADS, 0, s>>>(a); break;
+      default: a.ix.c16p ? k_plan_scores_direct<16, true><<<grid, PA_THREADS, 0, s>>>(a)
+                         : k_plan_scores_direct<16, false><<<grid, PA_THREADS, 0, s>>>(a); break;
     }
     return 1;
   }
