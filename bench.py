@@ -668,7 +668,8 @@ def run_reference(args, w):
         "metric": "queries/sec at fixed recall@10 (synthetic, B200)",
         "value": v, "unit": "queries/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-        "higher_is_better": True, "scaling": "strong" if args.layout == "lists" else "weak",
+        "higher_is_better": True,
+        "scaling": "strong" if args.layout == "lists" and int(os.environ.get("WORLD_SIZE", "1")) > 1 else "weak",
         "vs_baseline": None,
         "dtype": "f32/f64 (u8 codes)", "data": f"synthetic, noise={args.noise}",
         "config": dict(config_of(args, w, w["nq"]), queries_per_step_timed=per,
