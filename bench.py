@@ -577,6 +577,7 @@ def run_ours(args, w):
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
         },
         "roofline_probe": probe_roofline(w, nq, gemm_ms / prof_steps if gemm_n else None, peaks),
+        "roofline_plan": plan_roofline(w, nq, step_stage_ms.get("plan_scores"), hbm_peak),
         "stage_ms_per_step": step_stage_ms,
         "gpu_launches": int(launches),
         "fallback_queries_per_step": fallbacks,
@@ -598,6 +599,23 @@ def run_ours(args, w):
                                 "sample": f"{done} of the {nq} step queries in {wall:.1f}s "
                                           f"(oracle port of search.py, exact probe, fork x{cpu.cores})"}
     return line
+
+
+def plan_roofline(w, nq, ms, hbm_peak):
+    """K3a (approximate group scores, the pruning's input) against HBM.  With
+    the fused probe (K >= 2^17) it reads the fp16 rows of the P L neighbour
+    centroids of the probed regions, 32 ceil(d / 32) x 2 bytes each, from the
+    per-region packed copy; below that it gathers P L 2-byte scores from the
+    score matrix (sector-bound, no byte roofline stated)."""
+    if not ms or w["k"] < (1 << 17):
+        return None
+    row = -(-w["d"] // 32) * 32 * 2
+    nbytes = float(nq) * w["nprobe"] * w["l"] * row
+    gbs = nbytes / (ms / 1e3) / 1e9
+    return {"kernel": "k_plan_scores_direct (K3a: fp16 neighbour rows, packed per region)",
+            "bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
+            "algorithmic_bytes_per_step": nbytes, "kernel_ms_per_step": ms,
+            "note": "peak = measured copy bandwidth (read + write); a read-only stream can exceed it"}
 
 
 def probe_roofline(w, nq, gemm_ms, peaks):
