@@ -258,6 +258,8 @@ k_probe_filter(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
     const int slot = e >> 2;
     uint32_t acc = 0, acc_phase = 0;
     const float kInf = __int_as_float(0x7f800000);
+    const uint32_t f0 = (uint32_t)(slot * CW);
+    const uint32_t coff = (f0 / CPM) * BN + (f0 % CPM) * 32;  // TMEM column of the warp's first chunk
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int g = u % groups, sp = u / groups;
       const int t0 = sp * per_split, t1 = min(n_tiles, t0 + per_split);
@@ -280,14 +282,20 @@ k_probe_filter(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
         mbar_wait(&sm->tm_full[acc], acc_phase);
         fence_after();
         const uint32_t tq = tmem + ((uint32_t)(quarter * 32) << 16) + acc * TC;
+        // chunk c's TMEM column: a per-warp constant (coff) + a compile-time
+        // step when the warp's chunks lie in one m-block, so the tile loop
+        // carries no division
         auto chunk_addr = [&](int c) {
-          const int f = slot * CW + c;
+          if constexpr (CW <= CPM && CPM % CW == 0) return tq + coff + (uint32_t)c * 32u;
+          const uint32_t f = (uint32_t)(slot * CW + c);
           return tq + (f / CPM) * BN + (f % CPM) * 32;
         };
-        // columns past K (the last tile): -inf, never a maximum or a survivor
+        // columns past K (only a tile that crosses K): -inf, never a maximum
+        // or a survivor
+        const bool last = col0 + BN > a.K;
         auto clip = [&](uint32_t* r, int cc) {
           const int c0 = col0 + cc * 32;
-          if (c0 + 32 > a.K) {
+          if (last && c0 + 32 > a.K) {
 #pragma unroll
             for (int i = 0; i < 32; ++i)
               if (c0 + i >= a.K) r[i] = __float_as_uint(-kInf);
