@@ -314,11 +314,11 @@ ProbeShape probe_shape(int K, int P) {
 }
 
 // Fused-probe sizes for a sample of Ks of the K centroids: aim the
-// threshold at ~3P + 128 survivors (the sample's j-th smallest chunk minimum
+// threshold at ~2P + 128 survivors (the sample's j-th smallest chunk minimum
 // estimates the ftarget-th smallest score; with j >= 16 the chance that it
 // falls below the P-th is negligible), list capacity 6x that.
 void fused_shape(ProbeShape* s, int K, int Ks, int P) {
-  static const int mul = getenv("GIVF_FUSED_TARGET") ? atoi(getenv("GIVF_FUSED_TARGET")) : 3;
+  static const int mul = getenv("GIVF_FUSED_TARGET") ? atoi(getenv("GIVF_FUSED_TARGET")) : 2;
   const int64_t target = std::min<int64_t>(K, (int64_t)mul * P + 128);
   s->ftarget = (int)target;
   s->fj = (int)std::max<int64_t>(1, (target * Ks + K - 1) / K);
@@ -1058,7 +1058,7 @@ int givf_index_create(const givf_index_desc* ds, int device, givf_index_t* out) 
     v.c16T = T;
     const int dp = f16_pitch(d);
     // sample: every centroid up to 8192, else K/16 (at most 2^16); its
-    // j-th smallest chunk minimum aims the threshold at ~3P + 128 survivors
+    // j-th smallest chunk minimum aims the threshold at ~2P + 128 survivors
     // (j >= 20 at nprobe 64: a sample that lands below the P-th smallest
     // score of all K is a > 5 sigma event, and costs only a fallback)
     const int Ks = K <= 8192 ? K : std::min(1 << 16, std::max(8192, K / 16));
