@@ -539,6 +539,9 @@ k_probe_pick(const int* __restrict__ cnt, const int* __restrict__ cid,
              const float* __restrict__ thr, const float* __restrict__ q2, float cmax,
              float eps_scale, int P, int cap2, int* __restrict__ cand, int* __restrict__ cand_n,
              float* __restrict__ theta) {
+  constexpr int PICK_SM = 2048;
+  __shared__ uint32_t skey[PICK_SM];
+  __shared__ int sid[PICK_SM];
   __shared__ uint32_t hist[256];
   __shared__ uint32_t red[40];
   __shared__ uint32_t s_bin, s_k;
@@ -561,17 +564,43 @@ k_probe_pick(const int* __restrict__ cnt, const int* __restrict__ cid,
     if (tid == 0) { cand_n[b] = 0; theta[b] = -__int_as_float(0x7f800000); }
     return;
   }
-  // a_P: the P-th smallest survivor (radix select over the segments)
+  // The usual few hundred survivors are first gathered into shared memory
+  // (a thread per segment: the segments hold 0-3 entries each, so a warp per
+  // segment left 31 lanes idle on every pass); the radix passes and the
+  // compaction then run a thread per survivor.
+  const bool packed = total <= PICK_SM;
+  if (packed) {
+    uint32_t all;
+    uint32_t o = block_exclusive_scan((uint32_t)tot, red, &all);
+    for (int sg = tid; sg < nseg; sg += blockDim.x) {
+      const int c = cb[sg];
+      for (int i = 0; i < c; ++i) {
+        const int64_t at = base + (int64_t)sg * cap_u + i;
+        skey[o] = f32_key(cval[at]);
+        sid[o] = cid[at];
+        ++o;
+      }
+    }
+    __syncthreads();
+  }
+  // a_P: the P-th smallest survivor (radix select)
   uint32_t prefix = 0, mask = 0;
   int k = P;
   for (int shift = 24; shift >= 0; shift -= 8) {
     hist[tid] = 0;
     __syncthreads();
-    for (int sg = warp; sg < nseg; sg += nw) {
-      const int c = cb[sg];
-      for (int i = lane; i < c; i += 32) {
-        const uint32_t key = f32_key(cval[base + (int64_t)sg * cap_u + i]);
+    if (packed) {
+      for (int i = tid; i < total; i += blockDim.x) {
+        const uint32_t key = skey[i];
         if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+      }
+    } else {
+      for (int sg = warp; sg < nseg; sg += nw) {
+        const int c = cb[sg];
+        for (int i = lane; i < c; i += 32) {
+          const uint32_t key = f32_key(cval[base + (int64_t)sg * cap_u + i]);
+          if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+        }
       }
     }
     __syncthreads();
@@ -593,13 +622,22 @@ k_probe_pick(const int* __restrict__ cnt, const int* __restrict__ cid,
                      1e-12 * ((double)cmax + qn) * ((double)cmax + qn) +
                      1.2e-7 * (fabs((double)aP) + 4.0 * (double)cmax * qn + (double)q2[b]);
   const float tb = fminf(thr[b], (float)((double)aP + 2.02 * eps));
-  for (int sg = warp; sg < nseg; sg += nw) {
-    const int c = cb[sg];
-    for (int i = lane; i < c; i += 32) {
-      const int64_t at = base + (int64_t)sg * cap_u + i;
-      if (cval[at] < tb) {
+  if (packed) {
+    for (int i = tid; i < total; i += blockDim.x) {
+      if (key_f32(skey[i]) < tb) {
         const int p = atomicAdd(&s_n, 1);
-        if (p < cap2) cand[(int64_t)b * cap2 + p] = cid[at];
+        if (p < cap2) cand[(int64_t)b * cap2 + p] = sid[i];
+      }
+    }
+  } else {
+    for (int sg = warp; sg < nseg; sg += nw) {
+      const int c = cb[sg];
+      for (int i = lane; i < c; i += 32) {
+        const int64_t at = base + (int64_t)sg * cap_u + i;
+        if (cval[at] < tb) {
+          const int p = atomicAdd(&s_n, 1);
+          if (p < cap2) cand[(int64_t)b * cap2 + p] = cid[at];
+        }
       }
     }
   }
@@ -659,9 +697,22 @@ FilterShape filter_shape() {
 // Work units = (MB x 128 queries, slice of the centroid tiles), slice-major;
 // the slice count minimises the busiest CTA's tiles (+1 tile of overhead
 // per unit for its A block).
-// epilogue warps: 8 (16, four per lane quarter with two chunks each,
-// measured 3.53 ms against 2.85 at configs[2]; removed)
-int filter_warps() { return 8; }
+// epilogue warps of the 1 x 256 shape: 16 (four per TMEM lane quarter, two
+// 32-column chunks each).  The epilogue paces this kernel and is bound by
+// its own dependent-issue latency: with 8 warps (two per scheduler) each
+// tile took ~2000 cycles against an MMA floor of 896; four per scheduler
+// bring the GEMM from 2.27 to 1.94 ms (configs[2] shape).  An earlier 16-warp
+// variant, before the |c|^2 fold and the early buffer release, had measured
+// slower.  GIVF_FILTER_WARPS=8 keeps eight; the other shapes always use 8.
+int filter_warps() {
+  static const int w = [] {
+    const char* e = getenv("GIVF_FILTER_WARPS");
+    const FilterShape fs = filter_shape();
+    if (!(fs.mb == 1 && fs.bn == 256)) return 8;
+    return e && atoi(e) == 8 ? 8 : 16;
+  }();
+  return w;
+}
 
 int filter_nsplit(int nq, int K, int MB, int BN) {
   const int groups = (nq + MB * pf::BM - 1) / (MB * pf::BM);
@@ -694,6 +745,9 @@ cudaError_t launch_filter_w(const CUtensorMap& ma, const CUtensorMap& mb, const 
 template <int MB, int BN, int MODE>
 cudaError_t launch_filter_t(const CUtensorMap& ma, const CUtensorMap& mb, const FilterArgs& a,
                             cudaStream_t s) {
+  if constexpr (MB == 1 && BN == 256) {
+    if (filter_warps() == 16) return launch_filter_w<MB, BN, MODE, 16>(ma, mb, a, s);
+  }
   return launch_filter_w<MB, BN, MODE, 8>(ma, mb, a, s);
 }
 

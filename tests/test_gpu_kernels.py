@@ -114,6 +114,7 @@ def default_mode_result():
     {"GIVF_PROBE": "fused", "GIVF_FILTER_SHAPE": "1x128"},  # 128 queries, rows shared by 2 warps
     {"GIVF_PROBE": "fused", "GIVF_FUSED_TARGET": "0"},  # threshold at ~128 survivors
     {"GIVF_PROBE": "fused", "GIVF_PACK_NEIGHBORS": "0"},  # K3a gathers rows instead of the packed copy
+    {"GIVF_PROBE": "fused", "GIVF_FILTER_WARPS": "8"},  # 8 epilogue warps instead of 16
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_execution_modes_agree(env_over, default_mode_result):
     """Every tuning knob changes how the work is scheduled, never the result:
