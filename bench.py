@@ -622,8 +622,8 @@ def probe_roofline(w, nq, gemm_ms, peaks):
     """The probe GEMM stage against its bounds.  K >= 2^17 runs the fused
     probe (probe_fused.cu: one fp16 tcgen05 product per term, 2 K d flops per
     query; the epilogue reads every fp32 accumulator from TMEM once, K x 4
-    bytes per query -- the measured bound of that kernel; the MMA runs over
-    round_up(d + 2, 32) columns: q.c plus the folded |c|^2 term, zero padded);
+    bytes per query; the MMA runs ceil((d + 2) / 16) k-steps of 16 columns:
+    q.c plus the folded |c|^2 term, zero padded);
     smaller K the bf16x3 GEMM with fp16 score stores (probe_tc.cu)."""
     if not gemm_ms:
         return None
@@ -634,7 +634,7 @@ def probe_roofline(w, nq, gemm_ms, peaks):
                       if fused else "k_probe_gemm_tc (bf16x3 tcgen05 GEMM, fp16 score store)"),
            "unit": "TFLOP/s", "kernel_ms_per_step": gemm_ms,
            "achieved_tflops": flops / (gemm_ms / 1e3) / 1e12,
-           "mma_tflops": (flops * (-(-(w["d"] + 2) // 32) * 32) / w["d"] if fused
+           "mma_tflops": (flops * (-(-(w["d"] + 2) // 16) * 16) / w["d"] if fused
                           else flops * 10.0 / 3.0) / (gemm_ms / 1e3) / 1e12,
            "peak_tflops_dense_bf16": peak}
     out["frac_algorithmic"] = out["achieved_tflops"] / peak
